@@ -1,0 +1,401 @@
+"""Pins for the fp64 oracle.  Each test checks an oracle step against
+something other than itself: brute force, a closed form, a printed paper value, or an
+invariant.  Pin ids P1-P15 follow SURVEY §8(c) / DESIGN.md.  CPU only."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from gen import get_config
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")
+
+
+def _rand(n, seed):
+    return np.random.default_rng(seed).standard_normal(n)
+
+
+# ----------------------------------------------------------------------------------- window
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_window_unit_energy_and_peak(name):
+    """R1: sum g^2 = 1 within 2e-8 for L = 8 sigma windows (truncation tail), g[c] = (pi s^2)^-1/4
+    (P:L55), g symmetric about c, g' antisymmetric with g'[c] = 0."""
+    cfg = get_config(name)
+    g, gd, c = O.gaussian_window(cfg.L, cfg.sigma)
+    assert abs(np.sum(g * g) - 1.0) < 2e-8
+    assert g[c] == pytest.approx((np.pi * cfg.sigma ** 2) ** -0.25, rel=1e-15)
+    h = min(c, cfg.L - 1 - c)
+    assert np.allclose(g[c - h:c], g[c + h:c:-1], rtol=0, atol=1e-18)
+    assert np.allclose(gd[c - h:c], -gd[c + h:c:-1], rtol=0, atol=1e-18)
+    assert gd[c] == 0.0
+
+
+def test_window_derivative_is_derivative():
+    """g' is the derivative of g: compare with a 4th-order central difference of a
+    window evaluated at shifted centres (calculus, not the formula re-typed)."""
+    L, s, h = 129, 11.3, 1e-3
+    g, gd, c = O.gaussian_window(L, s, center=64)
+    t = np.arange(L) - 64.0
+
+    def gc(tt):   # P:L55 continuous Gaussian, sigma in samples
+        return (np.pi * s * s) ** -0.25 * np.exp(-tt * tt / (2 * s * s))
+    fd = (-gc(t + 2 * h) + 8 * gc(t + h) - 8 * gc(t - h) + gc(t - 2 * h)) / (12 * h)
+    assert np.max(np.abs(fd - gd)) < 1e-9
+    assert np.max(np.abs(gc(t) - g)) < 1e-15
+
+
+def test_frame_count():
+    """F = floor((N-1)/H) + 1 (R4)."""
+    assert O.frame_count(4096, 1) == 4096
+    assert O.frame_count(1 << 20, 8) == 131072
+    assert O.frame_count(10, 3) == 4      # frames at 0,3,6,9
+    assert O.frame_count(9, 3) == 3
+
+
+# ----------------------------------------------------------------------------------- STFT
+@pytest.mark.parametrize("L,nfft,hop", [(9, 16, 1), (8, 16, 3), (9, 32, 3), (8, 32, 1), (16, 16, 2), (1, 16, 5)])
+def test_P1_stft_matches_direct_eq8(L, nfft, hop):
+    """P1: Eq. 9 via FFT (phase factor, zero padding) equals the brute-force Eq. 8 sum, for g
+    and g', including frames hanging off both ends of the record."""
+    N = 64
+    x = _rand(N, 10 + L + nfft + hop)
+    g, gd, c = O.gaussian_window(L, max(1.0, L / 4))
+    F = O.frame_count(N, hop)
+    frames = np.arange(F)
+    bins = np.arange(nfft)
+    for w in (g, gd):
+        S = O.stft(x, w, c, hop, nfft, full=True)
+        D = O.stft_direct(x, w, c, hop, nfft, frames, bins)
+        assert np.linalg.norm(S - D) <= 1e-12 * max(1e-300, np.linalg.norm(D))
+
+
+def test_P2_hermitian_symmetry():
+    """P2: real input => S[m, N_f - k] = conj S[m, k]."""
+    x = _rand(300, 2)
+    g, _, c = O.gaussian_window(33, 6.0)
+    S = O.stft(x, g, c, 7, 64, full=True)
+    k = np.arange(1, 64)
+    assert np.max(np.abs(S[:, 64 - k] - np.conj(S[:, k]))) < 1e-12 * np.max(np.abs(S))
+
+
+def test_P3_impulse_response():
+    """P3: unit impulse at n0 => |S[m,k]| = |g[n0 - m H + c]| for every k."""
+    N, n0, hop = 200, 77, 3
+    x = np.zeros(N)
+    x[n0] = 1.0
+    g, gd, c = O.gaussian_window(31, 5.0)
+    S = O.stft(x, g, c, hop, 32)
+    F = O.frame_count(N, hop)
+    for m in range(F):
+        j = n0 - m * hop + c
+        expect = abs(g[j]) if 0 <= j < len(g) else 0.0
+        assert np.allclose(np.abs(S[m]), expect, rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("L,nfft,hop", [(33, 64, 1), (33, 64, 8), (64, 64, 16), (65, 128, 20), (32, 32, 16)])
+def test_P4_stft_round_trip(L, nfft, hop):
+    """P4: Eq. 10-11 synthesis with the d[n] division inverts Eq. 9 exactly."""
+    N = 600
+    x = _rand(N, L * hop)
+    g, _, c = O.gaussian_window(L, L / 6.0)
+    S = O.stft(x, g, c, hop, nfft, full=True)
+    xr = O.stft_inverse(S, g, c, hop, nfft, N)
+    assert np.max(np.abs(xr - x)) < 1e-12 * np.max(np.abs(x))
+
+
+def test_coverage_rule():
+    """d[n] > 0 on [0, N) iff H_t <= L and the last frame reaches N-1: (F-1) H - c + L >= N.
+    With H = L = 32 and N = 600 the tail 592..599 is uncovered (SST_E_COVERAGE in the ABI)."""
+    g, _, c = O.gaussian_window(32, 5.0)
+    d = O.frame_diagonal(g, c, 32, 600)
+    assert np.all(d[:592] > 0) and np.all(d[592:] == 0)
+    d = O.frame_diagonal(g, c, 32, 592)
+    assert np.all(d > 0)
+
+
+def test_frame_diagonal_interior_and_edges():
+    """d[n]: interior value is the H-periodic sum of g^2 over taps j = n + c (mod H);
+    edges checked against an explicit frame loop."""
+    g, _, c = O.gaussian_window(40, 7.0)
+    N, hop = 300, 6
+    d = O.frame_diagonal(g, c, hop, N)
+    F = O.frame_count(N, hop)
+    ref = np.zeros(N)
+    for m in range(F):
+        for j in range(40):
+            n = m * hop - c + j
+            if 0 <= n < N:
+                ref[n] += g[j] ** 2
+    assert np.allclose(d, ref, rtol=0, atol=1e-15)
+    for n in range(60, 200):
+        per = np.sum(g[(n + c) % hop::hop] ** 2)
+        assert d[n] == pytest.approx(per, rel=1e-14)
+    # windowed evaluation agrees with the full one
+    assert np.allclose(O.frame_diagonal(g, c, hop, N, 50, 120), d[50:120], rtol=0, atol=1e-16)
+
+
+# ----------------------------------------------------------------------------------- IF / targets
+def _c1_window():
+    cfg = get_config("C1")
+    g, gd, c = O.gaussian_window(cfg.L, cfg.sigma)
+    return cfg, g, gd, c
+
+
+def test_P5_tone_squeezes_into_its_bin():
+    """P5: noiseless 100 Hz tone on the C1 grid (df = 0.25 Hz): >= 99.5% of |T|^2 in bin 400,
+    and omega_hat = 400 bins within 0.05 bin for |k - 400| <= 2 sigma_f (Eq. 13 on a tone)."""
+    cfg, g, gd, c = _c1_window()
+    t = np.arange(cfg.N) / cfg.fs
+    x = np.cos(2 * np.pi * 100.0 * t)
+    T, S, Sd, l = O.sst_forward(x, g, gd, c, 1, cfg.nfft, cfg.fs, 0.0, 512.0, 1, 0.0, debug=True)
+    P = np.abs(T) ** 2
+    assert P[:, 400].sum() / P.sum() >= 0.995
+    _, r, fhat = O.if_estimate(S, Sd, cfg.nfft, 0.0)
+    sf = cfg.nfft / (2 * np.pi * cfg.sigma)
+    k = np.arange(S.shape[1])
+    sel = np.abs(k - 400) <= 2 * sf
+    for m in (1000, 2048, 3000):
+        assert np.max(np.abs(fhat[m, sel] - 400.0)) < 0.05
+        # RF sign (Eq. 36): negative above the ridge, positive below, ~0 at it (the
+        # residual ~5e-4 bin is the truncated window's sidelobe of the negative-frequency image)
+        assert np.all(r[m, 401:400 + int(sf)] < 0) and np.all(r[m, 400 - int(sf):400] > 0)
+        assert abs(r[m, 400]) < 2e-3
+        # linear RF near the ridge: r ~ -(k - 400) (Eq. 44 limit df -> 0)
+        assert np.allclose(r[m, 390:411], -(np.arange(390, 411) - 400.0), atol=0.02)
+
+
+def test_P6_chirp_if_closed_form_and_ridge():
+    """P6: Gaussian-window IF estimate of a linear chirp (rate c): omega_hat(xi) = w0 + (xi - w0)
+    c^2 s^4/(1 + c^2 s^4) (closed form, derived in DESIGN.md §4); ridge argmax within 1 bin of the
+    analytic IF on interior frames."""
+    cfg, g, gd, c = _c1_window()
+    t = np.arange(cfg.N) / cfg.fs
+    x = np.cos(2 * np.pi * (200.0 * t + 25.0 * t * t))
+    T, S, Sd, l = O.sst_forward(x, g, gd, c, 1, cfg.nfft, cfg.fs, 0.0, 512.0, 1, 0.0, debug=True)
+    _, _, fhat = O.if_estimate(S, Sd, cfg.nfft, 0.0)
+    cr = 2 * np.pi * 50.0 / cfg.fs ** 2
+    kappa = (cr * cfg.sigma ** 2) ** 2 / (1 + (cr * cfg.sigma ** 2) ** 2)
+    assert kappa == pytest.approx(0.0860, abs=5e-5)
+    sf = cfg.nfft / (2 * np.pi * cfg.sigma)
+    k = np.arange(S.shape[1])
+    for m in range(600, 3500, 100):
+        IF = (200.0 + 50.0 * m / cfg.fs) / cfg.df
+        sel = np.abs(k - IF) <= 2 * sf
+        pred = IF + (k[sel] - IF) * kappa
+        assert np.max(np.abs(fhat[m, sel] - pred)) < 0.05
+        assert abs(np.argmax(np.abs(T[m])) - IF) <= 1.0
+
+
+def test_P7_chirp_reconstruction_closed_form():
+    """P7: Eq. 25-26 on that chirp reconstructs Re{(1 + i c s^2)^(-1/2) e^{i phi}} (amplitude 0.978,
+    phase -0.149 rad at c s^2 = 0.307), matching 'error grows with |f'|'."""
+    cfg, g, gd, c = _c1_window()
+    t = np.arange(cfg.N) / cfg.fs
+    phi = 2 * np.pi * (200.0 * t + 25.0 * t * t)
+    x = np.cos(phi)
+    T = O.sst_forward(x, g, gd, c, 1, cfg.nfft, cfg.fs, 0.0, 512.0, 1, 0.0)
+    xr = O.sst_inverse(T, g, c, 1, cfg.nfft, 1, 0, cfg.N)
+    cs2 = 2 * np.pi * 50.0 / cfg.fs ** 2 * cfg.sigma ** 2
+    pred = np.real((1 + 1j * cs2) ** -0.5 * np.exp(1j * phi))
+    s = slice(600, cfg.N - 600)
+    e_closed = np.linalg.norm(xr[s] - pred[s]) / np.linalg.norm(pred[s])
+    e_x = np.linalg.norm(xr[s] - x[s]) / np.linalg.norm(x[s])
+    assert e_closed < 0.01
+    assert e_x > 0.10
+
+
+def test_P8_tone_reconstruction_sqrt2():
+    """P8: tone at H_t = H_f = 1: x_hat = x (C_d / sqrt 2) up to far-tail truncation; relative L2
+    <= 2e-4 with sqrt 2 (Eq. 24) and closer with the discrete constant C_d (R15)."""
+    cfg, g, gd, c = _c1_window()
+    t = np.arange(cfg.N) / cfg.fs
+    x = np.cos(2 * np.pi * 100.0 * t)
+    T = O.sst_forward(x, g, gd, c, 1, cfg.nfft, cfg.fs, 0.0, 512.0, 1, 0.0)
+    s = slice(cfg.L, cfg.N - cfg.L)
+    xr = O.sst_inverse(T, g, c, 1, cfg.nfft, 1, 0, cfg.N)
+    xd = O.sst_inverse(T, g, c, 1, cfg.nfft, 1, 0, cfg.N, constant="discrete")
+    e2 = np.linalg.norm(xr[s] - x[s]) / np.linalg.norm(x[s])
+    ed = np.linalg.norm(xd[s] - x[s]) / np.linalg.norm(x[s])
+    closed = abs(O.discrete_constant(g, c) / np.sqrt(2.0) - 1.0)
+    assert closed == pytest.approx(5.92e-5, rel=0.01)
+    assert e2 <= 2e-4 and ed < e2
+    assert abs(e2 - closed) < 5e-5
+
+
+def test_P9_conservation_and_P10_linearity():
+    """P9: per frame, sum_l T[m,l] = sum of the kept S[m,k].  P10:
+    squeeze is linear in S for a fixed map; omega_hat is invariant to scaling x (gamma = 0)."""
+    x = _rand(2000, 9)
+    g, gd, c = O.gaussian_window(64, 10.0)
+    T, S, Sd, l = O.sst_forward(x, g, gd, c, 5, 128, 1000.0, 0.0, 500.0, 3, 0.0, debug=True)
+    kept = np.where(l >= 0, S, 0)
+    assert np.allclose(T.sum(axis=1), kept.sum(axis=1), rtol=1e-12, atol=1e-12)
+    S2 = O.stft(_rand(2000, 10), g, c, 5, 128)
+    lhs = O.squeeze(2.5 * S - 1.5j * S2, l, T.shape[1])
+    rhs = 2.5 * O.squeeze(S, l, T.shape[1]) - 1.5j * O.squeeze(S2, l, T.shape[1])
+    assert np.allclose(lhs, rhs, rtol=1e-12, atol=1e-12)
+    Sa, Sda = O.stft(3.7 * x, g, c, 5, 128), O.stft(3.7 * x, gd, c, 5, 128)
+    _, _, f1 = O.if_estimate(S, Sd, 128, 0.0)
+    _, _, f2 = O.if_estimate(Sa, Sda, 128, 0.0)
+    assert np.allclose(f1, f2, rtol=1e-10, atol=1e-10)
+
+
+def test_targets_match_eq28_membership_bruteforce():
+    """Eq. 28/29 membership written out (loop over l) equals the floor formula, on random
+    estimates and on exact half-bin ties (ties go to the upper bin, R10), for subdivided
+    selective bands and the full band."""
+    rng = np.random.default_rng(4)
+    for (k1, Nr, z) in [(0, 16, 1), (5, 7, 3), (2, 10, 4), (0, 8, 8)]:
+        B = z * Nr
+        fh = rng.uniform(k1 - 2, k1 + Nr + 2, size=(6, 40))
+        if z & (z - 1) == 0:                                # ties exactly representable
+            ties = k1 + (np.arange(-1, B + 1) + 0.5) / z    # exact half-bin positions
+            fh[5, :len(ties[:40])] = ties[:40]
+        mask = rng.uniform(size=fh.shape) > 0.1
+        a = O.targets(fh, mask, k1, B, z)
+        b = O.targets_bruteforce(fh, mask, float(k1), float(k1 + Nr), Nr, z)
+        assert np.array_equal(a, b)
+
+
+def test_P11_full_band_equals_eq14():
+    """P11: band [0, fs/2], z = 1 equals the full-band reassignment of Eq. 14 on the
+    non-negative bins: T[m, l] = sum_k S[m,k] over |omega_hat - xi[l]| <= dxi/2, written as a loop."""
+    x = _rand(400, 11)
+    g, gd, c = O.gaussian_window(31, 5.0)
+    nfft, hop, fs = 32, 4, 32.0
+    T, S, Sd, l = O.sst_forward(x, g, gd, c, hop, nfft, fs, 0.0, fs / 2, 1, 0.0, debug=True)
+    _, _, fhat = O.if_estimate(S, Sd, nfft, 0.0)
+    ref = np.zeros_like(T)
+    for m in range(S.shape[0]):
+        for k in range(S.shape[1]):
+            for ll in range(nfft // 2):
+                if abs(fhat[m, k] - ll) <= 0.5 and (ll == nfft // 2 - 1 or not abs(fhat[m, k] - (ll + 1)) <= 0.5):
+                    ref[m, ll] += S[m, k]
+                    break
+    assert np.allclose(T, ref, rtol=1e-12, atol=1e-12)
+
+
+def test_P12_hop_subsampling_identity():
+    """P12: frames are independent, so T at H_t = h equals rows 0, h, 2h, ... of T at H_t = 1."""
+    x = _rand(700, 12)
+    g, gd, c = O.gaussian_window(48, 8.0)
+    T1 = O.sst_forward(x, g, gd, c, 1, 64, 128.0, 10.0, 40.0, 2, 1e-3)
+    for h in (2, 7, 16):
+        Th = O.sst_forward(x, g, gd, c, h, 64, 128.0, 10.0, 40.0, 2, 1e-3)
+        assert np.array_equal(Th, T1[::h])
+
+
+def test_truncate_flag_restricts_sources():
+    """R12: with truncation only source bins k in [k1, k2) contribute."""
+    x = _rand(900, 13)
+    g, gd, c = O.gaussian_window(64, 9.0)
+    T, S, Sd, l = O.sst_forward(x, g, gd, c, 3, 64, 64.0, 8.0, 20.0, 2, 0.0, truncate=True, debug=True)
+    k = np.arange(S.shape[1])
+    assert np.all(l[:, (k < 8) | (k >= 20)] == -1)
+    Tf, _, _, lf = O.sst_forward(x, g, gd, c, 3, 64, 64.0, 8.0, 20.0, 2, 0.0, debug=True)
+    inside = (k >= 8) & (k < 20)
+    assert np.array_equal(l[:, inside], lf[:, inside])
+
+
+# ----------------------------------------------------------------------------------- inverse
+@pytest.mark.parametrize("zoom,f1,f2,lo,hi", [(1, 0.0, 512.0, 150.0, 300.0), (2, 0.0, 512.0, 150.0, 300.0),
+                                               (3, 0.0, 256.0, 80.0, 100.0), (4, 48.0, 448.0, 200.0, 300.0)])
+def test_P15_inverse_machinery_is_stft_synthesis(zoom, f1, f2, lo, hi):
+    """P15: feeding the un-squeezed positive-frequency STFT into Eq. 25-26 (zero-stuffed at
+    l = z (k - k1)) and undoing the 1/sqrt 2 gives back the Eq. 10-11 synthesis, i.e. x on the
+    interior, for tones >= 9 sigma_f inside [f1, f2) (plus a DC term when f1 = 0) and a window whose
+    truncation edge is e^-20.  Pins the mirror, phase, x z scaling, DC handling and OLA."""
+    fs, N, nfft, hop = 1024.0, 3000, 256, 5
+    g, _, c = O.gaussian_window(129, 10.0)
+    t = np.arange(N) / fs
+    rng = np.random.default_rng(zoom)
+    x = sum(rng.uniform(0.2, 1.0) * np.cos(2 * np.pi * f * t + rng.uniform(0, 6.28))
+            for f in rng.uniform(lo, hi, size=5))
+    if f1 == 0.0:
+        x = x + 0.3
+    S = O.stft(x, g, c, hop, nfft)
+    df = fs / nfft
+    k1, k2 = int(round(f1 / df)), int(round(f2 / df))
+    T = np.zeros((S.shape[0], zoom * (k2 - k1)), dtype=complex)
+    T[:, ::zoom] = S[:, k1:k2]
+    xr = O.sst_inverse(T, g, c, hop, nfft, zoom, k1, N) * np.sqrt(2.0)
+    s = slice(129, N - 129)
+    assert np.max(np.abs(xr[s] - x[s])) < 1e-9 * np.max(np.abs(x))
+
+
+@pytest.mark.parametrize("zoom,f1,f2", [(1, 0.0, 512.0), (2, 0.0, 512.0), (4, 50.0, 150.0), (8, 75.0, 125.0)])
+def test_P14_selective_subdivided_inverse(zoom, f1, f2):
+    """P14: at fs = 1024, N_f = 1024, H_t = 4, a 100 Hz tone reconstructs within 2e-4 through the
+    selective / subdivided path (bin z k1 + l on a z N_f grid, conj mirror, x z, 1/sqrt 2, / d)."""
+    fs, N, nfft, hop = 1024.0, 8192, 1024, 4
+    g, gd, c = O.gaussian_window(257, 32.0)
+    t = np.arange(N) / fs
+    x = np.cos(2 * np.pi * 100.0 * t)
+    T = O.sst_forward(x, g, gd, c, hop, nfft, fs, f1, f2, zoom, 0.0)
+    xr = O.sst_inverse(T, g, c, hop, nfft, zoom, int(round(f1 * nfft / fs)), N)
+    s = slice(300, N - 300)
+    assert np.linalg.norm(xr[s] - x[s]) / np.linalg.norm(x[s]) <= 2e-4
+
+
+def test_inverse_window_matches_full():
+    """sst_inverse over an output window from the frames covering it equals the full result."""
+    x = _rand(1500, 14)
+    g, gd, c = O.gaussian_window(100, 15.0)
+    hop, nfft = 10, 128
+    T = O.sst_forward(x, g, gd, c, hop, nfft, 1.0, 0.0, 0.5, 2, 0.0)
+    full = O.sst_inverse(T, g, c, hop, nfft, 2, 0, 1500)
+    n0, n1 = 400, 700
+    fb = max(0, (n0 + c - 100) // hop)
+    fe = min(T.shape[0], (n1 - 1 + c) // hop + 1)
+    part = O.sst_inverse(T[fb:fe], g, c, hop, nfft, 2, 0, 1500, frame_begin=fb, n0=n0, n1=n1)
+    assert np.allclose(part, full[n0:n1], rtol=0, atol=1e-13)
+
+
+# ----------------------------------------------------------------------------------- analysis
+def test_paper_printed_values():
+    """Golden values printed in the paper (tests/golden/paper_values.json, each with its citation)."""
+    gv = json.load(open(GOLDEN))
+    v = gv["sigma_f_hz"]
+    assert abs(O.sigma_f_hz(v["sigma_s"]) - v["value"]) <= v["tol"]
+    v = gv["effective_support_hz"]
+    assert abs(6 * O.sigma_f_hz(v["sigma_s"]) - v["value"]) <= v["tol"]
+    v = gv["hf_bound_eq38"]
+    assert int(np.ceil(O.hf_bound_eq38(v["N"], v["sigma_s"], v["fs"]))) == v["value"]
+    v = gv["hf_bound_eq46"]
+    assert int(round(O.hf_bound_eq46(v["N"], v["sigma_s"], v["fs"]))) == v["value"]
+    v = gv["hf_critical_sec51"]
+    assert int(round(O.hf_bound_eq38(v["N"], v["sigma_s"], v["fs"]))) == v["value"]
+    v = gv["hf_sec51"]
+    assert int(round(v["N"] / v["nfft"])) == v["value"]
+    v = gv["dfz_sec51_hz"]
+    assert abs(O.band_grid(v["fs"], v["nfft"], 0.0, v["fs"] / 2, v["zoom"])["dfz_hz"] - v["value"]) <= v["tol"]
+    v = gv["half_interval_hf70_hz"]
+    assert abs(v["hf"] * v["fs"] / v["N"] / 2 - v["value"]) <= v["tol"]
+    v = gv["hop_sec51"]
+    assert int(round((1 - v["overlap"]) * v["L"])) == v["value"]
+
+
+def test_renyi_entropy_closed_forms():
+    """Eq. 32: uniform over n cells -> log2 n (any alpha); a single cell -> 0; scale invariant."""
+    for n in (4, 37, 1024):
+        assert O.renyi_entropy(np.ones(n) * 3.0) == pytest.approx(np.log2(n), rel=1e-12)
+    P = np.zeros(50)
+    P[7] = 2.0
+    assert O.renyi_entropy(P) == pytest.approx(0.0, abs=1e-12)
+    P = np.random.default_rng(1).uniform(size=100)
+    assert O.renyi_entropy(P) == pytest.approx(O.renyi_entropy(5 * P), rel=1e-12)
+
+
+def test_band_grid_snapping():
+    """R9: band edges snap to the coarse grid; off-grid edges are an error; B = z N_r."""
+    b = O.band_grid(51200.0, 2048, 0.0, 4000.0, 4)
+    assert (b["k1"], b["k2"], b["Nr"], b["B"]) == (0, 160, 160, 640)
+    b = O.band_grid(44100.0, 8192, 44100.0 / 8192 * 1282, 44100.0 / 8192 * 1765, 8)
+    assert (b["k1"], b["k2"], b["B"]) == (1282, 1765, 3864)
+    with pytest.raises(ValueError):
+        O.band_grid(1000.0, 100, 3.0, 50.0, 1)
+    with pytest.raises(ValueError):
+        O.band_grid(1000.0, 100, 0.0, 600.0, 1)
