@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark of the fast downsampled SST hot path (forward + approximate inverse) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C3] [--impl ours|reference]
+
+One step = the whole hot path over one record: sst_forward of every
+frame (band output T in HBM) then the inverse (Eq. 25-26) back to x_hat.  At N=1 the workload
+is BASELINE.json configs[2] (C3, aero-engine run-up, forward + inverse; DESIGN.md §8 says why).
+For N>1 (torchrun, one rank per GPU, NCCL) the record is time-sharded with per-rank work fixed
+(weak scaling: the run-up record is N x longer); ranks exchange the inverse's OLA seams.
+
+Prints ONE JSON line on rank 0.  ``--impl reference`` times the fp64 CPU oracle instead
+(the reference arm of this tier), on the box's host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from gen import generate, get_config  # noqa: E402
+
+WORKLOAD_DESC = {
+    "C1": "C1 tiny standard SST (100 Hz tone + chirp + noise), N=4096, fs=1024, L=257, H_t=1, N_f=4096, full band, z=1",
+    "C2": "C2 spindle-like, N=2^20, fs=25.6k, L=1024, H_t=8, N_f=1024, band 0-2 kHz, z=2",
+    "C3": "C3 aero-engine run-up, N=2^24, fs=51.2k, L=2048, H_t=16, N_f=2048, band 0-4 kHz, z=4, fwd+inverse",
+    "C4": "C4 long record, N=2^28, fs=51.2k, L=4096, H_t=32, N_f=4096, band 0-6.4 kHz, z=2",
+    "C5": "C5 dense grid, N=2^26, fs=25.6k, L=512, H_t=4, N_f=512, full band, z=8",
+}
+FP32_PEAK_NOTE = "148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz (B200_PROFILING.md unit counts, clocks.max.sm)"
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), float(mp.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return 6650.0, 1965.0, "fallback"
+
+
+def algorithmic_counts(cfg):
+    """Per-frame algorithmic work."""
+    K = cfg.nfft // 2 + 1
+    B = cfg.bins
+    zN = cfg.zoom * cfg.nfft
+    fwd_flops = 5.0 * cfg.nfft * math.log2(cfg.nfft) + 2.0 * cfg.L + 20.0 * K
+    inv_flops = 2.5 * zN * math.log2(zN) + 2.0 * cfg.L + 8.0 * B
+    fwd_bytes = 4.0 * cfg.hop + 8.0 * B
+    inv_bytes = 8.0 * B + 4.0 * cfg.hop
+    return fwd_flops, inv_flops, fwd_bytes, inv_bytes
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------------------------- reference arm
+def _oracle_window_record(cfg, nfr):
+    """A local record for timing the oracle on ``nfr`` consecutive frames from the middle of the
+    workload: local sample j = global sample f0*H + j, so local frame m = global frame f0 + m."""
+    f0 = cfg.frames // 3
+    lo = f0 * cfg.hop
+    hi = min(cfg.N, lo + nfr * cfg.hop + cfg.L)
+    return generate(cfg, lo, hi).astype(np.float64)
+
+
+def _oracle_step(O, cfg, xl, g, gd, c, gamma, nfr):
+    """Forward of nfr frames + inverse of the interior half (output window fully covered)."""
+    T = O.sst_forward(xl, g, gd, c, cfg.hop, cfg.nfft, cfg.fs, cfg.f1, cfg.f2, cfg.zoom, gamma,
+                      frames=np.arange(nfr))
+    n0, n1 = (nfr // 4) * cfg.hop, (3 * nfr // 4) * cfg.hop
+    O.sst_inverse(T, g, c, cfg.hop, cfg.nfft, cfg.zoom, cfg.k1, xl.size, frame_begin=0, n0=n0, n1=n1)
+    return nfr * cfg.hop
+
+
+def run_reference(args, cfg):
+    """The fp64 numpy oracle, as it stands, on a bounded sample of the workload per step."""
+    import oracle as O
+    g, gd, c = O.gaussian_window(cfg.L, cfg.sigma)
+    nfr = args.ref_frames
+    xl = _oracle_window_record(cfg, nfr)
+    gamma = 1e-6 * float(np.sum(g)) * float(np.abs(xl).max())
+    for _ in range(args.warmup):
+        _oracle_step(O, cfg, xl, g, gd, c, gamma, nfr)
+    t0 = time.perf_counter()
+    samples = 0
+    for _ in range(args.steps):
+        samples += _oracle_step(O, cfg, xl, g, gd, c, gamma, nfr)
+    dt = time.perf_counter() - t0
+    value = samples / dt / 1e6
+    sample_desc = (f"{nfr} consecutive frames of {cfg.name} per step (forward of all {nfr} frames + inverse of "
+                   f"the interior half), single-process numpy fp64")
+    line = {
+        "impl": "reference", "metric": "SST fwd+inverse input Msamples/s", "value": value, "unit": "Msamples/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD_DESC[cfg.name], "sample_frames": nfr},
+        "cpu_baseline": {"value": value, "unit": "Msamples/s", "cores": 1, "kind": "oracle", "sample": sample_desc},
+        "e2e": {"value": value, "unit": "Msamples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, seconds_target=12.0):
+    """Oracle timed on a bounded sample (rank 0, N=1 only): repeated 128-frame chunks for about
+    ``seconds_target`` seconds; Msamples/s = frames * H_t / time."""
+    import oracle as O
+    g, gd, c = O.gaussian_window(cfg.L, cfg.sigma)
+    nfr = 128
+    xl = _oracle_window_record(cfg, nfr)
+    gamma = 1e-6 * float(np.sum(g)) * float(np.abs(xl).max())
+    done = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds_target:
+        done += _oracle_step(O, cfg, xl, g, gd, c, gamma, nfr)
+    dt = time.perf_counter() - t0
+    return {"value": done / dt / 1e6, "unit": "Msamples/s", "cores": 1, "kind": "oracle",
+            "sample": f"{done // cfg.hop} frames of {cfg.name} in chunks of {nfr} consecutive frames (forward + "
+                      f"inverse of each chunk's interior half), single-process numpy fp64, {dt:.1f} s"}
+
+
+# ------------------------------------------------------------------------------------- our arm
+def run_ours(args, cfg_base):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2003_07065_b200 as P
+    from paper_2003_07065_b200 import dist as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = cfg_base.with_(N=cfg_base.N * world) if world > 1 else cfg_base   # weak scaling
+    g, gd = P.gaussian_window(cfg.L, cfg.sigma)
+    c = cfg.L // 2
+    sh = D.shard(cfg.N, cfg.hop, cfg.L, c, world, rank)
+
+    x_host = generate(cfg, sh.span_lo, sh.span_hi)
+    gamma = 1e-6 * float(np.sum(g)) * D.max_over_ranks(float(np.abs(x_host).max()), dev)   # reading R6
+    plan = P.Plan(cfg.N, cfg.fs, cfg.L, cfg.sigma, cfg.hop, cfg.nfft, cfg.f1, cfg.f2, cfg.zoom,
+                  gamma=gamma, device=local)
+    x = torch.from_numpy(x_host).to(dev)
+    T = torch.empty((sh.frames, plan.bins), dtype=torch.complex64, device=dev)
+    span = sh.span_hi - sh.span_lo
+    y = torch.empty(span if world > 1 else cfg.N, dtype=torch.float32, device=dev)
+    do_inv = True
+    stream = torch.cuda.current_stream(dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(record=None):
+        e0, e1, e2 = (ev(), ev(), ev()) if record is not None else (None, None, None)
+        if e0: e0.record(stream)
+        plan.forward(x, sh.frame_begin, sh.frame_end, x_off=sh.span_lo, out=T)
+        if e1: e1.record(stream)
+        if do_inv:
+            if world == 1:
+                plan.inverse(T, out=y)
+            else:
+                y.zero_()
+                plan.inverse_accumulate(T, sh.frame_begin, sh.frame_end, y, y_off=sh.span_lo)
+                D.exchange_seams(y, sh, cfg.hop, c)
+                plan.inverse_finalize(D.own_slice(y, sh), y_off=sh.own_lo)
+        if e2: e2.record(stream)
+        if record is not None:
+            record.append((e0, e1, e2))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    recs = []
+    with ClockSampler(local) as clk:
+        t_start, t_end = ev(), ev()
+        t_start.record(stream)
+        for _ in range(args.steps):
+            step(recs)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+    ms_local = t_start.elapsed_time(t_end)
+    fwd_ms = sum(a.elapsed_time(b) for a, b, _ in recs) / len(recs)
+    inv_ms = sum(b.elapsed_time(cc) for _, b, cc in recs) / len(recs)
+    ms_total = D.max_over_ranks(ms_local, dev)
+    ms_step = ms_total / args.steps
+    total_samples = cfg.N
+    value = total_samples / (ms_step * 1e-3) / 1e6
+    coeffs_per_s = cfg.frames * cfg.bins / (ms_step * 1e-3)
+
+    # ---- end to end through the public API with host buffers (pinned), per step
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.from_numpy(x_host).pin_memory()
+        own = sh.own_hi - sh.own_lo
+        yh = torch.empty(own, dtype=torch.float32).pin_memory()
+        for it in range(args.warmup + args.steps):
+            if it == args.warmup:
+                torch.cuda.synchronize()
+                if world > 1:
+                    dist.barrier()
+                a0 = ev()
+                a0.record(stream)
+            x.copy_(xh, non_blocking=True)
+            step()
+            src = y if world == 1 else D.own_slice(y, sh)
+            yh.copy_(src[:own] if world == 1 else src, non_blocking=True)
+        a1 = ev()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = D.max_over_ranks(a0.elapsed_time(a1), dev) / args.steps
+        e2e = {"value": total_samples / (e2e_ms * 1e-3) / 1e6, "unit": "Msamples/s",
+               "h2d_bytes_per_step": int(xh.numel() * 4 * world), "d2h_bytes_per_step": int(cfg.N * 4),
+               "ms_per_step": e2e_ms}
+
+    hbm_gbs, sm_max_mhz, peak_src = _peaks()
+    fwd_fl, inv_fl, fwd_b, inv_b = algorithmic_counts(cfg)
+    nfr_rank = sh.frames
+    fp32_peak = 148 * 128 * 2 * sm_max_mhz * 1e6 / 1e12   # TFLOP/s
+    fwd_tf = fwd_fl * nfr_rank / (fwd_ms * 1e-3) / 1e12
+    inv_tf = inv_fl * nfr_rank / (inv_ms * 1e-3) / 1e12
+    fwd_gbs = fwd_b * nfr_rank / (fwd_ms * 1e-3) / 1e9
+    inv_gbs = inv_b * nfr_rank / (inv_ms * 1e-3) / 1e9
+    dom = "forward" if fwd_ms >= inv_ms else "inverse"
+    ach = fwd_tf if dom == "forward" else inv_tf
+    roofline = {"bound": "alu", "kernel": f"sst_{dom}", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": ach / fp32_peak, "traffic": None,
+                "peak_source": f"derived: {FP32_PEAK_NOTE}",
+                "hbm": {"forward_gbs": fwd_gbs, "inverse_gbs": inv_gbs, "peak_gbs": hbm_gbs,
+                        "forward_frac": fwd_gbs / hbm_gbs, "inverse_frac": inv_gbs / hbm_gbs,
+                        "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json)"},
+                "alu": {"forward_tflops": fwd_tf, "inverse_tflops": inv_tf,
+                        "forward_frac": fwd_tf / fp32_peak, "inverse_frac": inv_tf / fp32_peak},
+                "per_frame": {"fwd_flops": fwd_fl, "inv_flops": inv_fl, "fwd_bytes": fwd_b, "inv_bytes": inv_b}}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg_base, args.cpu_seconds)
+    launches_per_step = 1 + (2 if world == 1 else 3)
+    if rank == 0:
+        line = {
+            "metric": "SST fwd+inverse input Msamples/s", "value": value, "unit": "Msamples/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD_DESC[cfg_base.name], "N_per_gpu": cfg_base.N, "N_total": cfg.N,
+                       "frames": cfg.frames, "bins": cfg.bins, "T_bytes": cfg.frames * cfg.bins * 8,
+                       "parallelism": f"time-shard x{world}",
+                       "l2": "inputs larger than L2 (T = %.1f GiB written and read per step)" % (
+                           cfg.frames * cfg.bins * 8 / 2 ** 30)},
+            "tf_coeffs_per_s": coeffs_per_s,
+            "fwd_ms": fwd_ms, "inv_ms": inv_ms,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            "gpu_launches": launches_per_step * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOAD_DESC))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-frames", type=int, default=256)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
+        args.warmup = 3
+    cfg = get_config(args.workload)
+    if args.impl == "reference":
+        if int(os.environ.get("RANK", "0")) != 0:
+            return
+        run_reference(args, cfg)
+        return
+    run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .configs import get_config
+from .configs import Config, get_config
 
 BLOCK = 1 << 16
 _STREAM_PARAMS, _STREAM_NOISE, _STREAM_IMPULSE = 0, 1, 2
@@ -155,9 +155,15 @@ _NOMINAL_POWER = {
 _SNR_DB = {"C2": 10.0, "C3": 5.0, "C4": 5.0, "C5": 20.0}
 
 
-def clean_components(name: str, start: int = 0, stop: int | None = None):
-    """Noise-free parts of a config's signal on [start, stop), fp64 (dict name -> array)."""
-    cfg = get_config(name)
+def _cfg(name_or_cfg):
+    return name_or_cfg if isinstance(name_or_cfg, Config) else get_config(name_or_cfg)
+
+
+def clean_components(name, start: int = 0, stop: int | None = None):
+    """Noise-free parts of a config's signal on [start, stop), fp64 (dict name -> array).
+    ``name`` is a config name or a Config (e.g. C3 with N scaled for weak scaling)."""
+    cfg = _cfg(name)
+    name = cfg.name
     stop = cfg.N if stop is None else stop
     t = np.arange(start, stop, dtype=np.float64) / cfg.fs
     if name == "C1":
@@ -173,16 +179,18 @@ def clean_components(name: str, start: int = 0, stop: int | None = None):
     raise KeyError(name)
 
 
-def generate(name: str, start: int = 0, stop: int | None = None, dtype=np.float32) -> np.ndarray:
+def generate(name, start: int = 0, stop: int | None = None, dtype=np.float32) -> np.ndarray:
     """Samples [start, stop) of config ``name``'s record (default: whole record) as ``dtype``.
-    fp32 is the GPU input; the oracle takes the same fp32 samples upcast to fp64."""
-    cfg = get_config(name)
+    ``name`` is a config name or a Config.  fp32 is the GPU input; the oracle takes the same
+    fp32 samples upcast to fp64."""
+    cfg = _cfg(name)
+    name = cfg.name
     stop = cfg.N if stop is None else stop
     if not (0 <= start <= stop <= cfg.N):
         raise ValueError("range outside record")
     if start == stop:
         return np.zeros(0, dtype=dtype)
-    parts = clean_components(name, start, stop)
+    parts = clean_components(cfg, start, stop)
     x = sum(parts.values())
     if name == "C1":
         x = x + 0.1 * _noise(cfg.seed, start, stop, "white")

@@ -1,0 +1,182 @@
+/*
+ * sst.h -- C ABI of the B200-native fast downsampled SST
+ *          (He & Cao, "Fast implementation of synchrosqueezing transform based on
+ *           downsampling for large-scale vibration signal analysis", arXiv 2003.07065).
+ *
+ * Citations: P:Lnnn = PAPER.md line nnn (section / equation); Rnn = reading in DESIGN.md §3.
+ *
+ * The problem, as the paper states it: given a real signal x
+ * sampled at fs, a window g and its derivative g', a time hop H_t and a DFT
+ * length N_f (Eq. 7-9), a band [f1, f2] with subdivision z (Eq. 27-29) and a threshold gamma
+ * (Eq. 13), return the synchrosqueezed plane T on the band grid, and invert T back to x
+ * (Eq. 25-26).
+ *
+ * Conventions (every entry point):
+ *  - Return an sst_status.  Nothing aborts, exits or prints.  sst_last_error() gives a
+ *    message for the last failing call on a plan (or, with plan == NULL, on this thread).
+ *  - Ownership: the caller owns every buffer passed in.  "device" pointers are CUDA device
+ *    memory on the plan's device; "host" pointers are ordinary host memory.  The plan owns
+ *    its copies of the window taps, twiddle tables and scratch.
+ *  - Complex arrays are complex64: interleaved float pairs (re, im), row-major.
+ *  - Asynchrony: compute calls enqueue work on `stream` (a cudaStream_t passed as void*;
+ *    NULL = legacy default stream) and return without synchronising.  Launch errors are
+ *    returned synchronously as SST_E_CUDA; asynchronous faults surface on the caller's
+ *    next synchronisation.
+ *  - Threading: a plan is bound to one device and is not thread-safe.
+ *  - Frames: F = floor((N-1)/H_t) + 1; frame m is centred on sample m*H_t and covers samples
+ *    [m*H_t - c, m*H_t - c + L) (Eq. 8, R4); samples outside [0, N) read as zero.
+ */
+#ifndef SST_H
+#define SST_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SST_ABI_VERSION 1
+
+typedef enum {
+    SST_OK = 0,
+    SST_E_INVALID_ARGUMENT = 1, /* bad parameter, pointer, size or range                       */
+    SST_E_COVERAGE = 2,         /* some n in [0,N) has frame diagonal d[n] = 0 (R20)   */
+    SST_E_UNSUPPORTED = 3,      /* valid per the paper, outside this library (N_f, B limits)   */
+    SST_E_CUDA = 4,             /* a CUDA runtime call or launch failed                        */
+    SST_E_OUT_OF_MEMORY = 5,    /* device allocation failed                                    */
+    SST_E_INTERNAL = 6
+} sst_status;
+
+/* sst_params.flags */
+enum {
+    SST_GAMMA_RELATIVE = 1u,    /* gamma is relative: gamma_abs = gamma * max|S| (Eq. 13, R6).
+                                   sst_forward computes max|S| over its own frames first (one
+                                   extra FFT pass) unless sst_plan_set_absmax() gave a device
+                                   scalar (e.g. a global max all-reduced over ranks).           */
+    SST_SOURCE_TRUNCATE = 2u,   /* only source bins k in [k1, k2) are reassigned (R12)  */
+    SST_DETERMINISTIC = 4u,     /* reserved: bitwise-reproducible accumulation order            */
+    SST_DISCRETE_CONSTANT = 8u  /* inverse divides by C_d = g[c] sum g / sum g^2 instead of
+                                   sqrt 2 (Eq. 24, R15)                                         */
+};
+
+typedef struct {
+    int64_t n;            /* N: samples of the whole record (also when sharded), >= 1          */
+    double fs;            /* sample rate, Hz, > 0                                              */
+    int32_t win_len;      /* L >= 1 taps                                                       */
+    int32_t win_center;   /* c in [0, L); -1 -> floor(L/2) (P:L85 for odd L, R3 for even L)     */
+    const double* g;      /* HOST [L]: analysis window g (copied into the plan)                */
+    const double* gd;     /* HOST [L]: g' = dg/dn per sample (R1) (copied)             */
+    double sigma;         /* Gaussian sigma in samples for the packing scale alpha = sigma*sqrt 2
+                             (R18); <= 0 -> alpha = sqrt(sum g^2 / sum g'^2)                  */
+    int32_t hop;          /* H_t >= 1                                                  */
+    int32_t nfft;         /* N_f: power of two, L <= N_f <= N                   */
+    double f1, f2;        /* band [f1, f2) in Hz, 0 <= f1 < f2 <= fs/2, on the grid fs/N_f (R9)*/
+    int32_t zoom;         /* subdivision z >= 1 (Eq. 28-29)                                    */
+    double gamma;         /* threshold on |S^g| (Eq. 13, R6), >= 0; absolute unless RELATIVE  */
+    uint32_t flags;       /* SST_* flags                                                       */
+} sst_params;
+
+typedef struct {
+    int64_t n;            /* N                                                                 */
+    int64_t frames;       /* F = floor((N-1)/H_t) + 1                                          */
+    int32_t bins;         /* B = z * N_r output bins per frame (Eq. 28-29, half-open R10)     */
+    int32_t k1, k2;       /* snapped band edges in coarse bins (R9), N_r = k2 - k1             */
+    int32_t nfft, zoom, hop, center, win_len;
+    int32_t src_bins;     /* N_f/2 + 1 source bins per frame (R7)                              */
+    double fs;
+    double f0_hz;         /* frequency of output bin 0 = k1 * df                               */
+    double df_hz;         /* coarse spacing fs / N_f (Eq. 12)                                  */
+    double dfz_hz;        /* output spacing df / z (Eq. 28)                                    */
+    double gamma_abs;     /* absolute gamma in use (0 until known when RELATIVE)              */
+    double alpha;         /* g' packing scale (R18)                                            */
+    double hf;            /* H_f = N / N_f                                             */
+    double hf_bound;      /* Eq. 38 bound 3N/(4 pi sigma fs) (sigma in s), 0 if sigma unknown  */
+} sst_layout;
+
+typedef struct sst_plan sst_plan;
+
+/* ---------------------------------------------------------------- host-only helpers -------- */
+
+/* Unit-energy Gaussian window and its analytic derivative, sigma in samples (R1):
+ *   g[j]  = (pi sigma^2)^(-1/4) exp(-(j-c)^2 / (2 sigma^2)),  g'[j] = -((j-c)/sigma^2) g[j].
+ * center < 0 -> c = floor(L/2).  g, gd: HOST arrays of L doubles, written.  No GPU needed.
+ * Errors: SST_E_INVALID_ARGUMENT for L < 1, sigma <= 0 / non-finite, c outside [0,L), NULL. */
+sst_status sst_gaussian_window(int32_t L, double sigma_samples, int32_t center, double* g, double* gd);
+
+/* Validate parameters without a GPU (the checks of sst_plan_create, R9, R20).
+ * Returns SST_OK, SST_E_INVALID_ARGUMENT, SST_E_COVERAGE or SST_E_UNSUPPORTED.             */
+sst_status sst_params_validate(const sst_params* p);
+
+/* Layout a valid parameter set would have (host only, no plan).                            */
+sst_status sst_params_layout(const sst_params* p, sst_layout* out);
+
+const char* sst_status_str(sst_status s);
+/* Message for the last failing call on `plan`; plan == NULL -> this thread's last failure.
+ * Also carries non-fatal warnings (H_f above the Eq. 38 bound) after plan creation. */
+const char* sst_last_error(const sst_plan* plan);
+int32_t sst_abi_version(void);
+
+/* ---------------------------------------------------------------- plan --------------------- */
+
+/* Create a plan on CUDA device `device`: validates p, snaps the band (R9), uploads window taps
+ * (g, alpha*g'), twiddle tables and inverse normalisation tables (1/(C d[n]), R2/R15), sizes
+ * the launch.  *out receives the plan (NULL on failure).  Synchronous, host-blocking.       */
+sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out);
+sst_status sst_plan_layout(const sst_plan* plan, sst_layout* out);
+/* Set the absolute threshold gamma (>= 0) used by later sst_forward / sst_targets calls.     */
+sst_status sst_plan_set_gamma(sst_plan* plan, double gamma_abs);
+/* RELATIVE mode: take max|S| from this device float (e.g. all-reduced over ranks) instead of
+ * computing it per call; NULL restores per-call computation.  Not owned by the plan.        */
+sst_status sst_plan_set_absmax(sst_plan* plan, const float* absmax_device);
+void sst_plan_destroy(sst_plan* plan);
+
+/* ---------------------------------------------------------------- forward ------------------ */
+
+/* Fused downsampled SST of frames [frame_begin, frame_end) (Eq. 9, 13, 27-29; P:L110-124,
+ * P:L192-210): STFT with g and g', omega_hat with threshold, selective reassignment with
+ * subdivision; writes only the band.
+ *   x:  device float [x_len] holding global samples [x_off, x_off + x_len); must cover
+ *       [frame_begin*H_t - c, (frame_end-1)*H_t - c + L) intersected with [0, N).
+ *   T:  device complex64, row i = frame frame_begin + i, T[i*ldT + l] for l in [0, B);
+ *       ldT >= B (complex elements).  Entries [B, ldT) of a row are not touched.
+ * Errors: SST_E_INVALID_ARGUMENT (NULL, empty or out-of-range frames, x not covering,
+ *         ldT < B), SST_E_CUDA.                                                              */
+sst_status sst_forward(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len,
+                       int64_t frame_begin, int64_t frame_end, float* T, int64_t ldT, void* stream);
+
+/* ---------------------------------------------------------------- inverse ------------------ */
+
+/* Whole-record approximate inverse (Eq. 25-26): T holds all F rows (row stride ldT),
+ * y: device float [N], overwritten with x_hat.                                              */
+sst_status sst_inverse(sst_plan* plan, const float* T, int64_t ldT, float* y, void* stream);
+
+/* Sharded inverse, step 1: y[n - y_off] += sum over frames m in [frame_begin, frame_end) of
+ * g[n - m H_t + c] r~[m, n - m H_t] (Eq. 26 before normalisation).  T row i = frame
+ * frame_begin + i.  y: device float [y_len] for global samples [y_off, y_off + y_len), must
+ * cover the frames' reach intersected with [0, N).                                          */
+sst_status sst_inverse_accumulate(sst_plan* plan, const float* T, int64_t ldT,
+                                  int64_t frame_begin, int64_t frame_end,
+                                  float* y, int64_t y_off, int64_t y_len, void* stream);
+/* Step 2: y[n - y_off] /= C d[n] for global n in [y_off, y_off + y_len) (C = sqrt 2 or C_d). */
+sst_status sst_inverse_finalize(sst_plan* plan, float* y, int64_t y_off, int64_t y_len, void* stream);
+
+/* ---------------------------------------------------------------- debug / parity ----------- */
+
+/* S^g and S^{g'} (Eq. 9) of frames [fb, fe) for k = 0..N_f/2: S, Sd device complex64
+ * [(fe-fb) * (N_f/2+1)].                                                                    */
+sst_status sst_stft(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len,
+                    int64_t fb, int64_t fe, float* S, float* Sd, void* stream);
+/* Target bin of every source coefficient (Eq. 13, 28): l device int32 [(fe-fb)*(N_f/2+1)];
+ * -1 = masked (|S| <= gamma or truncated), -2 = out of band / non-finite (R10, R17).       */
+sst_status sst_targets(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len,
+                       int64_t fb, int64_t fe, int32_t* l, void* stream);
+/* max over frames [fb, fe), k in [0, N_f/2] of |S^g[m,k]| into device float *out (overwritten;
+ * the gamma pre-pass for a relative threshold, Eq. 13, R6).                                */
+sst_status sst_absmax(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len,
+                      int64_t fb, int64_t fe, float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SST_H */

@@ -1,0 +1,136 @@
+// In-register complex DFTs for the SST kernels (sm_100a).
+//
+// fft<N, DIR>(a): a[0..N) in natural order -> DFT in natural order, N in {1,2,4,8,16,32,64},
+// DIR = -1 forward (e^{-2 pi i nk/N}), +1 inverse (no 1/N).  All indices are compile-time,
+// so the composite (four-step) orderings are pure register renaming: no data movement.
+// Twiddles W_64^e come from constant memory with compile-time offsets (operand c[][] form).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace sst {
+
+__constant__ float2 c_w64[64];   // W_64^e = exp(-2 pi i e / 64), rounded from fp64 (set by upload_w64)
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+// multiply by exp(DIR * i pi/2): DIR=-1 -> -i, DIR=+1 -> +i
+template <int DIR>
+__device__ __forceinline__ float2 rot90(float2 a) {
+    return DIR < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
+}
+// W_N^e for the transform direction (compile-time e, N | 64)
+template <int N, int DIR>
+__device__ __forceinline__ float2 twiddle(int e) {
+    float2 w = c_w64[(e * (64 / N)) & 63];
+    return DIR < 0 ? w : make_float2(w.x, -w.y);
+}
+
+template <int N, int DIR>
+struct Fft;
+
+template <int DIR>
+struct Fft<1, DIR> {
+    __device__ __forceinline__ static void run(float2 (&)[1]) {}
+};
+
+template <int DIR>
+struct Fft<2, DIR> {
+    __device__ __forceinline__ static void run(float2 (&a)[2]) {
+        float2 t = a[0];
+        a[0] = cadd(t, a[1]);
+        a[1] = csub(t, a[1]);
+    }
+};
+
+template <int DIR>
+struct Fft<4, DIR> {
+    __device__ __forceinline__ static void run(float2 (&a)[4]) {
+        float2 t0 = cadd(a[0], a[2]), t1 = csub(a[0], a[2]);
+        float2 t2 = cadd(a[1], a[3]), t3 = rot90<DIR>(csub(a[1], a[3]));
+        a[0] = cadd(t0, t2);
+        a[2] = csub(t0, t2);
+        a[1] = cadd(t1, t3);
+        a[3] = csub(t1, t3);
+    }
+};
+
+template <int DIR>
+struct Fft<8, DIR> {
+    __device__ __forceinline__ static void run(float2 (&a)[8]) {
+        const float h = 0.70710678118654752440f;
+        float2 e[4] = {a[0], a[2], a[4], a[6]};
+        float2 o[4] = {a[1], a[3], a[5], a[7]};
+        Fft<4, DIR>::run(e);
+        Fft<4, DIR>::run(o);
+        // o[k] *= W_8^k
+        float2 o1 = o[1], o3 = o[3];
+        if (DIR < 0) {
+            o[1] = make_float2(h * (o1.x + o1.y), h * (o1.y - o1.x));
+            o[3] = make_float2(h * (o3.y - o3.x), -h * (o3.x + o3.y));
+        } else {
+            o[1] = make_float2(h * (o1.x - o1.y), h * (o1.x + o1.y));
+            o[3] = make_float2(-h * (o3.x + o3.y), h * (o3.x - o3.y));
+        }
+        o[2] = rot90<DIR>(o[2]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            a[k] = cadd(e[k], o[k]);
+            a[k + 4] = csub(e[k], o[k]);
+        }
+    }
+};
+
+// composite N = R1 * R2 (four-step, registers only):
+//   n = R2 n1 + n2, k = k1 + R1 k2
+//   X[k1 + R1 k2] = sum_n2 W_R2^{n2 k2} W_N^{n2 k1} sum_n1 x[R2 n1 + n2] W_R1^{n1 k1}
+template <int N, int R1, int DIR>
+struct FftComposite {
+    static constexpr int R2 = N / R1;
+    __device__ __forceinline__ static void run(float2 (&a)[N]) {
+        float2 b[R2][R1];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) {
+            float2 t[R1];
+#pragma unroll
+            for (int n1 = 0; n1 < R1; ++n1) t[n1] = a[R2 * n1 + n2];
+            Fft<R1, DIR>::run(t);
+#pragma unroll
+            for (int k1 = 0; k1 < R1; ++k1) {
+                const int e = n2 * k1;
+                b[n2][k1] = (e == 0) ? t[k1] : cmul(t[k1], twiddle<N, DIR>(e));
+            }
+        }
+#pragma unroll
+        for (int k1 = 0; k1 < R1; ++k1) {
+            float2 u[R2];
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) u[n2] = b[n2][k1];
+            Fft<R2, DIR>::run(u);
+#pragma unroll
+            for (int k2 = 0; k2 < R2; ++k2) a[k1 + R1 * k2] = u[k2];
+        }
+    }
+};
+
+template <int DIR>
+struct Fft<16, DIR> {
+    __device__ __forceinline__ static void run(float2 (&a)[16]) { FftComposite<16, 4, DIR>::run(a); }
+};
+template <int DIR>
+struct Fft<32, DIR> {
+    __device__ __forceinline__ static void run(float2 (&a)[32]) { FftComposite<32, 8, DIR>::run(a); }
+};
+template <int DIR>
+struct Fft<64, DIR> {
+    __device__ __forceinline__ static void run(float2 (&a)[64]) { FftComposite<64, 8, DIR>::run(a); }
+};
+
+}  // namespace sst

@@ -1,0 +1,597 @@
+// Host side of the C ABI declared in include/sst.h: validation, plan creation (window taps,
+// twiddle and normalisation tables), argument checks and kernel launches.  No compute runs
+// on the host: every step of the transform is a kernel in sst_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/sst.h"
+#include "sst_internal.h"
+
+namespace {
+
+thread_local std::string g_thread_err;
+
+constexpr double kPi = 3.14159265358979323846264338327950288;
+
+}  // namespace
+
+struct sst_plan {
+    sst_params p{};
+    sst_layout lay{};
+    int device = 0;
+    std::vector<double> g, gd;
+    double cst = 0;                 // C (sqrt 2 or C_d)
+    // device tables
+    float2* d_taps = nullptr;       // [L]  (g, alpha g')
+    float2* d_tw = nullptr;         // [N_f]
+    float2* d_twz = nullptr;        // [z N_f]
+    float* d_inv_head = nullptr;    // [n_head]
+    float* d_inv_tail = nullptr;    // [n_tail]
+    float* d_inv_per = nullptr;     // [hop]
+    float* d_absmax = nullptr;      // scratch scalar
+    float* d_seam = nullptr;        // [inv_max_grid][2][seam_len]
+    int32_t n_head = 0, n_tail = 0;
+    int fwd_grid = 0, inv_grid = 0;
+    int ring = 0;
+    const float* ext_absmax = nullptr;
+    double gamma_abs = 0;
+    std::string err;
+    ~sst_plan() {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        for (void* q : {(void*)d_taps, (void*)d_tw, (void*)d_twz, (void*)d_inv_head, (void*)d_inv_tail,
+                        (void*)d_inv_per, (void*)d_absmax, (void*)d_seam})
+            if (q) cudaFree(q);
+        cudaSetDevice(prev);
+    }
+};
+
+namespace {
+
+sst_status fail(sst_plan* plan, sst_status s, const std::string& msg) {
+    if (plan) plan->err = msg;
+    g_thread_err = msg;
+    return s;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        cudaSetDevice(dev);
+    }
+    ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+int64_t frames_of(int64_t n, int32_t hop) { return (n - 1) / hop + 1; }
+
+// frame diagonal d[n] = sum_m g[n - m H + c]^2 over frames 0..F-1 (Eq. 11 / Eq. 26 normaliser, R2)
+double diag_at(const std::vector<double>& g, int64_t n, int64_t N, int32_t hop, int32_t c) {
+    const int64_t L = (int64_t)g.size();
+    const int64_t F = frames_of(N, hop);
+    int64_t m_lo = n + c - L + 1;
+    m_lo = m_lo <= 0 ? 0 : (m_lo + hop - 1) / hop;
+    int64_t m_hi = (n + c) / hop;
+    if (m_hi > F - 1) m_hi = F - 1;
+    double d = 0;
+    for (int64_t m = m_lo; m <= m_hi; ++m) {
+        const int64_t j = n - m * hop + c;
+        if (j >= 0 && j < L) d += g[j] * g[j];
+    }
+    return d;
+}
+
+// Validation shared by sst_params_validate / sst_params_layout / sst_plan_create.
+sst_status validate(const sst_params* p, sst_layout* lay, std::string& msg) {
+    if (!p) { msg = "params is NULL"; return SST_E_INVALID_ARGUMENT; }
+    if (!p->g || !p->gd) { msg = "window arrays g/gd are NULL"; return SST_E_INVALID_ARGUMENT; }
+    if (p->n < 1) { msg = "N must be >= 1"; return SST_E_INVALID_ARGUMENT; }
+    if (!std::isfinite(p->fs) || p->fs <= 0) { msg = "fs must be finite and > 0"; return SST_E_INVALID_ARGUMENT; }
+    if (p->win_len < 1) { msg = "window length L must be >= 1"; return SST_E_INVALID_ARGUMENT; }
+    const int32_t L = p->win_len;
+    const int32_t c = p->win_center < 0 ? L / 2 : p->win_center;
+    if (c >= L) { msg = "window centre outside [0, L)"; return SST_E_INVALID_ARGUMENT; }
+    if (p->hop < 1) { msg = "hop H_t must be >= 1"; return SST_E_INVALID_ARGUMENT; }
+    if (p->nfft < 1) { msg = "N_f must be >= 1"; return SST_E_INVALID_ARGUMENT; }
+    if (p->zoom < 1) { msg = "subdivision z must be >= 1"; return SST_E_INVALID_ARGUMENT; }
+    if (!std::isfinite(p->gamma) || p->gamma < 0) { msg = "gamma must be finite and >= 0"; return SST_E_INVALID_ARGUMENT; }
+    if (!std::isfinite(p->sigma)) { msg = "sigma must be finite"; return SST_E_INVALID_ARGUMENT; }
+    if (p->flags & ~(uint32_t)(SST_GAMMA_RELATIVE | SST_SOURCE_TRUNCATE | SST_DETERMINISTIC | SST_DISCRETE_CONSTANT)) {
+        msg = "unknown flag bits"; return SST_E_INVALID_ARGUMENT;
+    }
+    if ((int64_t)L > (int64_t)p->nfft || (int64_t)p->nfft > p->n) {
+        msg = "need L <= N_f <= N (P:L89)"; return SST_E_INVALID_ARGUMENT;
+    }
+    double sg2 = 0, sgd2 = 0;
+    for (int32_t j = 0; j < L; ++j) {
+        if (!std::isfinite(p->g[j]) || !std::isfinite(p->gd[j])) { msg = "non-finite window tap"; return SST_E_INVALID_ARGUMENT; }
+        sg2 += p->g[j] * p->g[j];
+        sgd2 += p->gd[j] * p->gd[j];
+    }
+    if (!(sg2 > 0)) { msg = "window g is identically zero"; return SST_E_INVALID_ARGUMENT; }
+    // band snapping (R9)
+    const double df = p->fs / p->nfft;
+    if (!std::isfinite(p->f1) || !std::isfinite(p->f2) || p->f1 < 0 || p->f2 <= p->f1 || p->f2 > p->fs / 2 * (1 + 1e-15)) {
+        msg = "need 0 <= f1 < f2 <= fs/2"; return SST_E_INVALID_ARGUMENT;
+    }
+    const double k1f = p->f1 / df, k2f = p->f2 / df;
+    const double k1r = std::nearbyint(k1f), k2r = std::nearbyint(k2f);
+    if (std::fabs(k1f - k1r) > 1e-9 || std::fabs(k2f - k2r) > 1e-9) {
+        msg = "band edges must lie on the coarse grid fs/N_f (R9)"; return SST_E_INVALID_ARGUMENT;
+    }
+    const int64_t k1 = (int64_t)k1r, k2 = (int64_t)k2r;
+    if (!(k1 >= 0 && k1 < k2 && k2 <= p->nfft / 2)) { msg = "band outside [0, N_f/2]"; return SST_E_INVALID_ARGUMENT; }
+    // library limits
+    if (!is_pow2(p->nfft)) { msg = "N_f must be a power of two (P:L93)"; return SST_E_UNSUPPORTED; }
+    if (p->nfft < 128 || p->nfft > 4096) { msg = "this build supports 128 <= N_f <= 4096"; return SST_E_UNSUPPORTED; }
+    if (p->zoom > 64 || (int64_t)p->zoom * p->nfft > (1 << 20)) { msg = "z <= 64 and z N_f <= 2^20 supported"; return SST_E_UNSUPPORTED; }
+    if (p->flags & SST_DETERMINISTIC) { msg = "SST_DETERMINISTIC is reserved (not implemented)"; return SST_E_UNSUPPORTED; }
+    // coverage (R20): every n in [0, N) needs d[n] > 0
+    const int64_t N = p->n;
+    const int64_t F = frames_of(N, p->hop);
+    if (p->hop > L || (F - 1) * (int64_t)p->hop - c + L < N) {
+        msg = "frames do not cover [0, N): need H_t <= L and (F-1) H_t - c + L >= N (R20)"; return SST_E_COVERAGE;
+    }
+    {
+        std::vector<double> g(p->g, p->g + L);
+        // periodic interior part
+        for (int32_t i = 0; i < p->hop; ++i) {
+            double s = 0;
+            for (int32_t j = i; j < L; j += p->hop) s += g[j] * g[j];
+            if (!(s > 0)) { msg = "frame diagonal vanishes (window zeros) (R20)"; return SST_E_COVERAGE; }
+        }
+        const int64_t nh = std::min<int64_t>(N, L), nt = std::min<int64_t>(N, (int64_t)L + p->hop);
+        for (int64_t n = 0; n < nh; ++n)
+            if (!(diag_at(g, n, N, p->hop, c) > 0)) { msg = "frame diagonal vanishes at the head (R20)"; return SST_E_COVERAGE; }
+        for (int64_t n = N - nt; n < N; ++n)
+            if (!(diag_at(g, n, N, p->hop, c) > 0)) { msg = "frame diagonal vanishes at the tail (R20)"; return SST_E_COVERAGE; }
+    }
+    if (lay) {
+        std::memset(lay, 0, sizeof(*lay));
+        lay->n = N;
+        lay->frames = F;
+        lay->k1 = (int32_t)k1;
+        lay->k2 = (int32_t)k2;
+        lay->bins = (int32_t)(p->zoom * (k2 - k1));
+        lay->nfft = p->nfft;
+        lay->zoom = p->zoom;
+        lay->hop = p->hop;
+        lay->center = c;
+        lay->win_len = L;
+        lay->src_bins = p->nfft / 2 + 1;
+        lay->fs = p->fs;
+        lay->df_hz = df;
+        lay->f0_hz = k1 * df;
+        lay->dfz_hz = df / p->zoom;
+        lay->gamma_abs = (p->flags & SST_GAMMA_RELATIVE) ? 0.0 : p->gamma;
+        lay->alpha = p->sigma > 0 ? p->sigma * std::sqrt(2.0) : (sgd2 > 0 ? std::sqrt(sg2 / sgd2) : 1.0);
+        lay->hf = (double)N / p->nfft;
+        lay->hf_bound = p->sigma > 0 ? 3.0 * (double)N / (4.0 * kPi * p->sigma) : 0.0;   // Eq. 38, sigma_s = sigma/fs
+    }
+    msg.clear();
+    return SST_OK;
+}
+
+std::mutex g_w64_mu;
+uint64_t g_w64_uploaded = 0;   // bitmask of devices with c_w64 set
+
+sst_status ensure_w64(int device, std::string& msg) {
+    std::lock_guard<std::mutex> lk(g_w64_mu);
+    if (device < 64 && (g_w64_uploaded >> device) & 1ull) return SST_OK;
+    float2 w[64];
+    for (int e = 0; e < 64; ++e) {
+        const double a = -2.0 * kPi * e / 64.0;
+        w[e] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    cudaError_t ce = sst::upload_w64(w);
+    if (ce != cudaSuccess) { msg = std::string("upload twiddles: ") + cudaGetErrorString(ce); return SST_E_CUDA; }
+    if (device < 64) g_w64_uploaded |= 1ull << device;
+    return SST_OK;
+}
+
+template <class T>
+sst_status upload(sst_plan* pl, T** dst, const std::vector<T>& src) {
+    if (src.empty()) return SST_OK;
+    cudaError_t ce = cudaMalloc((void**)dst, sizeof(T) * src.size());
+    if (ce == cudaErrorMemoryAllocation) return fail(pl, SST_E_OUT_OF_MEMORY, "cudaMalloc failed (out of memory)");
+    if (ce != cudaSuccess) return fail(pl, SST_E_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(ce));
+    ce = cudaMemcpy(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) return fail(pl, SST_E_CUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(ce));
+    return SST_OK;
+}
+
+sst_status cuda_status(sst_plan* pl, cudaError_t ce, const char* what) {
+    if (ce == cudaSuccess) return SST_OK;
+    cudaGetLastError();
+    return fail(pl, SST_E_CUDA, std::string(what) + ": " + cudaGetErrorString(ce));
+}
+
+// x slice must cover [fb H - c, (fe-1) H - c + L) intersected with [0, N)
+bool covers_input(const sst_plan* pl, int64_t x_off, int64_t x_len, int64_t fb, int64_t fe) {
+    const int64_t lo = std::max<int64_t>(0, fb * pl->lay.hop - pl->lay.center);
+    const int64_t hi = std::min<int64_t>(pl->lay.n, (fe - 1) * pl->lay.hop - pl->lay.center + pl->lay.win_len);
+    if (hi <= lo) return true;
+    return x_off <= lo && x_off + x_len >= hi;
+}
+
+sst_status check_frames(sst_plan* pl, int64_t fb, int64_t fe) {
+    if (!(fb >= 0 && fb < fe && fe <= pl->lay.frames))
+        return fail(pl, SST_E_INVALID_ARGUMENT, "frame range must satisfy 0 <= begin < end <= F");
+    return SST_OK;
+}
+
+sst::FwdArgs fwd_args(const sst_plan* pl, const float* x, int64_t x_off, int64_t fb, int64_t fe) {
+    sst::FwdArgs a{};
+    a.x = x;
+    a.x_off = x_off;
+    a.n = pl->lay.n;
+    a.frame_begin = fb;
+    a.frame_end = fe;
+    a.hop = pl->lay.hop;
+    a.L = pl->lay.win_len;
+    a.c = pl->lay.center;
+    a.nfft = pl->lay.nfft;
+    a.taps = pl->d_taps;
+    a.tw = pl->d_tw;
+    a.k1 = pl->lay.k1;
+    a.k2 = pl->lay.k2;
+    a.bins = pl->lay.bins;
+    a.zoom = pl->lay.zoom;
+    const bool trunc = pl->p.flags & SST_SOURCE_TRUNCATE;
+    a.src_lo = trunc ? pl->lay.k1 : 0;
+    a.src_hi = trunc ? pl->lay.k2 : pl->lay.nfft / 2 + 1;
+    const double gam = pl->gamma_abs;
+    a.gamma2x4 = (float)(4.0 * gam * gam);
+    a.absmax_dev = nullptr;
+    a.gamma_rel = (float)pl->p.gamma;
+    a.r_scale = (float)(pl->lay.nfft / (2.0 * kPi * pl->lay.alpha));
+    a.inv_alpha2 = (float)(1.0 / (2.0 * pl->lay.alpha));
+    return a;
+}
+
+int fwd_grid_for(const sst_plan* pl, int64_t nfr) {
+    const int G = sst::kCtaThreads / (pl->lay.nfft / 64);
+    const int64_t tiles = (nfr + G - 1) / G;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, pl->fwd_grid));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sst_status_str(sst_status s) {
+    switch (s) {
+        case SST_OK: return "SST_OK";
+        case SST_E_INVALID_ARGUMENT: return "SST_E_INVALID_ARGUMENT";
+        case SST_E_COVERAGE: return "SST_E_COVERAGE";
+        case SST_E_UNSUPPORTED: return "SST_E_UNSUPPORTED";
+        case SST_E_CUDA: return "SST_E_CUDA";
+        case SST_E_OUT_OF_MEMORY: return "SST_E_OUT_OF_MEMORY";
+        case SST_E_INTERNAL: return "SST_E_INTERNAL";
+    }
+    return "SST_E_UNKNOWN";
+}
+
+const char* sst_last_error(const sst_plan* plan) {
+    return plan ? plan->err.c_str() : g_thread_err.c_str();
+}
+
+int32_t sst_abi_version(void) { return SST_ABI_VERSION; }
+
+sst_status sst_gaussian_window(int32_t L, double sigma, int32_t center, double* g, double* gd) {
+    if (L < 1 || !std::isfinite(sigma) || sigma <= 0 || !g || !gd)
+        return fail(nullptr, SST_E_INVALID_ARGUMENT, "sst_gaussian_window: need L >= 1, sigma > 0, non-NULL outputs");
+    const int32_t c = center < 0 ? L / 2 : center;
+    if (c >= L) return fail(nullptr, SST_E_INVALID_ARGUMENT, "sst_gaussian_window: centre outside [0, L)");
+    const double amp = std::pow(kPi * sigma * sigma, -0.25);           // (pi sigma^2)^(-1/4)
+    for (int32_t j = 0; j < L; ++j) {
+        const double t = (double)(j - c);
+        const double e = amp * std::exp(-(t * t) / (2.0 * sigma * sigma));
+        g[j] = e;
+        gd[j] = -(t / (sigma * sigma)) * e;                              // analytic g'
+    }
+    return SST_OK;
+}
+
+sst_status sst_params_validate(const sst_params* p) {
+    std::string msg;
+    sst_status s = validate(p, nullptr, msg);
+    if (s != SST_OK) g_thread_err = msg;
+    return s;
+}
+
+sst_status sst_params_layout(const sst_params* p, sst_layout* out) {
+    if (!out) return fail(nullptr, SST_E_INVALID_ARGUMENT, "layout output is NULL");
+    std::string msg;
+    sst_status s = validate(p, out, msg);
+    if (s != SST_OK) g_thread_err = msg;
+    return s;
+}
+
+sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
+    if (!out) return fail(nullptr, SST_E_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    sst_plan* pl = new (std::nothrow) sst_plan();
+    if (!pl) return fail(nullptr, SST_E_INTERNAL, "host allocation failed");
+    std::string msg;
+    sst_status s = validate(p, &pl->lay, msg);
+    if (s != SST_OK) { delete pl; return fail(nullptr, s, msg); }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        delete pl;
+        return fail(nullptr, ndev == 0 ? SST_E_CUDA : SST_E_INVALID_ARGUMENT, "no such CUDA device");
+    }
+    pl->p = *p;
+    pl->device = device;
+    const int32_t L = pl->lay.win_len, c = pl->lay.center, H = pl->lay.hop, Nf = pl->lay.nfft, z = pl->lay.zoom;
+    const int64_t N = pl->lay.n;
+    pl->g.assign(p->g, p->g + L);
+    pl->gd.assign(p->gd, p->gd + L);
+    pl->p.g = nullptr;
+    pl->p.gd = nullptr;
+    pl->gamma_abs = pl->lay.gamma_abs;
+    {
+        double sg = 0, sg2 = 0;
+        for (double v : pl->g) { sg += v; sg2 += v * v; }
+        pl->cst = (p->flags & SST_DISCRETE_CONSTANT) ? pl->g[c] * sg / sg2 : std::sqrt(2.0);   // Eq. 24 / R15
+    }
+    DeviceGuard guard(device);
+    if ((s = ensure_w64(device, msg)) != SST_OK) { delete pl; return fail(nullptr, s, msg); }
+
+    const double alpha = pl->lay.alpha;
+    std::vector<float2> taps(L), tw(Nf), twz((size_t)z * Nf);
+    for (int32_t j = 0; j < L; ++j) taps[j] = make_float2((float)pl->g[j], (float)(alpha * pl->gd[j]));
+    for (int32_t i = 0; i < Nf; ++i) {
+        const double a = -2.0 * kPi * i / Nf;
+        tw[i] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    for (int64_t e = 0; e < (int64_t)z * Nf; ++e) {
+        const double a = 2.0 * kPi * (double)e / ((double)z * Nf);
+        twz[e] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    // 1/(C d[n]): head [0, n_head), tail [N - n_tail, N), interior periodic in (n + c) mod H
+    pl->n_head = (int32_t)std::min<int64_t>(N, L);
+    pl->n_tail = (int32_t)std::min<int64_t>(N, (int64_t)L + H);
+    std::vector<float> head(pl->n_head), tail(pl->n_tail), per(H);
+    for (int32_t n = 0; n < pl->n_head; ++n) head[n] = (float)(1.0 / (pl->cst * diag_at(pl->g, n, N, H, c)));
+    for (int32_t i = 0; i < pl->n_tail; ++i)
+        tail[i] = (float)(1.0 / (pl->cst * diag_at(pl->g, N - pl->n_tail + i, N, H, c)));
+    for (int32_t i = 0; i < H; ++i) {
+        double d = 0;
+        for (int32_t j = i; j < L; j += H) d += pl->g[j] * pl->g[j];
+        per[i] = (float)(1.0 / (pl->cst * d));
+    }
+    if ((s = upload(pl, &pl->d_taps, taps)) != SST_OK || (s = upload(pl, &pl->d_tw, tw)) != SST_OK ||
+        (s = upload(pl, &pl->d_twz, twz)) != SST_OK || (s = upload(pl, &pl->d_inv_head, head)) != SST_OK ||
+        (s = upload(pl, &pl->d_inv_tail, tail)) != SST_OK || (s = upload(pl, &pl->d_inv_per, per)) != SST_OK) {
+        msg = pl->err;
+        delete pl;
+        return fail(nullptr, s, msg);
+    }
+    cudaError_t ce = cudaMalloc((void**)&pl->d_absmax, sizeof(float));
+    if (ce != cudaSuccess) { delete pl; cudaGetLastError(); return fail(nullptr, SST_E_OUT_OF_MEMORY, "cudaMalloc absmax"); }
+    pl->fwd_grid = sst::forward_max_grid(Nf, device);
+    pl->inv_grid = sst::inverse_max_grid(Nf, H, L, device);
+    sst::inverse_smem_bytes(Nf, H, L, &pl->ring);
+    const int32_t seam_len = std::max(0, L - H);
+    if (seam_len > 0) {
+        ce = cudaMalloc((void**)&pl->d_seam, sizeof(float) * (size_t)pl->inv_grid * 2 * seam_len);
+        if (ce != cudaSuccess) { delete pl; cudaGetLastError(); return fail(nullptr, SST_E_OUT_OF_MEMORY, "cudaMalloc seams"); }
+    }
+    if (pl->fwd_grid <= 0 || pl->inv_grid <= 0) { delete pl; return fail(nullptr, SST_E_CUDA, "occupancy query failed"); }
+    pl->err.clear();
+    if (pl->lay.hf_bound > 0 && pl->lay.hf > pl->lay.hf_bound) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "warning: H_f = %.3g exceeds the Eq. 38 bound %.3g (P:L357); SST degenerates to STFT",
+                      pl->lay.hf, pl->lay.hf_bound);
+        pl->err = buf;
+    }
+    *out = pl;
+    return SST_OK;
+}
+
+sst_status sst_plan_layout(const sst_plan* plan, sst_layout* out) {
+    if (!plan || !out) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan or output");
+    *out = plan->lay;
+    out->gamma_abs = plan->gamma_abs;
+    return SST_OK;
+}
+
+sst_status sst_plan_set_gamma(sst_plan* plan, double gamma_abs) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    if (!std::isfinite(gamma_abs) || gamma_abs < 0) return fail(plan, SST_E_INVALID_ARGUMENT, "gamma must be finite and >= 0");
+    plan->gamma_abs = gamma_abs;
+    plan->p.flags &= ~(uint32_t)SST_GAMMA_RELATIVE;
+    return SST_OK;
+}
+
+sst_status sst_plan_set_absmax(sst_plan* plan, const float* absmax_device) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    plan->ext_absmax = absmax_device;
+    return SST_OK;
+}
+
+void sst_plan_destroy(sst_plan* plan) { delete plan; }
+
+static sst_status run_forward_mode(sst_plan* plan, int mode, const float* x, int64_t x_off, int64_t x_len, int64_t fb,
+                                   int64_t fe, sst::FwdArgs& a, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (mode != sst::kModeAbsmax && (plan->p.flags & SST_GAMMA_RELATIVE)) {
+        if (plan->ext_absmax) {
+            a.absmax_dev = plan->ext_absmax;
+        } else {
+            sst::FwdArgs m = a;
+            m.absmax_out = plan->d_absmax;
+            sst_status s = cuda_status(plan, cudaMemsetAsync(plan->d_absmax, 0, sizeof(float), st), "memset");
+            if (s != SST_OK) return s;
+            s = cuda_status(plan, sst::launch_forward(m, sst::kModeAbsmax, fwd_grid_for(plan, fe - fb), st), "absmax launch");
+            if (s != SST_OK) return s;
+            a.absmax_dev = plan->d_absmax;
+        }
+    }
+    (void)x; (void)x_off; (void)x_len;
+    return cuda_status(plan, sst::launch_forward(a, mode, fwd_grid_for(plan, fe - fb), st), "forward launch");
+}
+
+sst_status sst_forward(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len, int64_t frame_begin,
+                       int64_t frame_end, float* T, int64_t ldT, void* stream) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    if (!x || !T) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL x or T");
+    sst_status s = check_frames(plan, frame_begin, frame_end);
+    if (s != SST_OK) return s;
+    if (ldT < plan->lay.bins) return fail(plan, SST_E_INVALID_ARGUMENT, "ldT < B");
+    if (x_len < 0 || !covers_input(plan, x_off, x_len, frame_begin, frame_end))
+        return fail(plan, SST_E_INVALID_ARGUMENT, "x slice does not cover the frames' samples");
+    DeviceGuard guard(plan->device);
+    sst::FwdArgs a = fwd_args(plan, x - 0, x_off, frame_begin, frame_end);
+    a.T = reinterpret_cast<float2*>(T);
+    a.ldT = ldT;
+    return run_forward_mode(plan, sst::kModeForward, x, x_off, x_len, frame_begin, frame_end, a, stream);
+}
+
+sst_status sst_stft(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len, int64_t fb, int64_t fe, float* S,
+                    float* Sd, void* stream) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    if (!x || !S || !Sd) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL pointer");
+    sst_status s = check_frames(plan, fb, fe);
+    if (s != SST_OK) return s;
+    if (x_len < 0 || !covers_input(plan, x_off, x_len, fb, fe))
+        return fail(plan, SST_E_INVALID_ARGUMENT, "x slice does not cover the frames' samples");
+    DeviceGuard guard(plan->device);
+    sst::FwdArgs a = fwd_args(plan, x, x_off, fb, fe);
+    a.S = reinterpret_cast<float2*>(S);
+    a.Sd = reinterpret_cast<float2*>(Sd);
+    a.gamma2x4 = -1.0f;   // report every bin
+    a.src_lo = 0;
+    a.src_hi = plan->lay.nfft / 2 + 1;
+    return cuda_status(plan, sst::launch_forward(a, sst::kModeStft, fwd_grid_for(plan, fe - fb), (cudaStream_t)stream),
+                       "stft launch");
+}
+
+sst_status sst_targets(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len, int64_t fb, int64_t fe, int32_t* l,
+                       void* stream) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    if (!x || !l) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL pointer");
+    sst_status s = check_frames(plan, fb, fe);
+    if (s != SST_OK) return s;
+    if (x_len < 0 || !covers_input(plan, x_off, x_len, fb, fe))
+        return fail(plan, SST_E_INVALID_ARGUMENT, "x slice does not cover the frames' samples");
+    DeviceGuard guard(plan->device);
+    sst::FwdArgs a = fwd_args(plan, x, x_off, fb, fe);
+    a.lout = l;
+    return run_forward_mode(plan, sst::kModeTargets, x, x_off, x_len, fb, fe, a, stream);
+}
+
+sst_status sst_absmax(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len, int64_t fb, int64_t fe, float* out,
+                      void* stream) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    if (!x || !out) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL pointer");
+    sst_status s = check_frames(plan, fb, fe);
+    if (s != SST_OK) return s;
+    if (x_len < 0 || !covers_input(plan, x_off, x_len, fb, fe))
+        return fail(plan, SST_E_INVALID_ARGUMENT, "x slice does not cover the frames' samples");
+    DeviceGuard guard(plan->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    s = cuda_status(plan, cudaMemsetAsync(out, 0, sizeof(float), st), "memset");
+    if (s != SST_OK) return s;
+    sst::FwdArgs a = fwd_args(plan, x, x_off, fb, fe);
+    a.absmax_out = out;
+    a.gamma2x4 = -1.0f;
+    return cuda_status(plan, sst::launch_forward(a, sst::kModeAbsmax, fwd_grid_for(plan, fe - fb), st), "absmax launch");
+}
+
+static sst::InvArgs inv_args(const sst_plan* pl, const float* T, int64_t ldT, int64_t fb, int64_t fe, float* y,
+                             int64_t y_off, int64_t y_len, int normalize, int* grid) {
+    sst::InvArgs a{};
+    a.T = reinterpret_cast<const float2*>(T);
+    a.ldT = ldT;
+    a.n = pl->lay.n;
+    a.frame_begin = fb;
+    a.frame_end = fe;
+    a.hop = pl->lay.hop;
+    a.L = pl->lay.win_len;
+    a.c = pl->lay.center;
+    a.nfft = pl->lay.nfft;
+    a.zoom = pl->lay.zoom;
+    a.k1 = pl->lay.k1;
+    a.bins = pl->lay.bins;
+    a.taps = pl->d_taps;
+    a.tw = pl->d_tw;
+    a.twz = pl->d_twz;
+    a.inv_n = (float)(1.0 / pl->lay.nfft);
+    a.y = y;
+    a.y_off = y_off;
+    a.y_len = y_len;
+    a.normalize = normalize;
+    a.inv_head = pl->d_inv_head;
+    a.n_head = pl->n_head;
+    a.inv_tail = pl->d_inv_tail;
+    a.n_tail = pl->n_tail;
+    a.inv_per = pl->d_inv_per;
+    a.seam = pl->d_seam;
+    a.seam_len = std::max(0, pl->lay.win_len - pl->lay.hop);
+    a.ring = pl->ring;
+    const int64_t F = fe - fb;
+    const int64_t min_fpc = (pl->lay.win_len + pl->lay.hop - 1) / pl->lay.hop;
+    int64_t fpc = (F + pl->inv_grid - 1) / pl->inv_grid;
+    if (fpc < min_fpc) fpc = min_fpc;
+    a.frames_per_cta = fpc;
+    *grid = (int)((F + fpc - 1) / fpc);
+    return a;
+}
+
+static sst_status run_inverse(sst_plan* plan, const float* T, int64_t ldT, int64_t fb, int64_t fe, float* y, int64_t y_off,
+                              int64_t y_len, int normalize, void* stream) {
+    int grid = 0;
+    sst::InvArgs a = inv_args(plan, T, ldT, fb, fe, y, y_off, y_len, normalize, &grid);
+    cudaStream_t st = (cudaStream_t)stream;
+    sst_status s = cuda_status(plan, sst::launch_inverse(a, grid, st), "inverse launch");
+    if (s != SST_OK) return s;
+    return cuda_status(plan, sst::launch_inverse_seams(a, grid, st), "seam launch");
+}
+
+sst_status sst_inverse(sst_plan* plan, const float* T, int64_t ldT, float* y, void* stream) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    if (!T || !y) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL T or y");
+    if (ldT < plan->lay.bins) return fail(plan, SST_E_INVALID_ARGUMENT, "ldT < B");
+    DeviceGuard guard(plan->device);
+    return run_inverse(plan, T, ldT, 0, plan->lay.frames, y, 0, plan->lay.n, 1, stream);
+}
+
+sst_status sst_inverse_accumulate(sst_plan* plan, const float* T, int64_t ldT, int64_t frame_begin, int64_t frame_end,
+                                  float* y, int64_t y_off, int64_t y_len, void* stream) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    if (!T || !y) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL T or y");
+    sst_status s = check_frames(plan, frame_begin, frame_end);
+    if (s != SST_OK) return s;
+    if (ldT < plan->lay.bins) return fail(plan, SST_E_INVALID_ARGUMENT, "ldT < B");
+    if (y_len < 0 || !covers_input(plan, y_off, y_len, frame_begin, frame_end))
+        return fail(plan, SST_E_INVALID_ARGUMENT, "y span does not cover the frames' reach");
+    DeviceGuard guard(plan->device);
+    return run_inverse(plan, T, ldT, frame_begin, frame_end, y, y_off, y_len, 0, stream);
+}
+
+sst_status sst_inverse_finalize(sst_plan* plan, float* y, int64_t y_off, int64_t y_len, void* stream) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    if (!y || y_len < 0) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL y or negative length");
+    if (y_off < 0 || y_off + y_len > plan->lay.n) return fail(plan, SST_E_INVALID_ARGUMENT, "y span outside [0, N)");
+    DeviceGuard guard(plan->device);
+    return cuda_status(plan,
+                       sst::launch_finalize(y, y_off, y_len, plan->lay.n, plan->lay.hop, plan->lay.center, plan->d_inv_head,
+                                            plan->n_head, plan->d_inv_tail, plan->n_tail, plan->d_inv_per,
+                                            (cudaStream_t)stream),
+                       "finalize launch");
+}
+
+}  // extern "C"

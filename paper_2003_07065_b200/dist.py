@@ -1,0 +1,124 @@
+"""Time sharding of one long record over ranks.
+
+Rank r of P owns frames [F r / P, F (r+1) / P).  Frames are independent (Eq. 7-9), so the
+forward needs no communication: each rank reads its own samples plus a window-length halo.
+The inverse's overlap-add (Eq. 26) couples neighbours: samples in
+``seam(r) = [fb_r H - c, (fb_r - 1) H - c + L)`` (L - H of them) receive frames from ranks r-1
+and r.  Rank r-1 sends its partial sums there to rank r (one NCCL send/recv per boundary);
+rank r owns and finalises ``[fb_r H - c, fb_{r+1} H - c)`` clipped to [0, N).
+
+Pure host logic plus torch.distributed point-to-point calls; works with the NCCL backend on
+device tensors and with gloo on CPU tensors (tests/test_dist_gloo.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+@dataclass(frozen=True)
+class Shard:
+    rank: int
+    world: int
+    frame_begin: int
+    frame_end: int
+    span_lo: int      # samples [span_lo, span_hi) read by the forward / written by the accumulate
+    span_hi: int
+    own_lo: int       # samples this rank finalises
+    own_hi: int
+    seam_in: int      # length of the left seam received from rank-1 (0 for rank 0)
+    seam_out: int     # length of the right seam sent to rank+1 (0 for the last rank)
+
+    @property
+    def frames(self) -> int:
+        return self.frame_end - self.frame_begin
+
+
+def frames_of(n: int, hop: int) -> int:
+    return (n - 1) // hop + 1
+
+
+def shard(n: int, hop: int, win_len: int, center: int, world: int, rank: int) -> Shard:
+    """Frame range, sample span and owned output range of ``rank`` (see module doc)."""
+    F = frames_of(n, hop)
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    min_frames = -(-win_len // hop)
+    if F // world < min_frames and world > 1:
+        raise ValueError(f"each rank needs >= ceil(L/H) = {min_frames} frames; F={F}, world={world}")
+    fb = F * rank // world
+    fe = F * (rank + 1) // world
+    span_lo = max(0, fb * hop - center)
+    span_hi = min(n, (fe - 1) * hop - center + win_len)
+    own_lo = 0 if rank == 0 else max(0, fb * hop - center)
+    own_hi = n if rank == world - 1 else min(n, fe * hop - center)
+    seam_in = 0
+    if rank > 0:
+        lo = max(0, fb * hop - center)
+        hi = min(n, (fb - 1) * hop - center + win_len)
+        seam_in = max(0, hi - lo)
+    seam_out = 0
+    if rank < world - 1:
+        lo = max(0, fe * hop - center)
+        hi = min(n, (fe - 1) * hop - center + win_len)
+        seam_out = max(0, hi - lo)
+    return Shard(rank, world, fb, fe, span_lo, span_hi, own_lo, own_hi, seam_in, seam_out)
+
+
+def exchange_seams(y_span: torch.Tensor, sh: Shard, hop: int, center: int, group=None) -> torch.Tensor:
+    """Add rank-1's partial OLA sums into this rank's left seam and send this rank's right-seam
+    partials to rank+1 (ncclSend/ncclRecv via batch_isend_irecv).  ``y_span`` holds the
+    unnormalised partial y over [span_lo, span_hi).  Returns ``y_span`` (modified in place)."""
+    if sh.world == 1:
+        return y_span
+    ops = []
+    recv = None
+    if sh.seam_out > 0:
+        lo = max(0, sh.frame_end * hop - center) - sh.span_lo
+        ops.append(dist.P2POp(dist.isend, y_span[lo:lo + sh.seam_out].contiguous(), sh.rank + 1, group))
+    if sh.seam_in > 0:
+        recv = torch.empty(sh.seam_in, dtype=y_span.dtype, device=y_span.device)
+        ops.append(dist.P2POp(dist.irecv, recv, sh.rank - 1, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    if recv is not None:
+        lo = sh.own_lo - sh.span_lo
+        y_span[lo:lo + sh.seam_in] += recv
+    return y_span
+
+
+def own_slice(y_span: torch.Tensor, sh: Shard) -> torch.Tensor:
+    """View of the samples this rank finalises."""
+    return y_span[sh.own_lo - sh.span_lo: sh.own_hi - sh.span_lo]
+
+
+def gather_owned(y_own: torch.Tensor, sh: Shard, n: int, dst: int = 0, group=None):
+    """Collect every rank's owned samples into one [N] tensor on ``dst`` (verification only;
+    excluded from throughput).  Returns the tensor on dst, None elsewhere."""
+    if sh.world == 1:
+        return y_own
+    sizes = [torch.zeros(1, dtype=torch.int64, device=y_own.device) for _ in range(sh.world)]
+    dist.all_gather(sizes, torch.tensor([y_own.numel()], dtype=torch.int64, device=y_own.device), group=group)
+    mx = int(max(int(s.item()) for s in sizes))
+    pad = torch.zeros(mx, dtype=y_own.dtype, device=y_own.device)
+    pad[:y_own.numel()] = y_own
+    bufs = [torch.zeros(mx, dtype=y_own.dtype, device=y_own.device) for _ in range(sh.world)]
+    dist.all_gather(bufs, pad, group=group)
+    if sh.rank != dst:
+        return None
+    return torch.cat([b[:int(s.item())] for b, s in zip(bufs, sizes)])[:n]
+
+
+def max_over_ranks(value: float, device, group=None) -> float:
+    """all_reduce(MAX) of one float (timings, max|S|)."""
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+__all__ = ["Shard", "shard", "exchange_seams", "own_slice", "gather_owned", "max_over_ranks", "frames_of"]

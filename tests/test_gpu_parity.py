@@ -1,0 +1,309 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by element.
+
+Tolerances (BASELINE.json north_star): STFT relative Frobenius <= 1e-5; squeezed plane
+relative L2 <= 1e-3 with target disagreement <= 1e-4 of above-threshold coefficients, each
+(for |S| >= 1e-2 max) within 1e-4 coarse bins of a rounding boundary; reconstruction relative
+L2 <= 1e-4.  The oracle receives the same fp32 samples upcast to fp64 and its own window.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+import oracle as O  # noqa: E402
+from gen import get_config  # noqa: E402
+from tests._helpers import config_gamma, flip_stats, make_plan, rel, signal  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2003_07065_b200 as P
+    return P
+
+
+# (N, fs, L, sigma, hop, nfft, f1, f2, z): every N2 instantiation, ragged N / F, L < N_f,
+# selective bands, non-power-of-two z, the BIG (chunked) squeeze path
+SMALL = [
+    (50001, 1000.0, 128, 16.0, 3, 128, 0.0, 500.0, 1),
+    (40000, 2048.0, 200, 25.0, 7, 256, 256.0, 768.0, 3),
+    (30011, 25600.0, 512, 64.0, 4, 512, 0.0, 12800.0, 8),
+    (70000, 25600.0, 1024, 128.0, 8, 1024, 0.0, 2000.0, 2),
+    (60000, 51200.0, 2048, 256.0, 16, 2048, 0.0, 4000.0, 4),
+    (40960, 1024.0, 257, 32.0, 1, 4096, 0.0, 512.0, 1),
+    (50000, 51200.0, 4096, 512.0, 32, 4096, 0.0, 6400.0, 2),
+    (20000, 1024.0, 301, 40.0, 10, 512, 100.0, 400.0, 2),
+    (30000, 1000.0, 256, 30.0, 6, 256, 0.0, 500.0, 5),
+]
+
+
+def _sig(N, fs, seed):
+    t = np.arange(N) / fs
+    rng = np.random.default_rng(seed)
+    x = np.zeros(N)
+    for f in rng.uniform(0.02, 0.4, size=4) * fs:
+        x += rng.uniform(0.3, 1.0) * np.cos(2 * np.pi * f * t + rng.uniform(0, 6.28))
+    x += 0.5 * np.cos(2 * np.pi * (0.1 * fs * t + 0.02 * fs * t * t / t[-1]))
+    x += 0.1 * rng.standard_normal(N)
+    return x.astype(np.float32)
+
+
+def _case(spec, seed=0):
+    N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x = _sig(N, fs, seed + N)
+    g, gd, c = O.gaussian_window(L, sigma)
+    return x, g, gd, c
+
+
+@pytest.mark.parametrize("spec", SMALL, ids=[f"nf{s[5]}_h{s[4]}_z{s[8]}_N{s[0]}" for s in SMALL])
+def test_stft_parity(P, spec):
+    N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c = _case(spec)
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=0.0, device=0)
+    S, Sd = plan.stft(torch.from_numpy(x).to(DEV))
+    So = O.stft(x.astype(np.float64), g, c, hop, nfft)
+    Sdo = O.stft(x.astype(np.float64), gd, c, hop, nfft)
+    assert rel(S.cpu().numpy(), So) <= 1e-5
+    assert rel(Sd.cpu().numpy(), Sdo) <= 1e-5
+
+
+@pytest.mark.parametrize("spec", SMALL, ids=[f"nf{s[5]}_h{s[4]}_z{s[8]}_N{s[0]}" for s in SMALL])
+def test_forward_parity_and_flips(P, spec):
+    N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c = _case(spec)
+    So = O.stft(x.astype(np.float64), g, c, hop, nfft)
+    gamma = 1e-6 * float(np.abs(So).max())
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=gamma, device=0)
+    xd = torch.from_numpy(x).to(DEV)
+    T = plan.forward(xd).cpu().numpy()
+    lg = plan.targets(xd).cpu().numpy()
+    To, S, Sd, lo = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, gamma, debug=True)
+    _, _, fhat = O.if_estimate(S, Sd, nfft, gamma)
+    st = flip_stats(lg, lo, S, fhat, plan.layout["k1"], z)
+    assert T.shape == To.shape
+    assert rel(T, To) <= 1e-3, st
+    assert st["frac"] <= 1e-4, st
+    assert st["far_big"] <= 1e-4, st
+
+
+@pytest.mark.parametrize("spec", SMALL, ids=[f"nf{s[5]}_h{s[4]}_z{s[8]}_N{s[0]}" for s in SMALL])
+def test_inverse_parity(P, spec):
+    """Inverse kernel on the GPU's own T vs the oracle inverse of that T (isolates K4), and
+    end to end vs the oracle's inverse of the oracle's T."""
+    N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c = _case(spec)
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=0.0, device=0)
+    xd = torch.from_numpy(x).to(DEV)
+    T = plan.forward(xd)
+    y = plan.inverse(T).cpu().numpy()
+    Tn = T.cpu().numpy().astype(np.complex128)
+    k1 = plan.layout["k1"]
+    yo = O.sst_inverse(Tn, g, c, hop, nfft, z, k1, N)
+    assert rel(y, yo) <= 1e-4
+    To = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, 0.0)
+    ye = O.sst_inverse(To, g, c, hop, nfft, z, k1, N)
+    assert rel(y, ye) <= 1e-4
+
+
+def test_discrete_constant_flag(P):
+    N, fs, L, sigma, hop, nfft, f1, f2, z = SMALL[3]
+    x, g, gd, c = _case(SMALL[3])
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=0.0, flags=P.SST_DISCRETE_CONSTANT, device=0)
+    xd = torch.from_numpy(x).to(DEV)
+    T = plan.forward(xd)
+    y = plan.inverse(T).cpu().numpy()
+    yo = O.sst_inverse(T.cpu().numpy().astype(np.complex128), g, c, hop, nfft, z, 0, N, constant="discrete")
+    assert rel(y, yo) <= 1e-4
+
+
+def test_frame_ranges_and_offsets_bitwise(P):
+    """Forward over sub-ranges with an offset x slice reproduces rows of the full forward
+    exactly (frames are independent, P12), including both record edges."""
+    spec = SMALL[4]
+    N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c = _case(spec)
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=1e-4, device=0)
+    xd = torch.from_numpy(x).to(DEV)
+    full = plan.forward(xd)
+    F = plan.frames
+    for fb, fe in [(0, 7), (5, 130), (F - 9, F), (1000, 1001)]:
+        lo = max(0, fb * hop - c)
+        hi = min(N, (fe - 1) * hop - c + L)
+        xs = xd[lo:hi].contiguous()
+        part = plan.forward(xs, fb, fe, x_off=lo)
+        assert torch.equal(part, full[fb:fe])
+
+
+def test_ldT_padding(P):
+    spec = SMALL[3]
+    N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c = _case(spec)
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=1e-4, device=0)
+    xd = torch.from_numpy(x).to(DEV)
+    full = plan.forward(xd)
+    out = torch.full((plan.frames, plan.bins + 7), 123.0 + 0j, dtype=torch.complex64, device=DEV)
+    plan.forward(xd, out=out)
+    assert torch.equal(out[:, :plan.bins], full)
+    assert torch.all(out[:, plan.bins:] == 123.0)
+    y1 = plan.inverse(full)
+    y2 = plan.inverse(out)
+    assert torch.allclose(y1, y2, rtol=0, atol=1e-6 * float(y1.abs().max()))
+
+
+def test_absmax_and_relative_gamma(P):
+    spec = SMALL[1]
+    N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c = _case(spec)
+    So = O.stft(x.astype(np.float64), g, c, hop, nfft)
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=0.05, flags=P.SST_GAMMA_RELATIVE, device=0)
+    xd = torch.from_numpy(x).to(DEV)
+    m = float(plan.absmax(xd))
+    assert m == pytest.approx(float(np.abs(So).max()), rel=1e-5)
+    T = plan.forward(xd).cpu().numpy()
+    To = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, 0.05 * float(np.abs(So).max()))
+    assert rel(T, To) <= 1e-3
+    # externally supplied max (as all-reduced over ranks)
+    ext = torch.tensor(2.0 * m, dtype=torch.float32, device=DEV)
+    plan.set_absmax(ext)
+    T2 = plan.forward(xd).cpu().numpy()
+    To2 = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, 0.1 * m)
+    assert rel(T2, To2) <= 1e-3
+
+
+def test_truncate_flag(P):
+    spec = SMALL[7]
+    N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c = _case(spec)
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=1e-5, flags=P.SST_SOURCE_TRUNCATE, device=0)
+    T = plan.forward(torch.from_numpy(x).to(DEV)).cpu().numpy()
+    To = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, 1e-5, truncate=True)
+    assert rel(T, To) <= 1e-3
+
+
+def test_sharded_inverse_equals_whole(P):
+    """Frame ranges accumulated into overlapping y spans, seams added, then finalised, equal the
+    single-call inverse (P13 on one device; ranks emulated sequentially, no cross-waiting)."""
+    spec = SMALL[4]
+    N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c = _case(spec)
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=0.0, device=0)
+    xd = torch.from_numpy(x).to(DEV)
+    T = plan.forward(xd)
+    whole = plan.inverse(T)
+    F = plan.frames
+    cuts = [0, F // 3, (2 * F) // 3 + 5, F]
+    y = torch.zeros(N, dtype=torch.float32, device=DEV)
+    for fb, fe in zip(cuts[:-1], cuts[1:]):
+        lo = max(0, fb * hop - c)
+        hi = min(N, (fe - 1) * hop - c + L)
+        part = torch.zeros(hi - lo, dtype=torch.float32, device=DEV)
+        plan.inverse_accumulate(T[fb:fe].contiguous(), fb, fe, part, y_off=lo)
+        y[lo:hi] += part
+    plan.inverse_finalize(y, 0)
+    assert rel(y.cpu().numpy(), whole.cpu().numpy()) <= 1e-6
+
+
+def test_c1_full(P):
+    """configs[0] (C1) end to end at full size: STFT, T, flips, reconstruction."""
+    cfg = get_config("C1")
+    x = signal("C1")
+    g, gd, c = O.gaussian_window(cfg.L, cfg.sigma)
+    gamma = config_gamma(cfg, x)
+    plan = make_plan(P, cfg, gamma)
+    xd = torch.from_numpy(x).to(DEV)
+    T = plan.forward(xd)
+    y = plan.inverse(T)
+    lg = plan.targets(xd).cpu().numpy()
+    To, S, Sd, lo = O.sst_forward(x.astype(np.float64), g, gd, c, cfg.hop, cfg.nfft, cfg.fs, cfg.f1, cfg.f2,
+                                  cfg.zoom, gamma, debug=True)
+    _, _, fhat = O.if_estimate(S, Sd, cfg.nfft, gamma)
+    st = flip_stats(lg, lo, S, fhat, cfg.k1, cfg.zoom)
+    Tg = T.cpu().numpy()
+    assert rel(Tg, To) <= 1e-3, st
+    assert st["frac"] <= 1e-4 and st["far_big"] <= 1e-4, st
+    yo = O.sst_inverse(To, g, c, cfg.hop, cfg.nfft, cfg.zoom, cfg.k1, cfg.N)
+    assert rel(y.cpu().numpy(), yo) <= 1e-4
+
+
+def _windows(F, n, size, seed):
+    rng = np.random.default_rng(seed)
+    starts = sorted(set([0, F - size] + list(rng.integers(0, F - size, size=n - 2))))
+    return [(int(s), int(s) + size) for s in starts]
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C5"])
+def test_config_sampled_frames(P, name):
+    """Full-size configs in the bench's launch configuration, compared on sampled frame windows
+    (both record edges included) that the oracle computes one by one."""
+    cfg = get_config(name)
+    x = signal(name)
+    g, gd, c = O.gaussian_window(cfg.L, cfg.sigma)
+    gamma = config_gamma(cfg, x)
+    plan = make_plan(P, cfg, gamma)
+    xd = torch.from_numpy(x).to(DEV)
+    F = cfg.frames
+    if name == "C5":
+        wins = _windows(F, 6, 512, 5)     # T of C5 is 256 GiB: forward the windows only
+        Tw = {w: plan.forward(xd, *w).cpu().numpy() for w in wins}
+    else:
+        T = plan.forward(xd)
+        wins = _windows(F, 6, 512, 5)
+        Tw = {w: T[w[0]:w[1]].cpu().numpy() for w in wins}
+        del T
+    x64 = x.astype(np.float64)
+    for w in wins:
+        fr = np.arange(*w)
+        To, S, Sd, lo = O.sst_forward(x64, g, gd, c, cfg.hop, cfg.nfft, cfg.fs, cfg.f1, cfg.f2, cfg.zoom,
+                                      gamma, frames=fr, debug=True)
+        assert rel(Tw[w], To) <= 1e-3, (name, w)
+        lg = plan.targets(xd, *w).cpu().numpy()
+        _, _, fhat = O.if_estimate(S, Sd, cfg.nfft, gamma)
+        st = flip_stats(lg, lo, S, fhat, cfg.k1, cfg.zoom)
+        assert st["frac"] <= 1e-4 and st["far_big"] <= 1e-4, (name, w, st)
+
+
+@pytest.mark.parametrize("name", ["C3"])
+def test_config_inverse_sampled(P, name):
+    """Full-size inverse (bench launch config) vs the oracle on sampled output windows, using the
+    GPU's T rows covering each window (isolates the inverse kernel)."""
+    cfg = get_config(name)
+    x = signal(name)
+    g, gd, c = O.gaussian_window(cfg.L, cfg.sigma)
+    plan = make_plan(P, cfg, config_gamma(cfg, x))
+    xd = torch.from_numpy(x).to(DEV)
+    T = plan.forward(xd)
+    y = plan.inverse(T).cpu().numpy()
+    rng = np.random.default_rng(3)
+    for n0 in [0, cfg.N - 4000] + list(rng.integers(0, cfg.N - 4000, size=3)):
+        n0 = int(n0)
+        n1 = n0 + 4000
+        fb = max(0, (n0 + c - cfg.L) // cfg.hop)
+        fe = min(cfg.frames, (n1 - 1 + c) // cfg.hop + 1)
+        Tn = T[fb:fe].cpu().numpy().astype(np.complex128)
+        yo = O.sst_inverse(Tn, g, c, cfg.hop, cfg.nfft, cfg.zoom, cfg.k1, cfg.N, frame_begin=fb, n0=n0, n1=n1)
+        assert rel(y[n0:n1], yo) <= 1e-4, n0
+
+
+def test_error_codes(P):
+    spec = SMALL[3]
+    N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c = _case(spec)
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=0.0, device=0)
+    xd = torch.from_numpy(x).to(DEV)
+    with pytest.raises(P.SSTError) as e:
+        plan.forward(xd, 5, 5)
+    assert e.value.status == P.SST_E_INVALID_ARGUMENT
+    with pytest.raises(P.SSTError):
+        plan.forward(xd, 0, plan.frames + 1)
+    with pytest.raises(P.SSTError):
+        plan.forward(xd[100:], 0, 10, x_off=100)       # slice does not cover frame 0
+    bad = torch.empty((plan.frames, plan.bins - 1), dtype=torch.complex64, device=DEV)
+    with pytest.raises(P.SSTError):
+        plan.forward(xd, out=bad)
+    with pytest.raises(TypeError):
+        plan.forward(xd.double())
