@@ -350,16 +350,23 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
     if ((s = ensure_w64(device, msg)) != SST_OK) { delete pl; return fail(nullptr, s, msg); }
 
     const double alpha = pl->lay.alpha;
-    std::vector<float2> taps(L), tw(Nf), twz((size_t)z * Nf);
+    // tw[k1 * N2 + t] = W_N^{t k1} (four-step twiddle, laid out so a warp's lanes t read
+    // consecutive entries); twz[(b-1) L + tau + c] = exp(+2 pi i b tau / (z N)), b = 1..z-1
+    const int32_t N2 = Nf / 64;
+    std::vector<float2> taps(L), tw(Nf), twz((size_t)std::max(1, z - 1) * L);
     for (int32_t j = 0; j < L; ++j) taps[j] = make_float2((float)pl->g[j], (float)(alpha * pl->gd[j]));
-    for (int32_t i = 0; i < Nf; ++i) {
-        const double a = -2.0 * kPi * i / Nf;
-        tw[i] = make_float2((float)std::cos(a), (float)std::sin(a));
-    }
-    for (int64_t e = 0; e < (int64_t)z * Nf; ++e) {
-        const double a = 2.0 * kPi * (double)e / ((double)z * Nf);
-        twz[e] = make_float2((float)std::cos(a), (float)std::sin(a));
-    }
+    for (int32_t k1 = 0; k1 < 64; ++k1)
+        for (int32_t t = 0; t < N2; ++t) {
+            const double a = -2.0 * kPi * (double)((int64_t)t * k1 % Nf) / Nf;
+            tw[(size_t)k1 * N2 + t] = make_float2((float)std::cos(a), (float)std::sin(a));
+        }
+    for (int32_t b = 1; b < z; ++b)
+        for (int32_t j = 0; j < L; ++j) {
+            const int64_t tau = j - c;
+            const int64_t e = (((int64_t)b * tau) % ((int64_t)z * Nf) + (int64_t)z * Nf) % ((int64_t)z * Nf);
+            const double a = 2.0 * kPi * (double)e / ((double)z * Nf);
+            twz[(size_t)(b - 1) * L + j] = make_float2((float)std::cos(a), (float)std::sin(a));
+        }
     // 1/(C d[n]): head [0, n_head), tail [N - n_tail, N), interior periodic in (n + c) mod H
     pl->n_head = (int32_t)std::min<int64_t>(N, L);
     pl->n_tail = (int32_t)std::min<int64_t>(N, (int64_t)L + H);

@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kCtaThreads, (N2 <= 32 ? 3 : 2)) fwd_kernel(co
 #pragma unroll
         for (int k1 = 0; k1 < 64; ++k1) {
             float2 t = v[k1];
-            if (k1 != 0) t = cmul(t, __ldg(a.tw + tg * k1));
+            if (k1 != 0) t = cmul(t, __ldg(a.tw + k1 * N2 + tg));   // W_N^{tg k1}, lane-contiguous
             buf[k1 * STRIDE + tg] = t;
         }
         group_sync<N2>(group);
@@ -315,7 +315,6 @@ __global__ void __launch_bounds__(kCtaThreads, 2) inv_kernel(const InvArgs a) {
     const bool first_cta = (blockIdx.x == 0);
     const bool last_cta = (f_hi == F);
     const int64_t H = a.hop;
-    const int zN = a.zoom * N;
     const int last_in = a.L - 1 - a.c;
 
     for (int i = threadIdx.x; i < a.ring; i += kCtaThreads) ring[i] = 0.0f;
@@ -361,7 +360,7 @@ __global__ void __launch_bounds__(kCtaThreads, 2) inv_kernel(const InvArgs a) {
 #pragma unroll
             for (int k1 = 0; k1 < 64; ++k1) {
                 float2 t = v[k1];
-                if (k1 != 0) t = cmulc(t, __ldg(a.tw + tg * k1));   // W_N^{-tg k1}
+                if (k1 != 0) t = cmulc(t, __ldg(a.tw + k1 * N2 + tg));   // W_N^{-tg k1}
                 buf[k1 * STRIDE + tg] = t;
             }
             group_sync<N2>(group);
@@ -379,11 +378,7 @@ __global__ void __launch_bounds__(kCtaThreads, 2) inv_kernel(const InvArgs a) {
                     const int tau = (p <= last_in) ? p : p - N;
                     if (tau < -a.c) continue;
                     float2 y = u[k2];
-                    if (b != 0) {
-                        int e = (b * tau) % zN;
-                        if (e < 0) e += zN;
-                        y = cmul(y, __ldg(a.twz + e));
-                    }
+                    if (b != 0) y = cmul(y, __ldg(a.twz + (int64_t)(b - 1) * a.L + (tau + a.c)));   // e^{i2pi b tau/(zN)}
                     const float gw = __ldg(&a.taps[tau + a.c].x) * a.inv_n;
                     if (vA) atomicAdd(&ring[(sA + tau) & rmask], gw * y.x);
                     if (vB) atomicAdd(&ring[(sB + tau) & rmask], gw * y.y);
