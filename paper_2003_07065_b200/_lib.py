@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsst.so")
+LIB_PATH = os.environ.get("SST_LIB_PATH") or os.path.join(_HERE, "libsst.so")   # override: dev A/B builds only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

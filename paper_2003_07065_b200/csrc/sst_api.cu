@@ -39,7 +39,6 @@ struct sst_plan {
     float* d_seam = nullptr;        // [inv_max_grid][2][seam_len]
     int32_t n_head = 0, n_tail = 0;
     int fwd_grid = 0, inv_grid = 0;
-    int ring = 0;
     const float* ext_absmax = nullptr;
     double gamma_abs = 0;
     std::string err;
@@ -230,10 +229,11 @@ sst_status check_frames(sst_plan* pl, int64_t fb, int64_t fe) {
     return SST_OK;
 }
 
-sst::FwdArgs fwd_args(const sst_plan* pl, const float* x, int64_t x_off, int64_t fb, int64_t fe) {
+sst::FwdArgs fwd_args(const sst_plan* pl, const float* x, int64_t x_off, int64_t x_len, int64_t fb, int64_t fe) {
     sst::FwdArgs a{};
     a.x = x;
     a.x_off = x_off;
+    a.x_len = x_len;
     a.n = pl->lay.n;
     a.frame_begin = fb;
     a.frame_end = fe;
@@ -256,11 +256,12 @@ sst::FwdArgs fwd_args(const sst_plan* pl, const float* x, int64_t x_off, int64_t
     a.gamma_rel = (float)pl->p.gamma;
     a.r_scale = (float)(pl->lay.nfft / (2.0 * kPi * pl->lay.alpha));
     a.inv_alpha2 = (float)(1.0 / (2.0 * pl->lay.alpha));
+    a.lay = sst::fwd_layout(pl->lay.nfft / 64, pl->lay.win_len, pl->lay.hop);
     return a;
 }
 
 int fwd_grid_for(const sst_plan* pl, int64_t nfr) {
-    const int G = sst::kCtaThreads / (pl->lay.nfft / 64);
+    const int G = sst::groups_of(pl->lay.nfft / 64);
     const int64_t tiles = (nfr + G - 1) / G;
     return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, pl->fwd_grid));
 }
@@ -388,9 +389,8 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
     }
     cudaError_t ce = cudaMalloc((void**)&pl->d_absmax, sizeof(float));
     if (ce != cudaSuccess) { delete pl; cudaGetLastError(); return fail(nullptr, SST_E_OUT_OF_MEMORY, "cudaMalloc absmax"); }
-    pl->fwd_grid = sst::forward_max_grid(Nf, device);
-    pl->inv_grid = sst::inverse_max_grid(Nf, H, L, device);
-    sst::inverse_smem_bytes(Nf, H, L, &pl->ring);
+    pl->fwd_grid = sst::forward_max_grid(Nf, L, H, device);
+    pl->inv_grid = sst::inverse_max_grid(Nf, H, L, z, device);
     const int32_t seam_len = std::max(0, L - H);
     if (seam_len > 0) {
         ce = cudaMalloc((void**)&pl->d_seam, sizeof(float) * (size_t)pl->inv_grid * 2 * seam_len);
@@ -461,7 +461,7 @@ sst_status sst_forward(sst_plan* plan, const float* x, int64_t x_off, int64_t x_
     if (x_len < 0 || !covers_input(plan, x_off, x_len, frame_begin, frame_end))
         return fail(plan, SST_E_INVALID_ARGUMENT, "x slice does not cover the frames' samples");
     DeviceGuard guard(plan->device);
-    sst::FwdArgs a = fwd_args(plan, x - 0, x_off, frame_begin, frame_end);
+    sst::FwdArgs a = fwd_args(plan, x, x_off, x_len, frame_begin, frame_end);
     a.T = reinterpret_cast<float2*>(T);
     a.ldT = ldT;
     return run_forward_mode(plan, sst::kModeForward, x, x_off, x_len, frame_begin, frame_end, a, stream);
@@ -476,7 +476,7 @@ sst_status sst_stft(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len
     if (x_len < 0 || !covers_input(plan, x_off, x_len, fb, fe))
         return fail(plan, SST_E_INVALID_ARGUMENT, "x slice does not cover the frames' samples");
     DeviceGuard guard(plan->device);
-    sst::FwdArgs a = fwd_args(plan, x, x_off, fb, fe);
+    sst::FwdArgs a = fwd_args(plan, x, x_off, x_len, fb, fe);
     a.S = reinterpret_cast<float2*>(S);
     a.Sd = reinterpret_cast<float2*>(Sd);
     a.gamma2x4 = -1.0f;   // report every bin
@@ -495,7 +495,7 @@ sst_status sst_targets(sst_plan* plan, const float* x, int64_t x_off, int64_t x_
     if (x_len < 0 || !covers_input(plan, x_off, x_len, fb, fe))
         return fail(plan, SST_E_INVALID_ARGUMENT, "x slice does not cover the frames' samples");
     DeviceGuard guard(plan->device);
-    sst::FwdArgs a = fwd_args(plan, x, x_off, fb, fe);
+    sst::FwdArgs a = fwd_args(plan, x, x_off, x_len, fb, fe);
     a.lout = l;
     return run_forward_mode(plan, sst::kModeTargets, x, x_off, x_len, fb, fe, a, stream);
 }
@@ -512,7 +512,7 @@ sst_status sst_absmax(sst_plan* plan, const float* x, int64_t x_off, int64_t x_l
     cudaStream_t st = (cudaStream_t)stream;
     s = cuda_status(plan, cudaMemsetAsync(out, 0, sizeof(float), st), "memset");
     if (s != SST_OK) return s;
-    sst::FwdArgs a = fwd_args(plan, x, x_off, fb, fe);
+    sst::FwdArgs a = fwd_args(plan, x, x_off, x_len, fb, fe);
     a.absmax_out = out;
     a.gamma2x4 = -1.0f;
     return cuda_status(plan, sst::launch_forward(a, sst::kModeAbsmax, fwd_grid_for(plan, fe - fb), st), "absmax launch");
@@ -548,7 +548,7 @@ static sst::InvArgs inv_args(const sst_plan* pl, const float* T, int64_t ldT, in
     a.inv_per = pl->d_inv_per;
     a.seam = pl->d_seam;
     a.seam_len = std::max(0, pl->lay.win_len - pl->lay.hop);
-    a.ring = pl->ring;
+    a.lay = sst::inv_layout(pl->lay.nfft / 64, pl->lay.win_len, pl->lay.hop, pl->lay.zoom);
     const int64_t F = fe - fb;
     const int64_t min_fpc = (pl->lay.win_len + pl->lay.hop - 1) / pl->lay.hop;
     int64_t fpc = (F + pl->inv_grid - 1) / pl->inv_grid;

@@ -1,5 +1,5 @@
-// Internal interface between the host API (sst_api.cu) and the kernels (sst_forward.cu,
-// sst_inverse.cu).  Not part of the ABI.
+// Internal interface between the host API (sst_api.cu) and the kernels (sst_kernels.cu).
+// Not part of the ABI.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -7,27 +7,64 @@
 
 namespace sst {
 
-constexpr int kCtaThreads = 128;        // threads per CTA for both kernels
-constexpr int kMinLogN = 7;             // N_f = 64 * N2, N2 in [2, 64]
-constexpr int kMaxLogN = 12;
-
 enum FwdMode : int { kModeForward = 0, kModeStft = 1, kModeTargets = 2, kModeAbsmax = 3 };
+
+// Threads per CTA: 128, or 256 for N_f = 4096 (two-warp frames).  G = TPB / N2 frames
+// (forward) or frame pairs (inverse) in flight per CTA, N_f = 64 N2.
+__host__ __device__ constexpr int tpb_of(int n2) { return n2 == 64 ? 256 : 128; }
+__host__ __device__ constexpr int groups_of(int n2) { return tpb_of(n2) / n2; }
+__host__ __device__ constexpr int cap_of(int n2) { return 64 * (n2 + 1); }   // float2 per group buffer
+__host__ __device__ constexpr int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// forward dynamic shared memory: [G exchange buffers][taps L float2][2 input tiles][2 mbarriers]
+struct FwdLayout {
+    int taps_off, xb_off, mbar_off, xcap, total;
+};
+__host__ __device__ inline FwdLayout fwd_layout(int n2, int L, int H) {
+    FwdLayout f{};
+    const int G = groups_of(n2);
+    f.taps_off = G * cap_of(n2) * 8;
+    f.xb_off = f.taps_off + round_up(L * 8, 16);
+    f.xcap = round_up((G - 1) * H + L + 8, 4);          // floats per input tile buffer
+    f.mbar_off = f.xb_off + 2 * f.xcap * 4;
+    f.total = f.mbar_off + 16;
+    return f;
+}
+
+// inverse dynamic shared memory: [G exchange buffers][window g, L floats][OLA ring]
+struct InvLayout {
+    int g_off, ring_off, ring, pairs, total;
+};
+__host__ __device__ inline InvLayout inv_layout(int n2, int L, int H, int zoom) {
+    InvLayout v{};
+    const int G = groups_of(n2);
+    v.pairs = G / zoom > 1 ? G / zoom : 1;
+    v.g_off = G * cap_of(n2) * 8;
+    v.ring_off = v.g_off + round_up(L * 4, 16);
+    const int span = (2 * v.pairs - 1) * H + L;
+    int r = 1;
+    while (r < span) r <<= 1;
+    v.ring = r;
+    v.total = v.ring_off + r * 4;
+    return v;
+}
 
 struct FwdArgs {
     const float* x;          // points at global sample x_off
-    int64_t x_off;
+    int64_t x_off, x_len;
     int64_t n;               // N
     int64_t frame_begin, frame_end;
     int32_t hop, L, c, nfft;
     const float2* taps;      // [L] (g, alpha g')
-    const float2* tw;        // [nfft] W_N^i = exp(-2 pi i i/N)
+    const float2* tw;        // [nfft] tw[k1 * N2 + t] = W_N^{t k1}
     int32_t k1, k2, bins, zoom;
     int32_t src_lo, src_hi;  // source bins reassigned: [src_lo, src_hi) (truncate flag)
-    float gamma2x4;          // 4 gamma^2 (mask on P^2 + Q^2 = 4|S|^2), used if gamma_dev == null
+    float gamma2x4;          // 4 gamma^2 (mask on P^2 + Q^2 = 4|S|^2), used if absmax_dev == null
     const float* absmax_dev; // relative mode: gamma = gamma_rel * (*absmax_dev)
     float gamma_rel;
     float r_scale;           // N_f / (2 pi alpha)
     float inv_alpha2;        // 1 / (2 alpha)
+    FwdLayout lay;
     // outputs
     float2* T; int64_t ldT;
     float2* S; float2* Sd;   // kModeStft
@@ -41,9 +78,10 @@ struct InvArgs {
     int64_t frame_begin, frame_end;   // frames in this launch; T row 0 = frame_begin
     int32_t hop, L, c, nfft, zoom, k1, bins;
     const float2* taps;               // .x = g
-    const float2* tw;                 // [nfft] W_N^i forward (conj used)
-    const float2* twz;                // [zoom*nfft] exp(+2 pi i e/(z N))
+    const float2* tw;                 // [nfft] tw[k1 * N2 + t] = W_N^{t k1} (conjugated here)
+    const float2* twz;                // [(zoom-1) L] exp(+2 pi i b tau/(z N)), b = 1..z-1, index tau + c
     float inv_n;                      // 1 / N_f
+    InvLayout lay;
     // output
     float* y; int64_t y_off, y_len;
     int normalize;                    // 1: write x_hat = sum / (C d) (y overwritten); 0: y += sum
@@ -53,21 +91,18 @@ struct InvArgs {
     float* seam;                      // [ctas][2][seam_len] partial sums
     int32_t seam_len;                 // L - hop
     int64_t frames_per_cta;           // contiguous chunk per CTA (>= ceil(L/hop))
-    int32_t ring;                     // ring buffer length (power of two)
 };
 
 // launchers (return cudaGetLastError())
 cudaError_t launch_forward(const FwdArgs& a, int mode, int grid, cudaStream_t s);
-int forward_smem_bytes(int nfft);
-int forward_max_grid(int nfft, int device);
+int forward_max_grid(int nfft, int L, int H, int device);
 
 cudaError_t launch_inverse(const InvArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_inverse_seams(const InvArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_finalize(float* y, int64_t y_off, int64_t y_len, int64_t n, int32_t hop, int32_t c,
                             const float* inv_head, int32_t n_head, const float* inv_tail, int32_t n_tail,
                             const float* inv_per, cudaStream_t s);
-int inverse_smem_bytes(int nfft, int hop, int L, int* ring_out);
-int inverse_max_grid(int nfft, int hop, int L, int device);
+int inverse_max_grid(int nfft, int hop, int L, int zoom, int device);
 
 // constant-memory table W_64^e (forward), uploaded once per device by the API
 cudaError_t upload_w64(const float2* w64_host);

@@ -1,27 +1,38 @@
 // sm_100a kernels of the fast downsampled SST (He & Cao, arXiv 2003.07065).
 //
 // Forward (one fused persistent kernel, rows a1-a7 of DESIGN.md §1):
-//   frame m, packed buffer z[n] = x[m H + tau] (g[tau+c] + i alpha g'[tau+c]), n = tau mod N_f
-//   (circular placement == Eq. 9's phase factor e^{i 2 pi k M/N_f});
-//   N_f = 64 * N2 four-step FFT: N2 threads per frame, each thread a 64-point register DFT of
-//   the decimated row n2 = thread, twiddle W_N^{n2 k1}, one padded shared-memory exchange,
-//   then N2-point register DFTs of columns.  Columns are assigned in conjugate pairs
-//   (k1, 64-k1) so that Z[k] and Z[N-k] meet in one thread (N2 <= 32), which makes the
-//   unpack S = (Z[k] + conj Z[N-k])/2, S' = (Z[k] - conj Z[N-k])/(2 i alpha) register-only.
+//   Each CTA walks a contiguous chunk of frames in tiles of G frames.  The tile's input span
+//   ((G-1) H + L samples) is copied HBM -> shared memory with one cp.async.bulk (TMA bulk copy)
+//   completed on an mbarrier, double-buffered so tile t+1 streams in while tile t computes; the
+//   window taps (g, alpha g') stay resident in shared memory.
+//   Frame m: packed buffer z[n] = x[m H + tau] (g[tau+c] + i alpha g'[tau+c]), n = tau mod N_f
+//   (circular placement == Eq. 9's phase factor e^{i 2 pi k M/N_f}).
+//   N_f = 64 N2 four-step FFT: N2 threads per frame, each a 64-point register DFT of the decimated
+//   row n2 = thread, twiddle W_N^{n2 k1}, one padded shared-memory exchange, then N2-point register
+//   DFTs of columns.  Columns are assigned in conjugate pairs (k1, 64-k1) so that Z[k] and Z[N-k]
+//   meet in one thread (N2 <= 32): the unpack S = (Z[k] + conj Z[N-k])/2,
+//   S' = (Z[k] - conj Z[N-k])/(2 i alpha) is register-only.
 //   Per source bin: mask |S| > gamma (Eq. 13), r = -Im(S'/S) N/(2 pi) (Eq. 36), target
 //   l = z(k-k1) + floor(z r + 1/2) (Eq. 28, R17), shared-memory atomics into the frame's band
 //   accumulator (Eq. 27/28), coalesced store of the band row.
 //
-// Inverse (rows a9-a11): two frames per complex IFFT (Hermitian packing), the z N_f-point
-//   band IDFT of P:L222 split into z N_f-point sub-transforms by residue b = j mod z, outer
-//   phase e^{i 2 pi b tau/(z N)}, real/imag -> the two frames, x g[tau+c] / N_f, OLA in a
-//   shared-memory ring per CTA (Eq. 26); samples shared with the neighbouring CTA go to a
-//   seam buffer combined by a second tiny kernel.
+// Inverse (rows a9-a11): two frames per complex IFFT (Hermitian packing), the z N_f-point band
+//   IDFT of P:L222 split into z N_f-point sub-transforms by residue b = j mod z; work item =
+//   (frame pair, b), one per group; outer phase e^{i 2 pi b tau/(z N)}; the CTA sums a pair's
+//   items, windows by g[tau+c]/N_f and overlap-adds frame A (real part) and frame B (imaginary
+//   part) into a shared-memory ring (Eq. 26).  Samples shared with the neighbouring CTA go to a
+//   seam buffer combined by a second small kernel.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "fft.cuh"
 #include "sst_internal.h"
+
+#ifdef SST_DEV_N2
+#define SST_HAS(n2) ((n2) == SST_DEV_N2)
+#else
+#define SST_HAS(n2) 1
+#endif
 
 namespace sst {
 
@@ -32,9 +43,10 @@ cudaError_t upload_w64(const float2* w64_host) {
 template <int N2>
 struct Geom {
     static constexpr int N = 64 * N2;
-    static constexpr int G = kCtaThreads / N2;   // frames (forward) / frame pairs (inverse) per CTA
+    static constexpr int TPB = tpb_of(N2);
+    static constexpr int G = groups_of(N2);
     static constexpr int STRIDE = N2 + 1;         // padded exchange row (odd -> conflict-free)
-    static constexpr int CAP = 64 * STRIDE;       // float2 per group buffer
+    static constexpr int CAP = cap_of(N2);        // float2 per group buffer
 };
 
 template <int N2>
@@ -46,57 +58,117 @@ __device__ __forceinline__ void group_sync(int group) {
     }
 }
 
-// ------------------------------------------------------------------------------- forward ------
-struct BinCtx {
-    float gam4, r_scale;
-    int k1, bins, zoom, src_lo, src_hi;
-};
+// ------------------------------------------------------------------------ TMA bulk copy helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// one-dimensional bulk copy global -> shared, completion counted on bar (bytes % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 
+// ------------------------------------------------------------------------------- forward ------
 // Per source bin k with Za = Z[k], Zb = Z[N-k]: returns target l (>= 0), -1 masked, -2 out of band.
 // S = (P, Q)/2 with P = Re Za + Re Zb, Q = Im Za - Im Zb;  S' = (U, -V)/(2 alpha) with
 // U = Im Za + Im Zb, V = Re Za - Re Zb;  -Im(S'/S) = (V P + U Q) / (alpha (P^2 + Q^2)).
-__device__ __forceinline__ int bin_target(const BinCtx& b, int k, float2 za, float2 zb, float& P, float& Q,
-                                          float& U, float& V, float& mag4) {
+__device__ __forceinline__ int bin_target(const FwdArgs& a, float gam4, int k, float2 za, float2 zb, float& P,
+                                          float& Q, float& U, float& V, float& mag4) {
     P = za.x + zb.x;
     Q = za.y - zb.y;
     U = za.y + zb.y;
     V = za.x - zb.x;
-    mag4 = fmaf(P, P, Q * Q);                       // 4 |S|^2
-    if (!(mag4 > b.gam4) || k < b.src_lo || k >= b.src_hi) return -1;
-    const float r = (fmaf(V, P, U * Q) / mag4) * b.r_scale;   // RF in coarse bins (Eq. 36)
-    const float zr = (float)b.zoom * r;
-    if (!(fabsf(zr) <= 1073741824.0f)) return -2;   // non-finite or huge (R17)
-    int l;
-    if (r >= -(float)k) l = b.zoom * (k - b.k1) + (int)floorf(zr + 0.5f);
-    else                l = -b.zoom * (k + b.k1) + (int)floorf(0.5f - zr);   // |k + r| = -(k + r) (Eq. 13 abs)
-    return (l >= 0 && l < b.bins) ? l : -2;
+    mag4 = fmaf(P, P, Q * Q);                                 // 4 |S|^2
+    if (!(mag4 > gam4) || k < a.src_lo || k >= a.src_hi) return -1;
+    const float r = __fdividef(fmaf(V, P, U * Q), mag4) * a.r_scale;   // RF in coarse bins (Eq. 36)
+    const float zr = (float)a.zoom * r;
+    if (!(fabsf(zr) <= 1073741824.0f)) return -2;             // non-finite or huge (R17)
+    const bool pos = r >= -(float)k;                          // k + r >= 0
+    const int base = pos ? a.zoom * (k - a.k1) : -a.zoom * (k + a.k1);   // |k + r| = -(k + r) otherwise
+    const int l = base + (int)floorf(pos ? zr + 0.5f : 0.5f - zr);
+    return ((unsigned)l < (unsigned)a.bins) ? l : -2;
+}
+
+// Tile t of a CTA covers frames [fb + t G, fb + t G + G) and input samples [s_lo, s_hi).  It is
+// fetched with one bulk copy when the 16-byte aligned span lies inside the valid x slice;
+// otherwise (record / slice edges, misaligned x) the CTA loads it cooperatively with zero fill.
+struct TileIn {
+    int64_t s_lo, a_lo;   // first sample; first copied x index (aligned)
+    int pad, bytes;       // s_lo - (x_off + a_lo); bytes of the bulk copy
+    bool bulk;
+};
+
+template <int G>
+__device__ __forceinline__ TileIn tile_in(const FwdArgs& a, int64_t t, bool x_aligned) {
+    TileIn ti;
+    const int64_t f = a.frame_begin + t * G;
+    ti.s_lo = f * a.hop - a.c;
+    const int64_t s_hi = (f + G - 1) * a.hop - a.c + a.L;
+    const int64_t v_lo = a.x_off > 0 ? a.x_off : 0;
+    const int64_t v_hi = min(a.n, a.x_off + a.x_len);
+    const int64_t d0 = ti.s_lo - a.x_off;
+    ti.a_lo = d0 - (((d0 % 4) + 4) % 4);
+    const int64_t a_hi = (s_hi - a.x_off + 3) / 4 * 4;
+    ti.pad = (int)(d0 - ti.a_lo);
+    ti.bytes = (int)((a_hi - ti.a_lo) * 4);
+    ti.bulk = x_aligned && a.x_off + ti.a_lo >= v_lo && a.x_off + a_hi <= v_hi && a_hi - ti.a_lo <= a.lay.xcap;
+    return ti;
 }
 
 // BIG: the band row (B bins) does not fit the group's exchange buffer (B > CAP): bins are kept
-// in registers and squeezed in chunks of CAP.  Otherwise (N2 <= 32) all column data is read
-// into registers first and the exchange buffer is reused as the band accumulator.
-template <int N2, int MODE, bool BIG>
-__global__ void __launch_bounds__(kCtaThreads, (N2 <= 32 ? 3 : 2)) fwd_kernel(const FwdArgs a) {
+// in registers and squeezed in chunks of CAP.  Otherwise (N2 <= 32) all column data is read into
+// registers first and the exchange buffer is reused as the band accumulator.
+// FULLWIN: L == N_f and c == N_f/2 (all of C2-C5): the packed index n = N2 n1 + tg maps to
+// tau = n (n1 < 32) or n - N (n1 >= 32) at compile time, so the gather has no checks.
+template <int N2, int MODE, bool BIG, bool FULLWIN>
+__global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) fwd_kernel(const FwdArgs a) {
     using Gm = Geom<N2>;
     constexpr int N = Gm::N;
+    constexpr int TPB = Gm::TPB;
     constexpr int STRIDE = Gm::STRIDE;
     constexpr int CAP = Gm::CAP;
     constexpr int G = Gm::G;
     constexpr int NB = 33;                         // source bins per thread (+1 Nyquist slot)
-    extern __shared__ float2 smem[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float2* smem = reinterpret_cast<float2*>(smem_raw);
+    float2* taps_s = reinterpret_cast<float2*>(smem_raw + a.lay.taps_off);
+    float* xbuf = reinterpret_cast<float*>(smem_raw + a.lay.xb_off);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw + a.lay.mbar_off);
     const int group = threadIdx.x / N2;
     const int tg = threadIdx.x % N2;
     float2* buf = smem + group * CAP;
 
-    BinCtx bc;
+    float gam4 = a.gamma2x4;
     if (a.absmax_dev) {
         const float gm = a.gamma_rel * __ldg(a.absmax_dev);
-        bc.gam4 = 4.0f * gm * gm;
-    } else {
-        bc.gam4 = a.gamma2x4;
+        gam4 = 4.0f * gm * gm;
     }
-    bc.r_scale = a.r_scale;
-    bc.k1 = a.k1; bc.bins = a.bins; bc.zoom = a.zoom; bc.src_lo = a.src_lo; bc.src_hi = a.src_hi;
 
     const int64_t nfr = a.frame_end - a.frame_begin;
     const int64_t ntiles = (nfr + G - 1) / G;
@@ -104,27 +176,83 @@ __global__ void __launch_bounds__(kCtaThreads, (N2 <= 32 ? 3 : 2)) fwd_kernel(co
     const int64_t t_begin = (int64_t)blockIdx.x * tiles_per_cta;
     const int64_t t_end = min(ntiles, t_begin + tiles_per_cta);
     const int last_in = a.L - 1 - a.c;             // largest tau
+    const bool x_aligned = (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
     float vmax = 0.0f;
 
+    for (int i = threadIdx.x; i < a.L; i += TPB) taps_s[i] = __ldg(a.taps + i);
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && t_begin < t_end) {
+        const TileIn ti = tile_in<G>(a, t_begin, x_aligned);
+        if (ti.bulk) {
+            mbar_arrive_tx(&mbar[0], ti.bytes);
+            bulk_g2s(xbuf, a.x + ti.a_lo, ti.bytes, &mbar[0]);
+        }
+    }
+    uint32_t phase = 0;                            // bit b = parity of buffer b's next completion
+
     for (int64_t tile = t_begin; tile < t_end; ++tile) {
+        const int bsel = (int)((tile - t_begin) & 1);
+        float* xb = xbuf + bsel * a.lay.xcap;
+        // prefetch tile + 1 into the other buffer (freed by the barrier that ended tile - 1)
+        if (threadIdx.x == 0 && tile + 1 < t_end) {
+            const TileIn tn = tile_in<G>(a, tile + 1, x_aligned);
+            if (tn.bulk) {
+                fence_proxy_async();
+                mbar_arrive_tx(&mbar[bsel ^ 1], tn.bytes);
+                bulk_g2s(xbuf + (bsel ^ 1) * a.lay.xcap, a.x + tn.a_lo, tn.bytes, &mbar[bsel ^ 1]);
+            }
+        }
+        const TileIn ti = tile_in<G>(a, tile, x_aligned);
+        int pad = ti.pad;
+        if (ti.bulk) {
+            mbar_wait(&mbar[bsel], (phase >> bsel) & 1);
+            phase ^= 1u << bsel;
+        } else {
+            const int64_t v_lo = a.x_off > 0 ? a.x_off : 0;
+            const int64_t v_hi = min(a.n, a.x_off + a.x_len);
+            const int span = (G - 1) * a.hop + a.L;
+            for (int i = threadIdx.x; i < span; i += TPB) {
+                const int64_t s = ti.s_lo + i;
+                xb[i] = (s >= v_lo && s < v_hi) ? __ldg(a.x + (s - a.x_off)) : 0.0f;
+            }
+            pad = 0;
+            __syncthreads();
+        }
+
         const int64_t fi = tile * G + group;       // frame index within the launch
         const bool valid = fi < nfr;
-        const int64_t sbase = (a.frame_begin + fi) * a.hop - a.x_off;   // x index of tau = 0
+        const float* xw = xb + pad + group * a.hop; // x[m H - c + j], j = 0..L-1 (j = tau + c)
 
         // ---- a1: gather + pack (circular placement), a2 step 1: 64-point DFT of row tg
         float2 v[64];
+        if constexpr (FULLWIN) {
+            const float* xt = xw + tg;
+            const float2* wt = taps_s + tg;
 #pragma unroll
-        for (int n1 = 0; n1 < 64; ++n1) {
-            const int n = N2 * n1 + tg;
-            const int tau = (n <= last_in) ? n : n - N;
-            float2 val = make_float2(0.0f, 0.0f);
-            const int64_t s = sbase + tau + a.x_off;             // global sample
-            if (valid && tau >= -a.c && s >= 0 && s < a.n) {
-                const float xs = __ldg(a.x + (sbase + tau));
-                const float2 w = __ldg(a.taps + (tau + a.c));
-                val = make_float2(xs * w.x, xs * w.y);
+            for (int n1 = 0; n1 < 64; ++n1) {
+                const int j = N2 * n1 + (n1 < 32 ? N / 2 : -N / 2);   // tau + c - tg (compile time)
+                const float xs = xt[j];
+                const float2 w = wt[j];
+                v[n1] = make_float2(xs * w.x, xs * w.y);
             }
-            v[n1] = val;
+        } else {
+#pragma unroll
+            for (int n1 = 0; n1 < 64; ++n1) {
+                const int n = N2 * n1 + tg;
+                const int j = ((n <= last_in) ? n : n - N) + a.c;
+                float2 val = make_float2(0.0f, 0.0f);
+                if (j >= 0) {
+                    const float xs = xw[j];
+                    const float2 w = taps_s[j];
+                    val = make_float2(xs * w.x, xs * w.y);
+                }
+                v[n1] = val;
+            }
         }
         Fft<64, -1>::run(v);
 #pragma unroll
@@ -142,7 +270,7 @@ __global__ void __launch_bounds__(kCtaThreads, (N2 <= 32 ? 3 : 2)) fwd_kernel(co
         float bsr[STORE ? NB : 1], bsi[STORE ? NB : 1];
         auto on_bin = [&](int idx, int k, float2 za, float2 zb, bool ok) {
             float P, Q, U, V, mag4;
-            int l = bin_target(bc, k, za, zb, P, Q, U, V, mag4);
+            int l = bin_target(a, gam4, k, za, zb, P, Q, U, V, mag4);
             if (!ok || !valid) l = -3;
             if constexpr (STORE) {
                 bl[idx] = l;
@@ -244,11 +372,10 @@ __global__ void __launch_bounds__(kCtaThreads, (N2 <= 32 ? 3 : 2)) fwd_kernel(co
         group_sync<N2>(group);
 
         // ---- a7 band store (DIRECT), or a6 + a7 in chunks of CAP bins (STORE)
-        float2* trow = (MODE == kModeForward) ? reinterpret_cast<float2*>(a.T) + fi * a.ldT : nullptr;
+        float2* trow = (MODE == kModeForward) ? a.T + fi * a.ldT : nullptr;
         if constexpr (DIRECT) {
             if (valid)
                 for (int i = tg; i < a.bins; i += N2) trow[i] = buf[i];
-            group_sync<N2>(group);
         }
         if constexpr (STORE) {
             for (int l0 = 0; l0 < a.bins; l0 += CAP) {
@@ -269,19 +396,20 @@ __global__ void __launch_bounds__(kCtaThreads, (N2 <= 32 ? 3 : 2)) fwd_kernel(co
                 group_sync<N2>(group);
             }
         }
+        __syncthreads();   // tile input buffer and group buffers free for the next tile
     }
 
     if constexpr (MODE == kModeAbsmax) {
         // block max of 4|S|^2 -> |S|
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
-        __shared__ float red[kCtaThreads / 32];
+        __shared__ float red[TPB / 32];
         __syncthreads();
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = vmax;
         __syncthreads();
         if (threadIdx.x == 0) {
             float m = 0.0f;
-            for (int w = 0; w < kCtaThreads / 32; ++w) m = fmaxf(m, red[w]);
+            for (int w = 0; w < TPB / 32; ++w) m = fmaxf(m, red[w]);
             atomicMax(reinterpret_cast<unsigned int*>(a.absmax_out), __float_as_uint(0.5f * sqrtf(m)));
         }
     }
@@ -294,19 +422,28 @@ __device__ __forceinline__ float inv_norm(int64_t s, const InvArgs& a) {
     return __ldg(a.inv_per + (int)((s + a.c) % a.hop));
 }
 
-template <int N2>
-__global__ void __launch_bounds__(kCtaThreads, 2) inv_kernel(const InvArgs a) {
+// Work item = (frame pair, residue b).  A tile holds P = max(1, G/z) consecutive frame pairs, so
+// its P z items occupy the G groups in ceil(P z / G) passes (one pass for every config here).
+// Per item the group computes V_b = IDFT_N of the Hermitian-packed sub-spectrum
+// G_b[q] = H_A[z q + b] + i H_B[z q + b] and leaves e^{i 2 pi b tau/(z N)} V_b[p] in its buffer
+// (indexed by p = tau mod N).  The CTA then sums the items of each pair over b, windows by
+// g[tau + c]/N and adds frame A (real part) and frame B (imaginary part) into the OLA ring.
+template <int N2, bool FULLWIN>
+__global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) inv_kernel(const InvArgs a) {
     using Gm = Geom<N2>;
     constexpr int N = Gm::N;
+    constexpr int TPB = Gm::TPB;
     constexpr int STRIDE = Gm::STRIDE;
     constexpr int CAP = Gm::CAP;
     constexpr int G = Gm::G;
-    extern __shared__ float2 smem[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float2* smem = reinterpret_cast<float2*>(smem_raw);
+    float* g_s = reinterpret_cast<float*>(smem_raw + a.lay.g_off);
+    float* ring = reinterpret_cast<float*>(smem_raw + a.lay.ring_off);
     const int group = threadIdx.x / N2;
     const int tg = threadIdx.x % N2;
     float2* buf = smem + group * CAP;
-    float* ring = reinterpret_cast<float*>(smem + G * CAP);
-    const int64_t rmask = a.ring - 1;
+    const int rmask = a.lay.ring - 1;
 
     const int64_t F = a.frame_end - a.frame_begin;
     const int64_t f_lo = (int64_t)blockIdx.x * a.frames_per_cta;
@@ -315,84 +452,119 @@ __global__ void __launch_bounds__(kCtaThreads, 2) inv_kernel(const InvArgs a) {
     const bool first_cta = (blockIdx.x == 0);
     const bool last_cta = (f_hi == F);
     const int64_t H = a.hop;
-    const int last_in = a.L - 1 - a.c;
+    const int c = a.c;
+    const int last_in = a.L - 1 - c;
+    const int zoom = a.zoom;
+    const int P = a.lay.pairs;                            // frame pairs per tile
+    const int items = P * zoom;
+    const int k1 = a.k1;
+    const int nr = a.bins / zoom;                          // N_r
+    const float inv_n = a.inv_n;
 
-    for (int i = threadIdx.x; i < a.ring; i += kCtaThreads) ring[i] = 0.0f;
+    for (int i = threadIdx.x; i < a.lay.ring; i += TPB) ring[i] = 0.0f;
+    for (int i = threadIdx.x; i < a.L; i += TPB) g_s[i] = __ldg(&a.taps[i].x) * inv_n;
     __syncthreads();
 
-    const int64_t g_lo = (a.frame_begin + f_lo) * H - a.c;           // first sample touched
-    const int64_t left_end = g_lo + a.seam_len;                        // [g_lo, left_end) = left seam
-    const int64_t right_start = (a.frame_begin + f_hi) * H - a.c;     // [right_start, ..) = right seam
+    const int64_t g_lo = (a.frame_begin + f_lo) * H - c;            // first sample touched
+    const int64_t left_end = g_lo + a.seam_len;                      // [g_lo, left_end) = left seam
+    const int64_t right_start = (a.frame_begin + f_hi) * H - c;     // [right_start, ..) = right seam
     int64_t flushed = g_lo;
-    const int k2band = a.k1 + a.bins / a.zoom;
 
-    for (int64_t f0 = f_lo; f0 < f_hi; f0 += 2 * G) {
-        const int64_t fA = f0 + 2 * group, fB = fA + 1;
-        const bool vA = fA < f_hi, vB = fB < f_hi;
-        const float2* TA = a.T + fA * a.ldT;
-        const float2* TB = a.T + fB * a.ldT;
-        const int64_t sA = (a.frame_begin + fA) * H, sB = sA + H;      // sample of tau = 0
-
-        for (int b = 0; b < a.zoom; ++b) {
-            // ---- a9: sub-spectrum G_b[q] = H_A[z q + b] + i H_B[z q + b] (Hermitian pair pack)
+    for (int64_t f0 = f_lo; f0 < f_hi; f0 += 2 * P) {
+        for (int it0 = 0; it0 < items; it0 += G) {
+            // ---------------- per-group item: sub-IFFT of one (pair, b)
+            const int item = it0 + group;
+            const int pair = item / zoom, b = item - pair * zoom;
+            const int64_t fA = f0 + 2 * pair;
+            const bool vA = item < items && fA < f_hi;
+            const bool vB = vA && fA + 1 < f_hi;
+            const float2* TA = a.T + (vA ? fA : f_lo) * a.ldT;
+            const float2* TB = vB ? TA + a.ldT : TA;
             float2 v[64];
 #pragma unroll
             for (int n1 = 0; n1 < 64; ++n1) {
-                const int q = N2 * n1 + tg;
-                float2 val = make_float2(0.0f, 0.0f);
-                if (q >= a.k1 && q < k2band) {
-                    const int l = a.zoom * (q - a.k1) + b;
-                    float2 ta = vA ? __ldg(TA + l) : make_float2(0.0f, 0.0f);
-                    float2 tb = vB ? __ldg(TB + l) : make_float2(0.0f, 0.0f);
-                    if (q == 0 && b == 0) { ta.y = 0.0f; tb.y = 0.0f; }    // DC: not doubled (R14)
-                    val = make_float2(ta.x - tb.y, ta.y + tb.x);
-                } else {
-                    const int lm = a.zoom * (N - a.k1 - q) - b;            // conj mirror (R14)
-                    if (lm >= 0 && lm < a.bins) {
-                        const float2 ta = vA ? __ldg(TA + lm) : make_float2(0.0f, 0.0f);
-                        const float2 tb = vB ? __ldg(TB + lm) : make_float2(0.0f, 0.0f);
-                        val = make_float2(ta.x + tb.y, tb.x - ta.y);
-                    }
-                }
-                v[n1] = val;
+                const int q = N2 * n1 + tg;                       // sub-spectrum index (coarse bin)
+                const int ib = q - k1;                            // band: j = z q + b = z k1 + l
+                const bool inb = (unsigned)ib < (unsigned)nr;
+                const int lm = zoom * (N - k1 - q) - b;           // mirror: j = z N - (z k1 + l')
+                const bool inm = !inb && q > 0 && (unsigned)lm < (unsigned)a.bins;
+                const int li = inb ? zoom * ib + b : lm;
+                float2 ta = make_float2(0.0f, 0.0f), tb = make_float2(0.0f, 0.0f);
+                if ((inb || inm) && vA) ta = __ldg(TA + li);
+                if ((inb || inm) && vB) tb = __ldg(TB + li);
+                if (q == 0 && b == 0) { ta.y = 0.0f; tb.y = 0.0f; }  // DC: real part only (R14)
+                v[n1] = inb ? make_float2(ta.x - tb.y, ta.y + tb.x)    // H_A + i H_B
+                            : make_float2(ta.x + tb.y, tb.x - ta.y);   // conj H_A + i conj H_B
             }
             Fft<64, +1>::run(v);
 #pragma unroll
-            for (int k1 = 0; k1 < 64; ++k1) {
-                float2 t = v[k1];
-                if (k1 != 0) t = cmulc(t, __ldg(a.tw + k1 * N2 + tg));   // W_N^{-tg k1}
-                buf[k1 * STRIDE + tg] = t;
+            for (int kk = 0; kk < 64; ++kk) {
+                float2 t = v[kk];
+                if (kk != 0) t = cmulc(t, __ldg(a.tw + kk * N2 + tg));   // W_N^{-tg kk}
+                buf[kk * STRIDE + tg] = t;
             }
             group_sync<N2>(group);
             constexpr int COLS = 64 / N2;
+            float2 u[COLS][N2];
+#pragma unroll
+            for (int ci = 0; ci < COLS; ++ci)
+#pragma unroll
+                for (int n2 = 0; n2 < N2; ++n2) u[ci][n2] = buf[(tg + N2 * ci) * STRIDE + n2];
+            group_sync<N2>(group);
+            const bool rot = b != 0;
+            const float2* tz = a.twz + (rot ? (b - 1) : 0) * a.L + c;       // index by tau
 #pragma unroll
             for (int ci = 0; ci < COLS; ++ci) {
                 const int col = tg + N2 * ci;
-                float2 u[N2];
-#pragma unroll
-                for (int n2 = 0; n2 < N2; ++n2) u[n2] = buf[col * STRIDE + n2];
-                Fft<N2, +1>::run(u);
+                Fft<N2, +1>::run(u[ci]);
+                const float2* tzc = tz + col;
 #pragma unroll
                 for (int k2 = 0; k2 < N2; ++k2) {
-                    const int p = col + 64 * k2;                 // output index tau mod N
-                    const int tau = (p <= last_in) ? p : p - N;
-                    if (tau < -a.c) continue;
-                    float2 y = u[k2];
-                    if (b != 0) y = cmul(y, __ldg(a.twz + (int64_t)(b - 1) * a.L + (tau + a.c)));   // e^{i2pi b tau/(zN)}
-                    const float gw = __ldg(&a.taps[tau + a.c].x) * a.inv_n;
-                    if (vA) atomicAdd(&ring[(sA + tau) & rmask], gw * y.x);
-                    if (vB) atomicAdd(&ring[(sB + tau) & rmask], gw * y.y);
+                    const int p = col + 64 * k2;                  // output index tau mod N
+                    float2 y = u[ci][k2];
+                    if constexpr (FULLWIN) {
+                        // tau = p (k2 < N2/2) or p - N: compile-time split
+                        const int toff = 64 * k2 - (k2 < N2 / 2 ? 0 : N);
+                        if (rot) y = cmul(y, __ldg(tzc + toff));   // e^{i 2 pi b tau/(z N)}
+                    } else {
+                        const int tau = (p <= last_in) ? p : p - N;
+                        if (rot && tau >= -c) y = cmul(y, __ldg(tz + tau));
+                    }
+                    buf[p] = y;
                 }
             }
-            group_sync<N2>(group);
+            __syncthreads();
+            // ---------------- combine the items of each pair over b, window, OLA into the ring
+            const int pr_lo = it0 / zoom, pr_hi = min(P, (it0 + G + zoom - 1) / zoom);
+            for (int pr = pr_lo; pr < pr_hi; ++pr) {
+                const int64_t fa = f0 + 2 * pr;
+                if (fa >= f_hi) break;
+                const bool hasB = fa + 1 < f_hi;
+                const int i_lo = max(it0, pr * zoom) - it0, i_hi = min(it0 + G, pr * zoom + zoom) - it0;
+                const int64_t sA = (a.frame_begin + fa) * H;
+                for (int p = threadIdx.x; p < N; p += TPB) {
+                    const int tau = (p <= last_in) ? p : p - N;
+                    if (tau < -c) continue;
+                    float2 y = smem[i_lo * CAP + p];
+                    for (int i = i_lo + 1; i < i_hi; ++i) {
+                        const float2 t = smem[i * CAP + p];
+                        y.x += t.x;
+                        y.y += t.y;
+                    }
+                    const float gw = g_s[tau + c];
+                    const int slot = (int)((sA + tau) & rmask);
+                    atomicAdd(&ring[slot], gw * y.x);
+                    if (hasB) atomicAdd(&ring[(slot + (int)H) & rmask], gw * y.y);
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();
-        // ---- a10: flush completed samples
-        const int64_t f_next = f0 + 2 * G;
-        const int64_t next_lo = (f_next >= f_hi) ? (a.frame_begin + f_hi - 1) * H - a.c + a.L
-                                                 : (a.frame_begin + f_next) * H - a.c;
-        for (int64_t s = flushed + threadIdx.x; s < next_lo; s += kCtaThreads) {
-            float* slot = &ring[s & rmask];
+        // ---------------- a10: flush completed samples
+        const int64_t f_next = f0 + 2 * P;
+        const int64_t next_lo = (f_next >= f_hi) ? (a.frame_begin + f_hi - 1) * H - c + a.L
+                                                 : (a.frame_begin + f_next) * H - c;
+        for (int64_t s = flushed + threadIdx.x; s < next_lo; s += TPB) {
+            float* slot = &ring[(int)(s & rmask)];
             const float val = *slot;
             *slot = 0.0f;
             if (s < 0 || s >= a.n) continue;
@@ -435,31 +607,27 @@ __global__ void finalize_kernel(float* y, int64_t y_off, int64_t y_len, InvArgs 
 }
 
 // ------------------------------------------------------------------------------- launchers ----
-template <int N2>
-static int fwd_smem() { return Geom<N2>::G * Geom<N2>::CAP * (int)sizeof(float2); }
-
-template <int N2>
-static int inv_smem(int hop, int L, int* ring_out) {
-    const int span = (2 * Geom<N2>::G - 1) * hop + L;
-    int ring = 1;
-    while (ring < span) ring <<= 1;
-    if (ring_out) *ring_out = ring;
-    return Geom<N2>::G * Geom<N2>::CAP * (int)sizeof(float2) + ring * (int)sizeof(float);
+template <int N2, int MODE, bool BIG, bool FULLWIN>
+static cudaError_t launch_fwd_b(const FwdArgs& a, int grid, cudaStream_t s) {
+    auto kern = fwd_kernel<N2, MODE, BIG, FULLWIN>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, a.lay.total);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, Geom<N2>::TPB, a.lay.total, s>>>(a);
+    return cudaGetLastError();
 }
 
 template <int N2, int MODE, bool BIG>
-static cudaError_t launch_fwd_b(const FwdArgs& a, int grid, cudaStream_t s) {
-    const int smem = fwd_smem<N2>();
-    cudaError_t e = cudaFuncSetAttribute(fwd_kernel<N2, MODE, BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    fwd_kernel<N2, MODE, BIG><<<grid, kCtaThreads, smem, s>>>(a);
-    return cudaGetLastError();
+static cudaError_t launch_fwd_w(const FwdArgs& a, int grid, cudaStream_t s) {
+    if (a.L == Geom<N2>::N && a.c == Geom<N2>::N / 2) return launch_fwd_b<N2, MODE, BIG, true>(a, grid, s);
+    return launch_fwd_b<N2, MODE, BIG, false>(a, grid, s);
 }
 
 template <int N2, int MODE>
 static cudaError_t launch_fwd_t(const FwdArgs& a, int grid, cudaStream_t s) {
-    if (MODE == kModeForward && N2 <= 32 && a.bins > Geom<N2>::CAP) return launch_fwd_b<N2, MODE, true>(a, grid, s);
-    return launch_fwd_b<N2, MODE, false>(a, grid, s);
+    if constexpr (MODE == kModeForward && N2 <= 32) {
+        if (a.bins > Geom<N2>::CAP) return launch_fwd_w<N2, MODE, true>(a, grid, s);
+    }
+    return launch_fwd_w<N2, MODE, false>(a, grid, s);
 }
 
 template <int N2>
@@ -475,67 +643,62 @@ static cudaError_t launch_fwd_mode(const FwdArgs& a, int mode, int grid, cudaStr
 
 cudaError_t launch_forward(const FwdArgs& a, int mode, int grid, cudaStream_t s) {
     switch (a.nfft) {
-        case 128: return launch_fwd_mode<2>(a, mode, grid, s);
-        case 256: return launch_fwd_mode<4>(a, mode, grid, s);
-        case 512: return launch_fwd_mode<8>(a, mode, grid, s);
-        case 1024: return launch_fwd_mode<16>(a, mode, grid, s);
-        case 2048: return launch_fwd_mode<32>(a, mode, grid, s);
-        case 4096: return launch_fwd_mode<64>(a, mode, grid, s);
+        case 128: if constexpr (SST_HAS(2)) return launch_fwd_mode<2>(a, mode, grid, s); break;
+        case 256: if constexpr (SST_HAS(4)) return launch_fwd_mode<4>(a, mode, grid, s); break;
+        case 512: if constexpr (SST_HAS(8)) return launch_fwd_mode<8>(a, mode, grid, s); break;
+        case 1024: if constexpr (SST_HAS(16)) return launch_fwd_mode<16>(a, mode, grid, s); break;
+        case 2048: if constexpr (SST_HAS(32)) return launch_fwd_mode<32>(a, mode, grid, s); break;
+        case 4096: if constexpr (SST_HAS(64)) return launch_fwd_mode<64>(a, mode, grid, s); break;
     }
     return cudaErrorInvalidValue;
 }
 
-int forward_smem_bytes(int nfft) {
-    switch (nfft) {
-        case 128: return fwd_smem<2>();
-        case 256: return fwd_smem<4>();
-        case 512: return fwd_smem<8>();
-        case 1024: return fwd_smem<16>();
-        case 2048: return fwd_smem<32>();
-        case 4096: return fwd_smem<64>();
-    }
-    return -1;
-}
-
 template <int N2>
-static int occ_fwd(int device) {
+static int occ_fwd(int L, int H, int device) {
     int nb = 0, sms = 0;
-    const int smem = fwd_smem<N2>();
-    cudaFuncSetAttribute(fwd_kernel<N2, kModeForward, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fwd_kernel<N2, kModeForward, false>, kCtaThreads, smem);
+    const int smem = fwd_layout(N2, L, H).total;
+    auto kern = fwd_kernel<N2, kModeForward, false, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Geom<N2>::TPB, smem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     return (nb > 0 ? nb : 1) * sms;
 }
 
-int forward_max_grid(int nfft, int device) {
+int forward_max_grid(int nfft, int L, int H, int device) {
     switch (nfft) {
-        case 128: return occ_fwd<2>(device);
-        case 256: return occ_fwd<4>(device);
-        case 512: return occ_fwd<8>(device);
-        case 1024: return occ_fwd<16>(device);
-        case 2048: return occ_fwd<32>(device);
-        case 4096: return occ_fwd<64>(device);
+        case 128: if constexpr (SST_HAS(2)) return occ_fwd<2>(L, H, device); break;
+        case 256: if constexpr (SST_HAS(4)) return occ_fwd<4>(L, H, device); break;
+        case 512: if constexpr (SST_HAS(8)) return occ_fwd<8>(L, H, device); break;
+        case 1024: if constexpr (SST_HAS(16)) return occ_fwd<16>(L, H, device); break;
+        case 2048: if constexpr (SST_HAS(32)) return occ_fwd<32>(L, H, device); break;
+        case 4096: if constexpr (SST_HAS(64)) return occ_fwd<64>(L, H, device); break;
     }
     return -1;
 }
 
+template <int N2, bool FULLWIN>
+static cudaError_t launch_inv_b(const InvArgs& a, int grid, cudaStream_t s) {
+    auto kern = inv_kernel<N2, FULLWIN>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, a.lay.total);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, Geom<N2>::TPB, a.lay.total, s>>>(a);
+    return cudaGetLastError();
+}
+
 template <int N2>
 static cudaError_t launch_inv_t(const InvArgs& a, int grid, cudaStream_t s) {
-    const int smem = inv_smem<N2>(a.hop, a.L, nullptr);
-    cudaError_t e = cudaFuncSetAttribute(inv_kernel<N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    inv_kernel<N2><<<grid, kCtaThreads, smem, s>>>(a);
-    return cudaGetLastError();
+    if (a.L == Geom<N2>::N && a.c == Geom<N2>::N / 2) return launch_inv_b<N2, true>(a, grid, s);
+    return launch_inv_b<N2, false>(a, grid, s);
 }
 
 cudaError_t launch_inverse(const InvArgs& a, int grid, cudaStream_t s) {
     switch (a.nfft) {
-        case 128: return launch_inv_t<2>(a, grid, s);
-        case 256: return launch_inv_t<4>(a, grid, s);
-        case 512: return launch_inv_t<8>(a, grid, s);
-        case 1024: return launch_inv_t<16>(a, grid, s);
-        case 2048: return launch_inv_t<32>(a, grid, s);
-        case 4096: return launch_inv_t<64>(a, grid, s);
+        case 128: if constexpr (SST_HAS(2)) return launch_inv_t<2>(a, grid, s); break;
+        case 256: if constexpr (SST_HAS(4)) return launch_inv_t<4>(a, grid, s); break;
+        case 512: if constexpr (SST_HAS(8)) return launch_inv_t<8>(a, grid, s); break;
+        case 1024: if constexpr (SST_HAS(16)) return launch_inv_t<16>(a, grid, s); break;
+        case 2048: if constexpr (SST_HAS(32)) return launch_inv_t<32>(a, grid, s); break;
+        case 4096: if constexpr (SST_HAS(64)) return launch_inv_t<64>(a, grid, s); break;
     }
     return cudaErrorInvalidValue;
 }
@@ -544,7 +707,8 @@ cudaError_t launch_inverse_seams(const InvArgs& a, int ctas, cudaStream_t s) {
     if (ctas < 2 || a.seam_len <= 0) return cudaSuccess;
     const int64_t total = (int64_t)(ctas - 1) * a.seam_len;
     const int threads = 256;
-    const int blocks = (int)((total + threads - 1) / threads < 4096 ? (total + threads - 1) / threads : 4096);
+    const int64_t want = (total + threads - 1) / threads;
+    const int blocks = (int)(want < 4096 ? want : 4096);
     seam_kernel<<<blocks, threads, 0, s>>>(a, ctas);
     return cudaGetLastError();
 }
@@ -556,42 +720,32 @@ cudaError_t launch_finalize(float* y, int64_t y_off, int64_t y_len, int64_t n, i
     a.n = n; a.hop = hop; a.c = c;
     a.inv_head = inv_head; a.n_head = n_head; a.inv_tail = inv_tail; a.n_tail = n_tail; a.inv_per = inv_per;
     const int threads = 256;
-    const int blocks = (int)((y_len + threads - 1) / threads < 2368 ? (y_len + threads - 1) / threads : 2368);
+    const int64_t want = (y_len + threads - 1) / threads;
+    const int blocks = (int)(want < 2368 ? want : 2368);
     if (blocks <= 0) return cudaSuccess;
     finalize_kernel<<<blocks, threads, 0, s>>>(y, y_off, y_len, a);
     return cudaGetLastError();
 }
 
-int inverse_smem_bytes(int nfft, int hop, int L, int* ring_out) {
-    switch (nfft) {
-        case 128: return inv_smem<2>(hop, L, ring_out);
-        case 256: return inv_smem<4>(hop, L, ring_out);
-        case 512: return inv_smem<8>(hop, L, ring_out);
-        case 1024: return inv_smem<16>(hop, L, ring_out);
-        case 2048: return inv_smem<32>(hop, L, ring_out);
-        case 4096: return inv_smem<64>(hop, L, ring_out);
-    }
-    return -1;
-}
-
 template <int N2>
-static int occ_inv(int hop, int L, int device) {
+static int occ_inv(int hop, int L, int zoom, int device) {
     int nb = 0, sms = 0;
-    const int smem = inv_smem<N2>(hop, L, nullptr);
-    cudaFuncSetAttribute(inv_kernel<N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, inv_kernel<N2>, kCtaThreads, smem);
+    const int smem = inv_layout(N2, L, hop, zoom).total;
+    auto kern = inv_kernel<N2, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Geom<N2>::TPB, smem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     return (nb > 0 ? nb : 1) * sms;
 }
 
-int inverse_max_grid(int nfft, int hop, int L, int device) {
+int inverse_max_grid(int nfft, int hop, int L, int zoom, int device) {
     switch (nfft) {
-        case 128: return occ_inv<2>(hop, L, device);
-        case 256: return occ_inv<4>(hop, L, device);
-        case 512: return occ_inv<8>(hop, L, device);
-        case 1024: return occ_inv<16>(hop, L, device);
-        case 2048: return occ_inv<32>(hop, L, device);
-        case 4096: return occ_inv<64>(hop, L, device);
+        case 128: if constexpr (SST_HAS(2)) return occ_inv<2>(hop, L, zoom, device); break;
+        case 256: if constexpr (SST_HAS(4)) return occ_inv<4>(hop, L, zoom, device); break;
+        case 512: if constexpr (SST_HAS(8)) return occ_inv<8>(hop, L, zoom, device); break;
+        case 1024: if constexpr (SST_HAS(16)) return occ_inv<16>(hop, L, zoom, device); break;
+        case 2048: if constexpr (SST_HAS(32)) return occ_inv<32>(hop, L, zoom, device); break;
+        case 4096: if constexpr (SST_HAS(64)) return occ_inv<64>(hop, L, zoom, device); break;
     }
     return -1;
 }
