@@ -264,8 +264,10 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) f
         group_sync<N2>(group);
 
         // ---- a2 step 2 + a3 unpack + a4/a5 per bin
-        constexpr bool STORE = (MODE == kModeForward) && (BIG || N2 > 32);   // keep bins, squeeze later
-        constexpr bool DIRECT = (MODE == kModeForward) && !STORE;           // squeeze while unpacking
+        // forward: bins are computed branch-free into registers (phase 1), then squeezed with
+        // predicated shared-memory atomics in chunks of CAP bins (phase 2; one chunk unless BIG)
+        constexpr bool STORE = (MODE == kModeForward);
+        constexpr bool DIRECT = false;
         int bl[STORE ? NB : 1];
         float bsr[STORE ? NB : 1], bsi[STORE ? NB : 1];
         auto on_bin = [&](int idx, int k, float2 za, float2 zb, bool ok) {
@@ -428,7 +430,10 @@ __device__ __forceinline__ float inv_norm(int64_t s, const InvArgs& a) {
 // G_b[q] = H_A[z q + b] + i H_B[z q + b] and leaves e^{i 2 pi b tau/(z N)} V_b[p] in its buffer
 // (indexed by p = tau mod N).  The CTA then sums the items of each pair over b, windows by
 // g[tau + c]/N and adds frame A (real part) and frame B (imaginary part) into the OLA ring.
-template <int N2, bool FULLWIN>
+// RM: every nonzero sub-spectrum entry q (band [k1, k2) or mirror [N - k2, N)) has
+// q / N2 in [0, RM) or [64 - RM, 64) (i.e. ceil(k2 / N2) <= RM): other rows of the step-1
+// input are compile-time zeros and cost nothing (narrow bands: C2, C3, C4 use RM = 8).
+template <int N2, bool FULLWIN, int RM>
 __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) inv_kernel(const InvArgs a) {
     using Gm = Geom<N2>;
     constexpr int N = Gm::N;
@@ -483,6 +488,10 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) i
             float2 v[64];
 #pragma unroll
             for (int n1 = 0; n1 < 64; ++n1) {
+                if (n1 >= RM && n1 < 64 - RM) {                   // outside band and mirror
+                    v[n1] = make_float2(0.0f, 0.0f);
+                    continue;
+                }
                 const int q = N2 * n1 + tg;                       // sub-spectrum index (coarse bin)
                 const int ib = q - k1;                            // band: j = z q + b = z k1 + l
                 const bool inb = (unsigned)ib < (unsigned)nr;
@@ -676,19 +685,27 @@ int forward_max_grid(int nfft, int L, int H, int device) {
     return -1;
 }
 
-template <int N2, bool FULLWIN>
+template <int N2, bool FULLWIN, int RM>
 static cudaError_t launch_inv_b(const InvArgs& a, int grid, cudaStream_t s) {
-    auto kern = inv_kernel<N2, FULLWIN>;
+    auto kern = inv_kernel<N2, FULLWIN, RM>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, a.lay.total);
     if (e != cudaSuccess) return e;
     kern<<<grid, Geom<N2>::TPB, a.lay.total, s>>>(a);
     return cudaGetLastError();
 }
 
+template <int N2, bool FULLWIN>
+static cudaError_t launch_inv_r(const InvArgs& a, int grid, cudaStream_t s) {
+    const int rows = (a.k1 + a.bins / a.zoom + N2 - 1) / N2;   // ceil(k2 / N2)
+    if (rows <= 8) return launch_inv_b<N2, FULLWIN, 8>(a, grid, s);
+    if (rows <= 16) return launch_inv_b<N2, FULLWIN, 16>(a, grid, s);
+    return launch_inv_b<N2, FULLWIN, 64>(a, grid, s);
+}
+
 template <int N2>
 static cudaError_t launch_inv_t(const InvArgs& a, int grid, cudaStream_t s) {
-    if (a.L == Geom<N2>::N && a.c == Geom<N2>::N / 2) return launch_inv_b<N2, true>(a, grid, s);
-    return launch_inv_b<N2, false>(a, grid, s);
+    if (a.L == Geom<N2>::N && a.c == Geom<N2>::N / 2) return launch_inv_r<N2, true>(a, grid, s);
+    return launch_inv_r<N2, false>(a, grid, s);
 }
 
 cudaError_t launch_inverse(const InvArgs& a, int grid, cudaStream_t s) {
@@ -731,7 +748,7 @@ template <int N2>
 static int occ_inv(int hop, int L, int zoom, int device) {
     int nb = 0, sms = 0;
     const int smem = inv_layout(N2, L, hop, zoom).total;
-    auto kern = inv_kernel<N2, true>;
+    auto kern = inv_kernel<N2, true, 64>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Geom<N2>::TPB, smem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
