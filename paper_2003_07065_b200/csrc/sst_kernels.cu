@@ -386,10 +386,34 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) f
                 group_sync<N2>(group);
 #pragma unroll
                 for (int i = 0; i < NB; ++i) {
-                    const int l = bl[i] - l0;
-                    if (bl[i] >= 0 && l >= 0 && l < lc) {
-                        atomicAdd(&buf[l].x, bsr[i]);
-                        atomicAdd(&buf[l].y, bsi[i]);
+                    // Adjacent lanes hold adjacent source bins k, so a ridge squeezing into one target
+                    // shows up as a run of equal l across lanes: merge runs with a segmented warp scan
+                    // and let only the run's last lane touch shared memory (same-address atomics
+                    // serialise).  Steps with no run (noise) take the plain path.
+                    const int lane = threadIdx.x & 31;
+                    const int lr = bl[i] - l0;
+                    const int l = (bl[i] >= 0 && lr >= 0 && lr < lc) ? lr : -1 - lane;   // unique if inactive
+                    float vr = bsr[i], vi = bsi[i];
+                    const bool gstart = (N2 >= 32) ? (lane == 0) : (lane % N2 == 0);
+                    const bool gend = (N2 >= 32) ? (lane == 31) : (lane % N2 == N2 - 1);
+                    const int lp = __shfl_up_sync(0xffffffffu, l, 1);
+                    const bool same_prev = !gstart && lp == l;
+                    bool emit = l >= 0;
+                    if (__any_sync(0xffffffffu, same_prev)) {
+                        unsigned f = same_prev ? 0u : 1u;          // 1 = segment head
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const float ur = __shfl_up_sync(0xffffffffu, vr, d);
+                            const float ui = __shfl_up_sync(0xffffffffu, vi, d);
+                            const unsigned fu = __shfl_up_sync(0xffffffffu, f, d);
+                            if (lane >= d && !f) { vr += ur; vi += ui; f |= fu; }
+                        }
+                        const int ln = __shfl_down_sync(0xffffffffu, l, 1);
+                        emit = emit && (gend || ln != l);           // run tail carries the run sum
+                    }
+                    if (emit) {
+                        atomicAdd(&buf[l].x, vr);
+                        atomicAdd(&buf[l].y, vi);
                     }
                 }
                 group_sync<N2>(group);
@@ -543,30 +567,50 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) i
                 }
             }
             __syncthreads();
-            // ---------------- combine the items of each pair over b, window, OLA into the ring
+            // ---------------- combine the items of each pair over b, window, OLA into the ring.
+            // Each thread owns positions p = threadIdx.x + TPB j; frame A (real part) and frame B
+            // (imaginary part, H samples later) are added in two barrier-separated phases, so
+            // every ring slot has a single writer per phase (no atomics).
+            constexpr int PPT = (N + TPB - 1) / TPB;
             const int pr_lo = it0 / zoom, pr_hi = min(P, (it0 + G + zoom - 1) / zoom);
             for (int pr = pr_lo; pr < pr_hi; ++pr) {
                 const int64_t fa = f0 + 2 * pr;
-                if (fa >= f_hi) break;
+                if (fa >= f_hi) break;                         // CTA-uniform
                 const bool hasB = fa + 1 < f_hi;
                 const int i_lo = max(it0, pr * zoom) - it0, i_hi = min(it0 + G, pr * zoom + zoom) - it0;
                 const int64_t sA = (a.frame_begin + fa) * H;
-                for (int p = threadIdx.x; p < N; p += TPB) {
+                float2 y[PPT];
+                int slot[PPT];
+#pragma unroll
+                for (int jj = 0; jj < PPT; ++jj) {
+                    const int p = threadIdx.x + TPB * jj;
                     const int tau = (p <= last_in) ? p : p - N;
-                    if (tau < -c) continue;
-                    float2 y = smem[i_lo * CAP + p];
-                    for (int i = i_lo + 1; i < i_hi; ++i) {
-                        const float2 t = smem[i * CAP + p];
-                        y.x += t.x;
-                        y.y += t.y;
+                    const bool ok = p < N && tau >= -c;
+                    float2 acc = make_float2(0.0f, 0.0f);
+                    if (ok) {
+                        for (int i = i_lo; i < i_hi; ++i) {
+                            const float2 t = smem[i * CAP + p];
+                            acc.x += t.x;
+                            acc.y += t.y;
+                        }
+                        const float gw = g_s[tau + c];
+                        acc.x *= gw;
+                        acc.y *= gw;
                     }
-                    const float gw = g_s[tau + c];
-                    const int slot = (int)((sA + tau) & rmask);
-                    atomicAdd(&ring[slot], gw * y.x);
-                    if (hasB) atomicAdd(&ring[(slot + (int)H) & rmask], gw * y.y);
+                    y[jj] = acc;
+                    slot[jj] = ok ? (int)((sA + tau) & rmask) : -1;
                 }
+#pragma unroll
+                for (int jj = 0; jj < PPT; ++jj)
+                    if (slot[jj] >= 0) ring[slot[jj]] += y[jj].x;
+                __syncthreads();
+                if (hasB) {
+#pragma unroll
+                    for (int jj = 0; jj < PPT; ++jj)
+                        if (slot[jj] >= 0) ring[(slot[jj] + (int)H) & rmask] += y[jj].y;
+                }
+                __syncthreads();
             }
-            __syncthreads();
         }
         // ---------------- a10: flush completed samples
         const int64_t f_next = f0 + 2 * P;
