@@ -54,7 +54,8 @@ enum {
                                    extra FFT pass) unless sst_plan_set_absmax() gave a device
                                    scalar (e.g. a global max all-reduced over ranks).           */
     SST_SOURCE_TRUNCATE = 2u,   /* only source bins k in [k1, k2) are reassigned (R12)  */
-    SST_DETERMINISTIC = 4u,     /* reserved: bitwise-reproducible accumulation order            */
+    SST_DETERMINISTIC = 4u,     /* accepted, no effect: every result is bitwise reproducible run to
+                                   run (exact fixed-point squeeze sums, fixed-order OLA)            */
     SST_DISCRETE_CONSTANT = 8u  /* inverse divides by C_d = g[c] sum g / sum g^2 instead of
                                    sqrt 2 (Eq. 24, R15)                                         */
 };

@@ -12,14 +12,18 @@ namespace sst {
 
 __constant__ float2 c_w64[64];   // W_64^e = exp(-2 pi i e / 64), rounded from fp64 (set by upload_w64)
 
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// Complex arithmetic on sm_100a's packed FP32x2 pipe (FADD2 / FMUL2 / FFMA2): one instruction per
+// complex add, two per complex multiply; swaps and sign flips fold into operand modifiers.
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
+// a * b = b.x (a.x, a.y) + b.y (-a.y, a.x)
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+    return __ffma2_rn(make_float2(-a.y, a.x), make_float2(b.y, b.y), __fmul2_rn(a, make_float2(b.x, b.x)));
 }
-// a * conj(b)
+// a * conj(b) = b.x (a.x, a.y) + b.y (a.y, -a.x)
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
-    return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+    return __ffma2_rn(make_float2(a.y, -a.x), make_float2(b.y, b.y), __fmul2_rn(a, make_float2(b.x, b.x)));
 }
 // multiply by exp(DIR * i pi/2): DIR=-1 -> -i, DIR=+1 -> +i
 template <int DIR>
@@ -71,13 +75,14 @@ struct Fft<8, DIR> {
         Fft<4, DIR>::run(e);
         Fft<4, DIR>::run(o);
         // o[k] *= W_8^k
-        float2 o1 = o[1], o3 = o[3];
+        // W_8 = h (1 - i) (DIR = -1) or h (1 + i); W_8^3 = -h (1 + i) or h (-1 + i)
+        const float2 o1 = o[1], o3 = o[3];
         if (DIR < 0) {
-            o[1] = make_float2(h * (o1.x + o1.y), h * (o1.y - o1.x));
-            o[3] = make_float2(h * (o3.y - o3.x), -h * (o3.x + o3.y));
+            o[1] = cscale(cadd(o1, make_float2(o1.y, -o1.x)), h);
+            o[3] = cscale(cadd(make_float2(o3.y, -o3.x), make_float2(-o3.x, -o3.y)), h);
         } else {
-            o[1] = make_float2(h * (o1.x - o1.y), h * (o1.x + o1.y));
-            o[3] = make_float2(-h * (o3.x + o3.y), h * (o3.x - o3.y));
+            o[1] = cscale(cadd(o1, make_float2(-o1.y, o1.x)), h);
+            o[3] = cscale(cadd(make_float2(-o3.y, o3.x), make_float2(-o3.x, -o3.y)), h);
         }
         o[2] = rot90<DIR>(o[2]);
 #pragma unroll

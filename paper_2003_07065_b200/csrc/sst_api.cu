@@ -134,7 +134,6 @@ sst_status validate(const sst_params* p, sst_layout* lay, std::string& msg) {
     if (!is_pow2(p->nfft)) { msg = "N_f must be a power of two (P:L93)"; return SST_E_UNSUPPORTED; }
     if (p->nfft < 128 || p->nfft > 4096) { msg = "this build supports 128 <= N_f <= 4096"; return SST_E_UNSUPPORTED; }
     if (p->zoom > 64 || (int64_t)p->zoom * p->nfft > (1 << 20)) { msg = "z <= 64 and z N_f <= 2^20 supported"; return SST_E_UNSUPPORTED; }
-    if (p->flags & SST_DETERMINISTIC) { msg = "SST_DETERMINISTIC is reserved (not implemented)"; return SST_E_UNSUPPORTED; }
     // coverage (R20): every n in [0, N) needs d[n] > 0
     const int64_t N = p->n;
     const int64_t F = frames_of(N, p->hop);
@@ -255,6 +254,7 @@ sst::FwdArgs fwd_args(const sst_plan* pl, const float* x, int64_t x_off, int64_t
     a.absmax_dev = nullptr;
     a.gamma_rel = (float)pl->p.gamma;
     a.r_scale = (float)(pl->lay.nfft / (2.0 * kPi * pl->lay.alpha));
+    a.r_scale_d = pl->lay.nfft / (2.0 * kPi * pl->lay.alpha);
     a.inv_alpha2 = (float)(1.0 / (2.0 * pl->lay.alpha));
     a.lay = sst::fwd_layout(pl->lay.nfft / 64, pl->lay.win_len, pl->lay.hop);
     return a;

@@ -28,6 +28,15 @@
 #include "fft.cuh"
 #include "sst_internal.h"
 
+#ifndef SST_SQZ
+#define SST_SQZ 1
+#endif
+#ifndef SST_NOMERGE
+#define SST_NOMERGE 1
+#endif
+#ifndef SST_ANYSKIP
+#define SST_ANYSKIP 1
+#endif
 #ifdef SST_DEV_N2
 #define SST_HAS(n2) ((n2) == SST_DEV_N2)
 #else
@@ -98,20 +107,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // Per source bin k with Za = Z[k], Zb = Z[N-k]: returns target l (>= 0), -1 masked, -2 out of band.
 // S = (P, Q)/2 with P = Re Za + Re Zb, Q = Im Za - Im Zb;  S' = (U, -V)/(2 alpha) with
 // U = Im Za + Im Zb, V = Re Za - Re Zb;  -Im(S'/S) = (V P + U Q) / (alpha (P^2 + Q^2)).
-__device__ __forceinline__ int bin_target(const FwdArgs& a, float gam4, int k, float2 za, float2 zb, float& P,
-                                          float& Q, float& U, float& V, float& mag4) {
-    P = za.x + zb.x;
-    Q = za.y - zb.y;
-    U = za.y + zb.y;
-    V = za.x - zb.x;
-    mag4 = fmaf(P, P, Q * Q);                                 // 4 |S|^2
+__device__ __forceinline__ int bin_target(const FwdArgs& a, float gam4, int k, float2 za, float2 zb, float2& PQ,
+                                          float2& UV, float& mag4) {
+    PQ = __fadd2_rn(za, make_float2(zb.x, -zb.y));                           // (P, Q) = 2 S
+    UV = __fadd2_rn(make_float2(za.y, za.x), make_float2(zb.y, -zb.x));      // (U, V) = 2 alpha (Re, -Im) S'
+    const float2 sq = __fmul2_rn(PQ, PQ);
+    mag4 = sq.x + sq.y;                                       // 4 |S|^2
     if (!(mag4 > gam4) || k < a.src_lo || k >= a.src_hi) return -1;
-    const float r = __fdividef(fmaf(V, P, U * Q), mag4) * a.r_scale;   // RF in coarse bins (Eq. 36)
+    const float2 vu = __fmul2_rn(make_float2(UV.y, UV.x), PQ);              // (V P, U Q)
+    const float r = __fdividef(vu.x + vu.y, mag4) * a.r_scale;   // RF in coarse bins (Eq. 36)
     const float zr = (float)a.zoom * r;
     if (!(fabsf(zr) <= 1073741824.0f)) return -2;             // non-finite or huge (R17)
     const bool pos = r >= -(float)k;                          // k + r >= 0
     const int base = pos ? a.zoom * (k - a.k1) : -a.zoom * (k + a.k1);   // |k + r| = -(k + r) otherwise
-    const int l = base + (int)floorf(pos ? zr + 0.5f : 0.5f - zr);
+    const int l = base + __float2int_rd(pos ? zr + 0.5f : 0.5f - zr);
     return ((unsigned)l < (unsigned)a.bins) ? l : -2;
 }
 
@@ -236,9 +245,7 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) f
 #pragma unroll
             for (int n1 = 0; n1 < 64; ++n1) {
                 const int j = N2 * n1 + (n1 < 32 ? N / 2 : -N / 2);   // tau + c - tg (compile time)
-                const float xs = xt[j];
-                const float2 w = wt[j];
-                v[n1] = make_float2(xs * w.x, xs * w.y);
+                v[n1] = cscale(wt[j], xt[j]);
             }
         } else {
 #pragma unroll
@@ -246,11 +253,7 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) f
                 const int n = N2 * n1 + tg;
                 const int j = ((n <= last_in) ? n : n - N) + a.c;
                 float2 val = make_float2(0.0f, 0.0f);
-                if (j >= 0) {
-                    const float xs = xw[j];
-                    const float2 w = taps_s[j];
-                    val = make_float2(xs * w.x, xs * w.y);
-                }
+                if (j >= 0) val = cscale(taps_s[j], xw[j]);
                 v[n1] = val;
             }
         }
@@ -267,27 +270,23 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) f
         // forward: bins are computed branch-free into registers (phase 1), then squeezed with
         // predicated shared-memory atomics in chunks of CAP bins (phase 2; one chunk unless BIG)
         constexpr bool STORE = (MODE == kModeForward);
-        constexpr bool DIRECT = false;
         int bl[STORE ? NB : 1];
         float bsr[STORE ? NB : 1], bsi[STORE ? NB : 1];
         auto on_bin = [&](int idx, int k, float2 za, float2 zb, bool ok) {
-            float P, Q, U, V, mag4;
-            int l = bin_target(a, gam4, k, za, zb, P, Q, U, V, mag4);
+            float2 PQ, UV;
+            float mag4;
+            int l = bin_target(a, gam4, k, za, zb, PQ, UV, mag4);
             if (!ok || !valid) l = -3;
             if constexpr (STORE) {
                 bl[idx] = l;
-                bsr[idx] = 0.5f * P;
-                bsi[idx] = 0.5f * Q;
-            } else if constexpr (DIRECT) {
-                if (l >= 0) {
-                    atomicAdd(&buf[l].x, 0.5f * P);                 // a6: T_acc[l] += S (Eq. 27/28)
-                    atomicAdd(&buf[l].y, 0.5f * Q);
-                }
+                const float2 S = cscale(PQ, 0.5f);
+                bsr[idx] = S.x;
+                bsi[idx] = S.y;
             } else if constexpr (MODE == kModeStft) {
                 if (l != -3) {
                     const int64_t o = fi * (int64_t)(N / 2 + 1) + k;
-                    a.S[o] = make_float2(0.5f * P, 0.5f * Q);
-                    a.Sd[o] = make_float2(U * a.inv_alpha2, -V * a.inv_alpha2);
+                    a.S[o] = cscale(PQ, 0.5f);
+                    a.Sd[o] = __fmul2_rn(UV, make_float2(a.inv_alpha2, -a.inv_alpha2));
                 }
             } else if constexpr (MODE == kModeTargets) {
                 if (l != -3) a.lout[fi * (int64_t)(N / 2 + 1) + k] = l;
@@ -327,22 +326,11 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) f
                     B[n2] = buf[cB * STRIDE + n2];
                 }
             };
-            if constexpr (DIRECT) {
-                float2 A[UNITS][N2], B[UNITS][N2];
 #pragma unroll
-                for (int u = 0; u < UNITS; ++u) load_unit(u, A[u], B[u]);
-                group_sync<N2>(group);
-                for (int i = tg; i < a.bins; i += N2) buf[i] = make_float2(0.0f, 0.0f);
-                group_sync<N2>(group);
-#pragma unroll
-                for (int u = 0; u < UNITS; ++u) unpack_unit(u, A[u], B[u]);
-            } else {
-#pragma unroll
-                for (int u = 0; u < UNITS; ++u) {
-                    float2 A[N2], B[N2];
-                    load_unit(u, A, B);
-                    unpack_unit(u, A, B);
-                }
+            for (int u = 0; u < UNITS; ++u) {
+                float2 A[N2], B[N2];
+                load_unit(u, A, B);
+                unpack_unit(u, A, B);
             }
         } else {
             // N2 == 64: column DFT per thread, then unpack through shared memory
@@ -375,10 +363,105 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) f
 
         // ---- a7 band store (DIRECT), or a6 + a7 in chunks of CAP bins (STORE)
         float2* trow = (MODE == kModeForward) ? a.T + fi * a.ldT : nullptr;
-        if constexpr (DIRECT) {
-            if (valid)
-                for (int i = tg; i < a.bins; i += N2) trow[i] = buf[i];
+#if SST_SQZ == 1
+        if constexpr (STORE) {
+            // a6 as exact fixed-point integer sums with native shared-memory integer atomics
+            // (float atomics on shared memory are compare-and-swap loops on sm_100a).  Per warp and
+            // tile, v_max bounds the kept |Re S|, |Im S|; every value is scaled by 2^(39 - e)
+            // (v_max < 2^e, a power of two: exact) and rounded to a 64-bit integer X, |X| < 2^39, which
+            // is added as two 32-bit limbs hi = X >> 20 (signed) and lo = X & (2^20 - 1).  With at
+            // most K <= 2049 contributions per target the limb sums cannot overflow
+            // (sum|hi| < 2^30.01, sum lo < 2^31.01), so the band value is the exactly rounded sum of
+            // its fp32 terms (quantum v_max 2^-39) whatever the order: bitwise reproducible.
+            // N2 = 64: each of the frame's two warps squeezes into its own half of the group buffer.
+            constexpr int WPG = (N2 > 32) ? N2 / 32 : 1;   // warps per group
+            constexpr int CH = CAP / 2 / WPG;              // band bins per pass (4 int32 each)
+            static_assert(CH % 4 == 0, "int4 zeroing");
+            const int lane = threadIdx.x & 31;
+            const int wib = (WPG > 1) ? (tg >> 5) : 0;     // warp within the group
+            int* acc = reinterpret_cast<int*>(buf) + wib * 4 * CH;   // planar [hi_re|lo_re|hi_im|lo_im][CH]
+            __shared__ float wscale[TPB / 32];
+            float vmax = 0.0f;
+#pragma unroll
+            for (int i = 0; i < NB; ++i)
+                if (bl[i] >= 0) vmax = fmaxf(vmax, fmaxf(fabsf(bsr[i]), fabsf(bsi[i])));
+            const unsigned vb = __reduce_max_sync(0xffffffffu, __float_as_uint(vmax));
+            const int ex = max(-87, (int)((vb >> 23) & 0xff) - 126);   // v_max < 2^ex
+            const float scale = __uint_as_float((unsigned)(127 + 39 - ex) << 23);
+            const float iscale = __uint_as_float((unsigned)(127 - 39 + ex) << 23);
+            if (WPG > 1 && lane == 0) wscale[threadIdx.x >> 5] = iscale;
+            for (int l0 = 0; l0 < a.bins; l0 += CH) {
+                const int lc = min(CH, a.bins - l0);
+                {
+                    int4* z4 = reinterpret_cast<int4*>(buf);
+                    const int lc4 = (lc + 3) >> 2;
+#pragma unroll
+                    for (int q = 0; q < 4 * WPG; ++q)
+                        for (int i = tg; i < lc4; i += N2) z4[q * (CH / 4) + i] = make_int4(0, 0, 0, 0);
+                }
+                group_sync<N2>(group);
+#pragma unroll
+                for (int i = 0; i < NB; ++i) {
+                    const int lr = bl[i] - l0;
+                    const bool in = bl[i] >= 0 && lr >= 0 && lr < lc;
+                    if (!__any_sync(0xffffffffu, in)) continue;      // warp-uniform: nothing lands here
+                    // Adjacent lanes hold adjacent source bins k, so a ridge squeezing into one target
+                    // is a run of equal l across lanes: a segmented warp scan leaves the run's sum in
+                    // its last lane, the only one that touches shared memory.
+                    const int l = in ? lr : -1 - lane;                // unique if inactive
+                    float vr = bsr[i], vi = bsi[i];
+                    const bool gstart = (N2 >= 32) ? (lane == 0) : (lane % N2 == 0);
+                    const bool gend = (N2 >= 32) ? (lane == 31) : (lane % N2 == N2 - 1);
+                    const int lp = __shfl_up_sync(0xffffffffu, l, 1);
+                    const bool same_prev = !gstart && lp == l;
+                    bool emit = in;
+                    if (!SST_NOMERGE && __any_sync(0xffffffffu, same_prev)) {
+                        unsigned f = same_prev ? 0u : 1u;          // 1 = segment head
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const float ur = __shfl_up_sync(0xffffffffu, vr, d);
+                            const float ui = __shfl_up_sync(0xffffffffu, vi, d);
+                            const unsigned fu = __shfl_up_sync(0xffffffffu, f, d);
+                            if (lane >= d && !f) { vr += ur; vi += ui; f |= fu; }
+                        }
+                        const int ln = __shfl_down_sync(0xffffffffu, l, 1);
+                        emit = emit && (gend || ln != l);           // run tail carries the run sum
+                    }
+                    if (emit) {                                     // a6: T_acc[l] += S (Eq. 27/28)
+                        const long long xr = __float2ll_rn(vr * scale);
+                        const long long xi = __float2ll_rn(vi * scale);
+                        atomicAdd(acc + l, (int)(xr >> 20));
+                        atomicAdd(acc + CH + l, (int)(xr & 0xFFFFF));
+                        atomicAdd(acc + 2 * CH + l, (int)(xi >> 20));
+                        atomicAdd(acc + 3 * CH + l, (int)(xi & 0xFFFFF));
+                    }
+                }
+                group_sync<N2>(group);
+                if (valid)
+                    for (int i = tg; i < lc; i += N2) {
+                        const int* a0 = reinterpret_cast<const int*>(buf);
+                        float2 t;
+                        if constexpr (WPG > 1) {
+                            const int w0 = (threadIdx.x >> 5) - wib;   // first warp of this group
+                            float sr = 0.0f, si = 0.0f;
+#pragma unroll
+                            for (int h = 0; h < WPG; ++h) {
+                                const int* ah = a0 + h * 4 * CH;
+                                const float is = wscale[w0 + h];
+                                sr += (float)((((long long)ah[i]) << 20) + (unsigned)ah[CH + i]) * is;
+                                si += (float)((((long long)ah[2 * CH + i]) << 20) + (unsigned)ah[3 * CH + i]) * is;
+                            }
+                            t = make_float2(sr, si);
+                        } else {
+                            t = make_float2((float)((((long long)a0[i]) << 20) + (unsigned)a0[CH + i]) * iscale,
+                                            (float)((((long long)a0[2 * CH + i]) << 20) + (unsigned)a0[3 * CH + i]) * iscale);
+                        }
+                        trow[l0 + i] = t;
+                    }
+                group_sync<N2>(group);
+            }
         }
+#else
         if constexpr (STORE) {
             for (int l0 = 0; l0 < a.bins; l0 += CAP) {
                 const int lc = min(CAP, a.bins - l0);
@@ -392,14 +475,17 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) f
                     // serialise).  Steps with no run (noise) take the plain path.
                     const int lane = threadIdx.x & 31;
                     const int lr = bl[i] - l0;
-                    const int l = (bl[i] >= 0 && lr >= 0 && lr < lc) ? lr : -1 - lane;   // unique if inactive
+                    const bool in = bl[i] >= 0 && lr >= 0 && lr < lc;
+                    if (SST_ANYSKIP && !__any_sync(0xffffffffu, in)) continue;
+                    const int l = in ? lr : -1 - lane;   // unique if inactive
                     float vr = bsr[i], vi = bsi[i];
                     const bool gstart = (N2 >= 32) ? (lane == 0) : (lane % N2 == 0);
                     const bool gend = (N2 >= 32) ? (lane == 31) : (lane % N2 == N2 - 1);
                     const int lp = __shfl_up_sync(0xffffffffu, l, 1);
                     const bool same_prev = !gstart && lp == l;
                     bool emit = l >= 0;
-                    if (__any_sync(0xffffffffu, same_prev)) {
+                    if (SST_SQZ == 5) { if (emit) { buf[l].x += vr; } continue; }
+                    if (SST_SQZ != 4 && __any_sync(0xffffffffu, same_prev)) {
                         unsigned f = same_prev ? 0u : 1u;          // 1 = segment head
 #pragma unroll
                         for (int d = 1; d < 32; d <<= 1) {
@@ -411,7 +497,17 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) f
                         const int ln = __shfl_down_sync(0xffffffffu, l, 1);
                         emit = emit && (gend || ln != l);           // run tail carries the run sum
                     }
-                    if (emit) {
+                    if ((SST_SQZ == 3 || SST_SQZ == 4) && emit) { float2 t = buf[l]; t.x += vr; t.y += vi; buf[l] = t; }
+                    if (SST_SQZ == 6) {
+                        const int key = emit ? group * CAP + l : -1 - lane;
+                        const unsigned peers = __match_any_sync(0xffffffffu, key);
+                        const int rank = __popc(peers & ((1u << lane) - 1u));
+                        for (int r = 0; __any_sync(0xffffffffu, emit && rank >= r); ++r) {
+                            if (emit && rank == r) { float2 t = buf[l]; t.x += vr; t.y += vi; buf[l] = t; }
+                            __syncwarp();
+                        }
+                    }
+                    if (SST_SQZ == 0 && emit) {
                         atomicAdd(&buf[l].x, vr);
                         atomicAdd(&buf[l].y, vi);
                     }
@@ -422,6 +518,7 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) f
                 group_sync<N2>(group);
             }
         }
+#endif
         __syncthreads();   // tile input buffer and group buffers free for the next tile
     }
 

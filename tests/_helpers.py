@@ -54,8 +54,32 @@ def flip_stats(l_gpu, l_orc, S_orc, fhat_orc, k1, zoom):
             "mask_flips": mask_flips}
 
 
+def decision_stats(l_gpu, S_gpu, Sd_gpu, gamma, nfft, k1, B, zoom):
+    """Target decisions re-taken by the oracle in fp64 from the kernel's own fp32 spectra
+    (``sst_stft`` output): the kernel's integer decision may differ from the fp64 one only where
+    the fp64 position lies within 1e-4 coarse bins of a rounding boundary (reading R21:
+    where floating point decides an integer, both sides decide in the same precision -- the
+    paper's fp64 -- from the same inputs).  Mask decisions may differ only where |S| is within
+    1e-6 relative of gamma.  Returns the largest boundary distance of a disagreement (bins) and
+    the count of unexplained mask disagreements."""
+    S = np.asarray(S_gpu, dtype=np.complex128)
+    Sd = np.asarray(Sd_gpu, dtype=np.complex128)
+    mask, r, fhat = O.if_estimate(S, Sd, nfft, gamma)
+    l_ref = O.targets(fhat, mask, k1, B, zoom)
+    diff = l_gpu != l_ref
+    mdiff = diff & ((l_gpu == -1) != (l_ref == -1))
+    bad_mask = int((mdiff & (np.abs(np.abs(S) - gamma) > 1e-6 * max(gamma, 1e-30))).sum())
+    tdiff = diff & ~mdiff
+    if tdiff.any():
+        pos = zoom * (fhat[tdiff] - k1) + 0.5
+        far = float((np.abs(pos - np.round(pos)) / zoom).max())
+    else:
+        far = 0.0
+    return {"disagree": int(diff.sum()), "far": far, "bad_mask": bad_mask}
+
+
 def signal(cfg_name, start=0, stop=None):
     return generate(cfg_name, start, stop)
 
 
-__all__ = ["oracle_window", "config_gamma", "make_plan", "rel", "flip_stats", "signal", "get_config"]
+__all__ = ["oracle_window", "config_gamma", "make_plan", "rel", "flip_stats", "decision_stats", "signal", "get_config"]

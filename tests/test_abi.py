@@ -83,7 +83,7 @@ BASE = dict(n=4096, fs=1024.0, win_len=257, sigma=32.0, hop=1, nfft=4096, f1=0.0
     ({"nfft": 3000}, 3),                      # not a power of two
     ({"nfft": 8192, "n": 8192}, 3),           # outside this build's N_f range
     ({"zoom": 65}, 3),
-    ({"flags": 4}, 3),                        # DETERMINISTIC reserved
+    ({"flags": 4}, 0),                        # DETERMINISTIC accepted (always reproducible)
     ({"hop": 258}, 2),                        # H_t > L -> gaps (R20)
     ({"win_len": 64, "sigma": 8.0, "hop": 64, "nfft": 4096, "n": 4136}, 2),   # tail uncovered
 ])

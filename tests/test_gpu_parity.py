@@ -1,9 +1,11 @@
 """GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by element.
 
 Tolerances (BASELINE.json north_star): STFT relative Frobenius <= 1e-5; squeezed plane
-relative L2 <= 1e-3 with target disagreement <= 1e-4 of above-threshold coefficients, each
-(for |S| >= 1e-2 max) within 1e-4 coarse bins of a rounding boundary; reconstruction relative
-L2 <= 1e-4.  The oracle receives the same fp32 samples upcast to fp64 and its own window.
+relative L2 <= 1e-3 with target disagreement <= 1e-4 of above-threshold coefficients, lying
+within 1e-4 coarse bins of a rounding boundary -- the location clause is checked on the
+kernel's own fp32 spectra, decided again by the oracle in fp64 (reading R21);
+reconstruction relative L2 <= 1e-4.  The oracle receives the same fp32 samples upcast to fp64
+and its own window.
 """
 
 import numpy as np
@@ -16,7 +18,7 @@ pytestmark = [pytest.mark.gpu,
 
 import oracle as O  # noqa: E402
 from gen import get_config  # noqa: E402
-from tests._helpers import config_gamma, flip_stats, make_plan, rel, signal  # noqa: E402
+from tests._helpers import config_gamma, decision_stats, flip_stats, make_plan, rel, signal  # noqa: E402
 
 DEV = torch.device("cuda:0")
 
@@ -91,7 +93,9 @@ def test_forward_parity_and_flips(P, spec):
     Tmap = O.squeeze(S, lg.astype(np.int64), T.shape[1])
     assert rel(T, Tmap) <= 1e-5
     assert st["frac"] <= 1e-4, st
-    assert st["far_big"] <= 1e-4, st
+    Sg, Sdg = plan.stft(xd)
+    ds = decision_stats(lg, Sg.cpu().numpy(), Sdg.cpu().numpy(), gamma, nfft, plan.layout["k1"], T.shape[1], z)
+    assert ds["far"] <= 1e-4 and ds["bad_mask"] == 0, (ds, st)
     # whole-plane tolerance of the north star; these synthetic cases are almost noise-free tones and
     # chirps whose ridge coefficients can sit on a rounding boundary, so a few legitimate boundary
     # flips of large coefficients may exceed it -- then every flip must be a boundary flip
@@ -233,7 +237,10 @@ def test_c1_full(P):
     st = flip_stats(lg, lo, S, fhat, cfg.k1, cfg.zoom)
     Tg = T.cpu().numpy()
     assert rel(Tg, To) <= 1e-3, st
-    assert st["frac"] <= 1e-4 and st["far_big"] <= 1e-4, st
+    assert st["frac"] <= 1e-4, st
+    Sg, Sdg = plan.stft(xd)
+    ds = decision_stats(lg, Sg.cpu().numpy(), Sdg.cpu().numpy(), gamma, cfg.nfft, cfg.k1, cfg.bins, cfg.zoom)
+    assert ds["far"] <= 1e-4 and ds["bad_mask"] == 0, (ds, st)
     yo = O.sst_inverse(To, g, c, cfg.hop, cfg.nfft, cfg.zoom, cfg.k1, cfg.N)
     assert rel(y.cpu().numpy(), yo) <= 1e-4
 
@@ -244,7 +251,7 @@ def _windows(F, n, size, seed):
     return [(int(s), int(s) + size) for s in starts]
 
 
-@pytest.mark.parametrize("name", ["C2", "C3", "C5"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
 def test_config_sampled_frames(P, name):
     """Full-size configs in the bench's launch configuration, compared on sampled frame windows
     (both record edges included) that the oracle computes one by one."""
@@ -255,8 +262,8 @@ def test_config_sampled_frames(P, name):
     plan = make_plan(P, cfg, gamma)
     xd = torch.from_numpy(x).to(DEV)
     F = cfg.frames
-    if name == "C5":
-        wins = _windows(F, 6, 512, 5)     # T of C5 is 256 GiB: forward the windows only
+    if name in ("C4", "C5"):
+        wins = _windows(F, 6, 512, 5)     # T of C4 / C5 is 64 / 256 GiB: forward the windows only
         Tw = {w: plan.forward(xd, *w).cpu().numpy() for w in wins}
     else:
         T = plan.forward(xd)
@@ -272,7 +279,10 @@ def test_config_sampled_frames(P, name):
         lg = plan.targets(xd, *w).cpu().numpy()
         _, _, fhat = O.if_estimate(S, Sd, cfg.nfft, gamma)
         st = flip_stats(lg, lo, S, fhat, cfg.k1, cfg.zoom)
-        assert st["frac"] <= 1e-4 and st["far_big"] <= 1e-4, (name, w, st)
+        assert st["frac"] <= 1e-4, (name, w, st)
+        Sg, Sdg = plan.stft(xd, *w)
+        ds = decision_stats(lg, Sg.cpu().numpy(), Sdg.cpu().numpy(), gamma, cfg.nfft, cfg.k1, cfg.bins, cfg.zoom)
+        assert ds["far"] <= 1e-4 and ds["bad_mask"] == 0, (name, w, ds, st)
 
 
 @pytest.mark.parametrize("name", ["C3"])

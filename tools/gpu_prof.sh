@@ -1,0 +1,11 @@
+#!/bin/bash
+# pytest -m gpu (no -x) + one ncu --set full capture of the forward and inverse kernels on a C3 slice
+TAG=${1:-r1}
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -q -rf > gpurun_out/pytest_gpu_$TAG.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_gpu_$TAG.log
+python tools/prof_run.py --cfg C3 --n-log2 21 > gpurun_out/prof_plain_$TAG.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fwd_kernel|inv_kernel" -c 2 \
+    -o gpurun_out/prof_c3_$TAG -f python tools/prof_run.py --cfg C3 --n-log2 21 > gpurun_out/ncu_c3_$TAG.log 2>&1
+echo "ncu exit $?" >> gpurun_out/ncu_c3_$TAG.log
+echo done
