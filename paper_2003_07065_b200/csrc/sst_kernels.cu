@@ -49,6 +49,11 @@ cudaError_t upload_w64(const float2* w64_host) {
     return cudaMemcpyToSymbol(c_w64, w64_host, sizeof(float2) * 64);
 }
 
+template <int V>
+struct IntC {
+    static constexpr int value = V;
+};
+
 template <int N2>
 struct Geom {
     static constexpr int N = 64 * N2;
@@ -428,8 +433,10 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) f
                         emit = emit && (gend || ln != l);           // run tail carries the run sum
                     }
                     if (emit) {                                     // a6: T_acc[l] += S (Eq. 27/28)
-                        const long long xr = __float2ll_rn(vr * scale);
-                        const long long xi = __float2ll_rn(vi * scale);
+                        // volatile: keep the conversions inside this rarely-taken branch
+                        long long xr, xi;
+                        asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xr) : "f"(vr * scale));
+                        asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xi) : "f"(vi * scale));
                         atomicAdd(acc + l, (int)(xr >> 20));
                         atomicAdd(acc + CH + l, (int)(xr & 0xFFFFF));
                         atomicAdd(acc + 2 * CH + l, (int)(xi >> 20));
@@ -597,6 +604,18 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) i
     int64_t flushed = g_lo;
 
     for (int64_t f0 = f_lo; f0 < f_hi; f0 += 2 * P) {
+        {
+            // L2 prefetch of the next tile's T rows (2P rows of B complex values): their DRAM
+            // latency overlaps this tile's transforms
+            const int64_t fn = f0 + 2 * P;
+            const int nrows = (int)min((int64_t)(2 * P), f_hi - fn);
+            const int lines = (a.bins * 8 + 127) >> 7;
+            for (int i = threadIdx.x; i < nrows * lines; i += TPB) {
+                const int r = i / lines, q = i - r * lines;
+                const char* ptr = reinterpret_cast<const char*>(a.T + (fn + r) * a.ldT) + q * 128;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+            }
+        }
         for (int it0 = 0; it0 < items; it0 += G) {
             // ---------------- per-group item: sub-IFFT of one (pair, b)
             const int item = it0 + group;
@@ -678,24 +697,36 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) i
                 const int64_t sA = (a.frame_begin + fa) * H;
                 float2 y[PPT];
                 int slot[PPT];
+                // sum of the pair's items (compile-time count for the usual z = 1, 2, 4, 8)
+                auto combine = [&](auto nic) {
+                    constexpr int NI = decltype(nic)::value;
 #pragma unroll
-                for (int jj = 0; jj < PPT; ++jj) {
-                    const int p = threadIdx.x + TPB * jj;
-                    const int tau = (p <= last_in) ? p : p - N;
-                    const bool ok = p < N && tau >= -c;
-                    float2 acc = make_float2(0.0f, 0.0f);
-                    if (ok) {
-                        for (int i = i_lo; i < i_hi; ++i) {
-                            const float2 t = smem[i * CAP + p];
-                            acc.x += t.x;
-                            acc.y += t.y;
+                    for (int jj = 0; jj < PPT; ++jj) {
+                        const int p = threadIdx.x + TPB * jj;
+                        const int tau = (p <= last_in) ? p : p - N;
+                        const bool ok = (FULLWIN || (p < N && tau >= -c));
+                        float2 acc = make_float2(0.0f, 0.0f);
+                        if (ok) {
+                            const float2* sp = smem + i_lo * CAP + p;
+                            if constexpr (NI > 0) {
+                                acc = sp[0];
+#pragma unroll
+                                for (int i = 1; i < NI; ++i) acc = cadd(acc, sp[i * CAP]);
+                            } else {
+                                for (int i = 0; i < i_hi - i_lo; ++i) acc = cadd(acc, sp[i * CAP]);
+                            }
+                            acc = cscale(acc, g_s[tau + c]);
                         }
-                        const float gw = g_s[tau + c];
-                        acc.x *= gw;
-                        acc.y *= gw;
+                        y[jj] = acc;
+                        slot[jj] = ok ? (int)((sA + tau) & rmask) : -1;
                     }
-                    y[jj] = acc;
-                    slot[jj] = ok ? (int)((sA + tau) & rmask) : -1;
+                };
+                switch (i_hi - i_lo) {
+                    case 1: combine(IntC<1>{}); break;
+                    case 2: combine(IntC<2>{}); break;
+                    case 4: combine(IntC<4>{}); break;
+                    case 8: combine(IntC<8>{}); break;
+                    default: combine(IntC<0>{}); break;
                 }
 #pragma unroll
                 for (int jj = 0; jj < PPT; ++jj)
