@@ -52,6 +52,19 @@ def _peaks():
         return 6650.0, 1965.0, "fallback"
 
 
+def _traffic(workload, kernel, frames):
+    """DRAM bytes (read + write) per launch of the dominant kernel, from the committed ncu --set full
+    capture of this bench command (profiles/traffic.json, written by tools/ncu_traffic.py); None if
+    there is no capture for this workload and frame count."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        e = t[workload][kernel]
+        return e["dram_bytes"] if e["frames"] == frames else None
+    except Exception:
+        return None
+
+
 def algorithmic_counts(cfg):
     """Per-frame algorithmic work."""
     K = cfg.nfft // 2 + 1
@@ -289,8 +302,9 @@ def run_ours(args, cfg_base):
     inv_gbs = inv_b * nfr_rank / (inv_ms * 1e-3) / 1e9
     dom = "forward" if fwd_ms >= inv_ms else "inverse"
     ach = fwd_tf if dom == "forward" else inv_tf
+    traffic = _traffic(cfg_base.name, dom, nfr_rank) if world == 1 else None
     roofline = {"bound": "alu", "kernel": f"sst_{dom}", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": ach / fp32_peak, "traffic": None,
+                "frac": ach / fp32_peak, "traffic": traffic,
                 "peak_source": f"derived: {FP32_PEAK_NOTE}",
                 "hbm": {"forward_gbs": fwd_gbs, "inverse_gbs": inv_gbs, "peak_gbs": hbm_gbs,
                         "forward_frac": fwd_gbs / hbm_gbs, "inverse_frac": inv_gbs / hbm_gbs,
@@ -330,7 +344,7 @@ def run_ours(args, cfg_base):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="C3", choices=sorted(WORKLOAD_DESC))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -4,7 +4,7 @@
 TAG=${1:-r1}
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/nvsmi_$TAG.txt 2>&1
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$TAG.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -rf > gpurun_out/pytest_gpu_$TAG.log 2>&1
 echo "pytest exit $?" >> gpurun_out/pytest_gpu_$TAG.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1
 echo "smoke exit $?" >> gpurun_out/smoke_$TAG.log
