@@ -254,6 +254,7 @@ sst::FwdArgs fwd_args(const sst_plan* pl, const float* x, int64_t x_off, int64_t
     a.absmax_dev = nullptr;
     a.gamma_rel = (float)pl->p.gamma;
     a.r_scale = (float)(pl->lay.nfft / (2.0 * kPi * pl->lay.alpha));
+    a.zr_scale = (float)(pl->lay.zoom * pl->lay.nfft / (2.0 * kPi * pl->lay.alpha));
     a.r_scale_d = pl->lay.nfft / (2.0 * kPi * pl->lay.alpha);
     a.inv_alpha2 = (float)(1.0 / (2.0 * pl->lay.alpha));
     a.lay = sst::fwd_layout(pl->lay.nfft / 64, pl->lay.win_len, pl->lay.hop);

@@ -63,6 +63,7 @@ struct FwdArgs {
     const float* absmax_dev; // relative mode: gamma = gamma_rel * (*absmax_dev)
     float gamma_rel;
     float r_scale;           // N_f / (2 pi alpha)
+    float zr_scale;          // z N_f / (2 pi alpha)
     double r_scale_d;        // same, fp64 (near-boundary re-decision)
     float inv_alpha2;        // 1 / (2 alpha)
     FwdLayout lay;
