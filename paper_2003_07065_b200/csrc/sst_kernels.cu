@@ -112,6 +112,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // Per source bin k with Za = Z[k], Zb = Z[N-k]: returns target l (>= 0), -1 masked, -2 out of band.
 // S = (P, Q)/2 with P = Re Za + Re Zb, Q = Im Za - Im Zb;  S' = (U, -V)/(2 alpha) with
 // U = Im Za + Im Zb, V = Re Za - Re Zb;  -Im(S'/S) = (V P + U Q) / (alpha (P^2 + Q^2)).
+// (hi 2^20 + lo) * s for the squeeze's limb sums: one fused rounding of the two converted limbs
+// (|hi| < 2^30, 0 <= lo < 2^31.01), i.e. within an fp32 ulp of the exact integer sum
+__device__ __forceinline__ float limbs_to_float(int hi, int lo, float s) {
+    return fmaf((float)hi, 1048576.0f, (float)(unsigned)lo) * s;
+}
+
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -384,8 +390,8 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) f
             // (v_max < 2^e, a power of two: exact) and rounded to a 64-bit integer X, |X| < 2^39, which
             // is added as two 32-bit limbs hi = X >> 20 (signed) and lo = X & (2^20 - 1).  With at
             // most K <= 2049 contributions per target the limb sums cannot overflow
-            // (sum|hi| < 2^30.01, sum lo < 2^31.01), so the band value is the exactly rounded sum of
-            // its fp32 terms (quantum v_max 2^-39) whatever the order: bitwise reproducible.
+            // (sum|hi| < 2^30.01, sum lo < 2^31.01): the integer sum is exact whatever the order (quantum
+            // v_max 2^-39), so the band value is bitwise reproducible.
             // N2 = 64: each of the frame's two warps squeezes into its own half of the group buffer.
             constexpr int WPG = (N2 > 32) ? N2 / 32 : 1;   // warps per group
             constexpr int CH = CAP / 2 / WPG;              // band bins per pass (4 int32 each)
@@ -463,13 +469,13 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) f
                             for (int h = 0; h < WPG; ++h) {
                                 const int* ah = a0 + h * 4 * CH;
                                 const float is = wscale[w0 + h];
-                                sr += (float)((((long long)ah[i]) << 20) + (unsigned)ah[CH + i]) * is;
-                                si += (float)((((long long)ah[2 * CH + i]) << 20) + (unsigned)ah[3 * CH + i]) * is;
+                                sr += limbs_to_float(ah[i], ah[CH + i], is);
+                                si += limbs_to_float(ah[2 * CH + i], ah[3 * CH + i], is);
                             }
                             t = make_float2(sr, si);
                         } else {
-                            t = make_float2((float)((((long long)a0[i]) << 20) + (unsigned)a0[CH + i]) * iscale,
-                                            (float)((((long long)a0[2 * CH + i]) << 20) + (unsigned)a0[3 * CH + i]) * iscale);
+                            t = make_float2(limbs_to_float(a0[i], a0[CH + i], iscale),
+                                            limbs_to_float(a0[2 * CH + i], a0[3 * CH + i], iscale));
                         }
                         trow[l0 + i] = t;
                     }
@@ -634,6 +640,10 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) i
             const float2* TA = a.T + (vA ? fA : f_lo) * a.ldT;
             const float2* TB = vB ? TA + a.ldT : TA;
             float2 v[64];
+            // band entries q in [k1, k2): l = z (q - k1) + b; mirror entries: l' = z (N - k1 - q) - b
+            const int zstep = zoom * N2;                           // l step per row n1
+            const int lbase = zoom * (tg - k1) + b;                // band l at n1 = 0
+            const int mbase = zoom * (N - k1 - tg) - b;            // mirror l at n1 = 0
 #pragma unroll
             for (int n1 = 0; n1 < 64; ++n1) {
                 if (n1 >= RM && n1 < 64 - RM) {                   // outside band and mirror
@@ -641,15 +651,18 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) i
                     continue;
                 }
                 const int q = N2 * n1 + tg;                       // sub-spectrum index (coarse bin)
-                const int ib = q - k1;                            // band: j = z q + b = z k1 + l
-                const bool inb = (unsigned)ib < (unsigned)nr;
-                const int lm = zoom * (N - k1 - q) - b;           // mirror: j = z N - (z k1 + l')
-                const bool inm = !inb && q > 0 && (unsigned)lm < (unsigned)a.bins;
-                const int li = inb ? zoom * ib + b : lm;
+                // RM < 32: rows below RM can only hold band entries, rows above 64 - RM only mirror
+                // entries (k2 <= RM N2 and N - k2 >= (64 - RM) N2)
+                const bool lower = (RM < 32) ? (n1 < RM) : true;
+                const bool upper = (RM < 32) ? (n1 >= 64 - RM) : true;
+                const bool inb = lower && (unsigned)(q - k1) < (unsigned)nr;
+                const int lm = mbase - n1 * zstep;
+                const bool inm = upper && !inb && q > 0 && (unsigned)lm < (unsigned)a.bins;
+                const int li = inb ? lbase + n1 * zstep : lm;
                 float2 ta = make_float2(0.0f, 0.0f), tb = make_float2(0.0f, 0.0f);
                 if ((inb || inm) && vA) ta = __ldg(TA + li);
                 if ((inb || inm) && vB) tb = __ldg(TB + li);
-                if (q == 0 && b == 0) { ta.y = 0.0f; tb.y = 0.0f; }  // DC: real part only (R14)
+                if (n1 == 0 && q == 0 && b == 0) { ta.y = 0.0f; tb.y = 0.0f; }  // DC: real part only (R14)
                 v[n1] = inb ? make_float2(ta.x - tb.y, ta.y + tb.x)    // H_A + i H_B
                             : make_float2(ta.x + tb.y, tb.x - ta.y);   // conj H_A + i conj H_B
             }
