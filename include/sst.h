@@ -161,6 +161,28 @@ sst_status sst_inverse_accumulate(sst_plan* plan, const float* T, int64_t ldT,
 /* Step 2: y[n - y_off] /= C d[n] for global n in [y_off, y_off + y_len) (C = sqrt 2 or C_d). */
 sst_status sst_inverse_finalize(sst_plan* plan, float* y, int64_t y_off, int64_t y_len, void* stream);
 
+/* ---------------------------------------------------------------- plain STFT synthesis ----- */
+
+/* Downsampled STFT synthesis, Eq. (10)-(11): per frame the N_f-point inverse DFT of
+ * the one-sided spectrum S[m, k], k = 0..N_f/2 (as written by sst_stft; conjugate mirror, DC and
+ * Nyquist real, window-centred phase of Eq. 9), times g, overlap-added and divided by the frame
+ * diagonal d[n] = sum_m g[n - m H_t + c]^2 (R2).  No sqrt 2: this is the plain STFT inverse the
+ * paper compares the SST against (Figs 4, 7), exact up to rounding (pin P4).
+ *   S: device complex64, row m = frame m (all F rows), S[m*ldS + k], ldS >= N_f/2 + 1.
+ *   y: device float [N], overwritten.
+ * Errors: SST_E_INVALID_ARGUMENT (NULL, ldS too small), SST_E_CUDA.                        */
+sst_status sst_istft(sst_plan* plan, const float* S, int64_t ldS, float* y, void* stream);
+
+/* ---------------------------------------------------------------- analysis ----------------- */
+
+/* Renyi entropy of order alpha of the TF plane P = |T|^2 (Eq. 32):
+ *   H_alpha = log2( sum P^alpha / (sum P)^alpha ) / (1 - alpha).
+ * T: device complex64 [rows][ldT], columns [0, B).  out: device double [3] receives
+ * { sum P, sum P^alpha, H_alpha } (fp64 accumulation in a fixed order: reproducible).
+ * alpha > 0, alpha != 1.  Errors: SST_E_INVALID_ARGUMENT, SST_E_CUDA.                    */
+sst_status sst_renyi(sst_plan* plan, const float* T, int64_t rows, int64_t ldT, double alpha, double* out,
+                     void* stream);
+
 /* ---------------------------------------------------------------- debug / parity ----------- */
 
 /* S^g and S^{g'} (Eq. 9) of frames [fb, fe) for k = 0..N_f/2: S, Sd device complex64

@@ -75,6 +75,8 @@ SIGNATURES = {
     "sst_inverse": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "sst_inverse_accumulate": (_i32, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp]),
     "sst_inverse_finalize": (_i32, [_vp, _vp, _i64, _i64, _vp]),
+    "sst_istft": (_i32, [_vp, _vp, _i64, _vp, _vp]),
+    "sst_renyi": (_i32, [_vp, _vp, _i64, _i64, _dbl, _vp, _vp]),
     "sst_stft": (_i32, [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp]),
     "sst_targets": (_i32, [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp]),
     "sst_absmax": (_i32, [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp]),

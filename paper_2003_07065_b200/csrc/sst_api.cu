@@ -31,7 +31,8 @@ struct sst_plan {
     // device tables
     float2* d_taps = nullptr;       // [L]  (g, alpha g')
     float2* d_tw = nullptr;         // [N_f]
-    float2* d_twz = nullptr;        // [z N_f]
+    float2* d_phz = nullptr;        // [z][64 + 2 N_f/64]
+    double* d_renyi = nullptr;      // [kRenyiBlocks][2] partial sums
     float* d_inv_head = nullptr;    // [n_head]
     float* d_inv_tail = nullptr;    // [n_tail]
     float* d_inv_per = nullptr;     // [hop]
@@ -46,7 +47,7 @@ struct sst_plan {
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(device);
-        for (void* q : {(void*)d_taps, (void*)d_tw, (void*)d_twz, (void*)d_inv_head, (void*)d_inv_tail,
+        for (void* q : {(void*)d_taps, (void*)d_tw, (void*)d_phz, (void*)d_renyi, (void*)d_inv_head, (void*)d_inv_tail,
                         (void*)d_inv_per, (void*)d_absmax, (void*)d_seam})
             if (q) cudaFree(q);
         cudaSetDevice(prev);
@@ -353,22 +354,32 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
 
     const double alpha = pl->lay.alpha;
     // tw[k1 * N2 + t] = W_N^{t k1} (four-step twiddle, laid out so a warp's lanes t read
-    // consecutive entries); twz[(b-1) L + tau + c] = exp(+2 pi i b tau / (z N)), b = 1..z-1
+    // consecutive entries).  Inverse phase exp(+2 pi i b tau/(z N)) of residue b at output
+    // p = col + 64 k2 (tau = p, or p - N where the window wraps): phz[b][col] * phz[b][64 + w N2 + k2]
+    // with phz[b][col] = e(b col), phz[b][64 + k2] = e(64 b k2), phz[b][64 + N2 + k2] = e(b (64 k2 - N)),
+    // e(x) = exp(2 pi i x/(z N)); all rounded once from fp64.
     const int32_t N2 = Nf / 64;
-    std::vector<float2> taps(L), tw(Nf), twz((size_t)std::max(1, z - 1) * L);
+    const int32_t PH = 64 + 2 * N2;
+    std::vector<float2> taps(L), tw(Nf), phz((size_t)z * PH);
     for (int32_t j = 0; j < L; ++j) taps[j] = make_float2((float)pl->g[j], (float)(alpha * pl->gd[j]));
     for (int32_t k1 = 0; k1 < 64; ++k1)
         for (int32_t t = 0; t < N2; ++t) {
             const double a = -2.0 * kPi * (double)((int64_t)t * k1 % Nf) / Nf;
             tw[(size_t)k1 * N2 + t] = make_float2((float)std::cos(a), (float)std::sin(a));
         }
-    for (int32_t b = 1; b < z; ++b)
-        for (int32_t j = 0; j < L; ++j) {
-            const int64_t tau = j - c;
-            const int64_t e = (((int64_t)b * tau) % ((int64_t)z * Nf) + (int64_t)z * Nf) % ((int64_t)z * Nf);
-            const double a = 2.0 * kPi * (double)e / ((double)z * Nf);
-            twz[(size_t)(b - 1) * L + j] = make_float2((float)std::cos(a), (float)std::sin(a));
+    const int64_t zN = (int64_t)z * Nf;
+    auto ez = [&](int64_t x) {
+        const int64_t e = ((x % zN) + zN) % zN;
+        const double a = 2.0 * kPi * (double)e / (double)zN;
+        return make_float2((float)std::cos(a), (float)std::sin(a));
+    };
+    for (int32_t b = 0; b < z; ++b) {
+        for (int32_t col = 0; col < 64; ++col) phz[(size_t)b * PH + col] = ez((int64_t)b * col);
+        for (int32_t k2 = 0; k2 < N2; ++k2) {
+            phz[(size_t)b * PH + 64 + k2] = ez((int64_t)b * 64 * k2);
+            phz[(size_t)b * PH + 64 + N2 + k2] = ez((int64_t)b * (64 * k2 - Nf));
         }
+    }
     // 1/(C d[n]): head [0, n_head), tail [N - n_tail, N), interior periodic in (n + c) mod H
     pl->n_head = (int32_t)std::min<int64_t>(N, L);
     pl->n_tail = (int32_t)std::min<int64_t>(N, (int64_t)L + H);
@@ -382,7 +393,7 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
         per[i] = (float)(1.0 / (pl->cst * d));
     }
     if ((s = upload(pl, &pl->d_taps, taps)) != SST_OK || (s = upload(pl, &pl->d_tw, tw)) != SST_OK ||
-        (s = upload(pl, &pl->d_twz, twz)) != SST_OK || (s = upload(pl, &pl->d_inv_head, head)) != SST_OK ||
+        (s = upload(pl, &pl->d_phz, phz)) != SST_OK || (s = upload(pl, &pl->d_inv_head, head)) != SST_OK ||
         (s = upload(pl, &pl->d_inv_tail, tail)) != SST_OK || (s = upload(pl, &pl->d_inv_per, per)) != SST_OK) {
         msg = pl->err;
         delete pl;
@@ -536,12 +547,13 @@ static sst::InvArgs inv_args(const sst_plan* pl, const float* T, int64_t ldT, in
     a.bins = pl->lay.bins;
     a.taps = pl->d_taps;
     a.tw = pl->d_tw;
-    a.twz = pl->d_twz;
+    a.phz = pl->d_phz;
     a.inv_n = (float)(1.0 / pl->lay.nfft);
     a.y = y;
     a.y_off = y_off;
     a.y_len = y_len;
     a.normalize = normalize;
+    a.out_scale = 1.0f;
     a.inv_head = pl->d_inv_head;
     a.n_head = pl->n_head;
     a.inv_tail = pl->d_inv_tail;
@@ -556,6 +568,18 @@ static sst::InvArgs inv_args(const sst_plan* pl, const float* T, int64_t ldT, in
     if (fpc < min_fpc) fpc = min_fpc;
     a.frames_per_cta = fpc;
     *grid = (int)((F + fpc - 1) / fpc);
+    return a;
+}
+
+// plain STFT synthesis (Eq. 10-11): the inverse kernel on the full one-sided band, z = 1,
+// with the normalisation 1/(C d) rescaled by C (tables hold 1/(C d[n]))
+static sst::InvArgs istft_args(const sst_plan* pl, const float* S, int64_t ldS, float* y, int* grid) {
+    sst::InvArgs a = inv_args(pl, S, ldS, 0, pl->lay.frames, y, 0, pl->lay.n, 1, grid);
+    a.zoom = 1;
+    a.k1 = 0;
+    a.bins = pl->lay.nfft / 2 + 1;
+    a.out_scale = (float)pl->cst;
+    a.lay = sst::inv_layout(pl->lay.nfft / 64, pl->lay.win_len, pl->lay.hop, 1);
     return a;
 }
 
@@ -588,6 +612,35 @@ sst_status sst_inverse_accumulate(sst_plan* plan, const float* T, int64_t ldT, i
         return fail(plan, SST_E_INVALID_ARGUMENT, "y span does not cover the frames' reach");
     DeviceGuard guard(plan->device);
     return run_inverse(plan, T, ldT, frame_begin, frame_end, y, y_off, y_len, 0, stream);
+}
+
+sst_status sst_istft(sst_plan* plan, const float* S, int64_t ldS, float* y, void* stream) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    if (!S || !y) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL S or y");
+    if (ldS < plan->lay.nfft / 2 + 1) return fail(plan, SST_E_INVALID_ARGUMENT, "ldS < N_f/2 + 1");
+    DeviceGuard guard(plan->device);
+    int grid = 0;
+    sst::InvArgs a = istft_args(plan, S, ldS, y, &grid);
+    cudaStream_t st = (cudaStream_t)stream;
+    sst_status s = cuda_status(plan, sst::launch_inverse(a, grid, st), "istft launch");
+    if (s != SST_OK) return s;
+    return cuda_status(plan, sst::launch_inverse_seams(a, grid, st), "istft seam launch");
+}
+
+sst_status sst_renyi(sst_plan* plan, const float* T, int64_t rows, int64_t ldT, double alpha, double* out,
+                     void* stream) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    if (!T || !out) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL T or out");
+    if (rows < 1 || ldT < plan->lay.bins) return fail(plan, SST_E_INVALID_ARGUMENT, "rows < 1 or ldT < B");
+    if (!(alpha > 0.0) || alpha == 1.0 || !std::isfinite(alpha))
+        return fail(plan, SST_E_INVALID_ARGUMENT, "alpha must be > 0, finite and != 1 (Eq. 32)");
+    DeviceGuard guard(plan->device);
+    if (!plan->d_renyi) {
+        cudaError_t ce = cudaMalloc((void**)&plan->d_renyi, sizeof(double) * 2 * sst::kRenyiBlocks);
+        if (ce != cudaSuccess) { cudaGetLastError(); return fail(plan, SST_E_OUT_OF_MEMORY, "cudaMalloc renyi"); }
+    }
+    return cuda_status(plan, sst::launch_renyi(reinterpret_cast<const float2*>(T), rows, plan->lay.bins, ldT, alpha,
+                                               plan->d_renyi, out, (cudaStream_t)stream), "renyi launch");
 }
 
 sst_status sst_inverse_finalize(sst_plan* plan, float* y, int64_t y_off, int64_t y_len, void* stream) {

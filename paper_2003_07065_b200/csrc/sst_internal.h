@@ -81,12 +81,13 @@ struct InvArgs {
     int32_t hop, L, c, nfft, zoom, k1, bins;
     const float2* taps;               // .x = g
     const float2* tw;                 // [nfft] tw[k1 * N2 + t] = W_N^{t k1} (conjugated here)
-    const float2* twz;                // [(zoom-1) L] exp(+2 pi i b tau/(z N)), b = 1..z-1, index tau + c
+    const float2* phz;                // [z][64 + 2 N2] phase factors of exp(+2 pi i b tau/(z N)), see sst_api.cu
     float inv_n;                      // 1 / N_f
     InvLayout lay;
     // output
     float* y; int64_t y_off, y_len;
     int normalize;                    // 1: write x_hat = sum / (C d) (y overwritten); 0: y += sum
+    float out_scale;                  // extra factor at normalisation (1; C for the plain STFT synthesis)
     const float* inv_head; int32_t n_head;   // 1/(C d[n]) for n in [0, n_head)
     const float* inv_tail; int32_t n_tail;   // for n in [N - n_tail, N)
     const float* inv_per;             // [hop] for interior n: index (n + c) mod hop
@@ -105,6 +106,12 @@ cudaError_t launch_finalize(float* y, int64_t y_off, int64_t y_len, int64_t n, i
                             const float* inv_head, int32_t n_head, const float* inv_tail, int32_t n_tail,
                             const float* inv_per, cudaStream_t s);
 int inverse_max_grid(int nfft, int hop, int L, int zoom, int device);
+
+// Renyi sums over a complex64 plane: partial[2*blockIdx] = {sum |T|^2, sum |T|^(2 alpha)},
+// then out = {sum, sum, entropy}; fixed reduction order
+constexpr int kRenyiBlocks = 592;
+cudaError_t launch_renyi(const float2* T, int64_t rows, int64_t cols, int64_t ldT, double alpha, double* partial,
+                         double* out, cudaStream_t s);
 
 // constant-memory table W_64^e (forward), uploaded once per device by the API
 cudaError_t upload_w64(const float2* w64_host);

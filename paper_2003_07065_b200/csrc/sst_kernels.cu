@@ -663,6 +663,7 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) i
                 if ((inb || inm) && vA) ta = __ldg(TA + li);
                 if ((inb || inm) && vB) tb = __ldg(TB + li);
                 if (n1 == 0 && q == 0 && b == 0) { ta.y = 0.0f; tb.y = 0.0f; }  // DC: real part only (R14)
+                if (n1 == 32 && q == N / 2 && b == 0) { ta.y = 0.0f; tb.y = 0.0f; }   // Nyquist (full band only)
                 v[n1] = inb ? make_float2(ta.x - tb.y, ta.y + tb.x)    // H_A + i H_B
                             : make_float2(ta.x + tb.y, tb.x - ta.y);   // conj H_A + i conj H_B
             }
@@ -682,23 +683,22 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) i
                 for (int n2 = 0; n2 < N2; ++n2) u[ci][n2] = buf[(tg + N2 * ci) * STRIDE + n2];
             group_sync<N2>(group);
             const bool rot = b != 0;
-            const float2* tz = a.twz + (rot ? (b - 1) : 0) * a.L + c;       // index by tau
+            const float2* pb = a.phz + b * (64 + 2 * N2);              // phase tables of residue b
 #pragma unroll
             for (int ci = 0; ci < COLS; ++ci) {
                 const int col = tg + N2 * ci;
                 Fft<N2, +1>::run(u[ci]);
-                const float2* tzc = tz + col;
+                const float2 fb = __ldg(pb + col);                      // e(b col)
 #pragma unroll
                 for (int k2 = 0; k2 < N2; ++k2) {
                     const int p = col + 64 * k2;                  // output index tau mod N
                     float2 y = u[ci][k2];
                     if constexpr (FULLWIN) {
-                        // tau = p (k2 < N2/2) or p - N: compile-time split
-                        const int toff = 64 * k2 - (k2 < N2 / 2 ? 0 : N);
-                        if (rot) y = cmul(y, __ldg(tzc + toff));   // e^{i 2 pi b tau/(z N)}
+                        // tau = p (k2 < N2/2) or p - N: compile-time split; e(b tau) = e(b col) e(b (64 k2 [- N]))
+                        if (rot) y = cmul(y, cmul(fb, __ldg(pb + 64 + (k2 < N2 / 2 ? 0 : N2) + k2)));
                     } else {
-                        const int tau = (p <= last_in) ? p : p - N;
-                        if (rot && tau >= -c) y = cmul(y, __ldg(tz + tau));
+                        const bool wrap = p > last_in;
+                        if (rot && (!wrap || p - N >= -c)) y = cmul(y, cmul(fb, __ldg(pb + 64 + (wrap ? N2 : 0) + k2)));
                     }
                     buf[p] = y;
                 }
@@ -775,7 +775,7 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) i
             } else if (!last_cta && s >= right_start) {
                 a.seam[((int64_t)blockIdx.x * 2 + 1) * a.seam_len + (s - right_start)] = val;
             } else if (a.normalize) {
-                a.y[s - a.y_off] = val * inv_norm(s, a);
+                a.y[s - a.y_off] = val * inv_norm(s, a) * a.out_scale;
             } else {
                 a.y[s - a.y_off] += val;
             }
@@ -795,7 +795,7 @@ __global__ void seam_kernel(const InvArgs a, int ctas) {
         const int64_t s = (a.frame_begin + i * a.frames_per_cta) * a.hop - a.c + t;
         if (s < 0 || s >= a.n) continue;
         const float val = a.seam[(i * 2 + 0) * a.seam_len + t] + a.seam[((i - 1) * 2 + 1) * a.seam_len + t];
-        if (a.normalize) a.y[s - a.y_off] = val * inv_norm(s, a);
+        if (a.normalize) a.y[s - a.y_off] = val * inv_norm(s, a) * a.out_scale;
         else             a.y[s - a.y_off] += val;
     }
 }
@@ -920,6 +920,58 @@ cudaError_t launch_inverse_seams(const InvArgs& a, int ctas, cudaStream_t s) {
     const int64_t want = (total + threads - 1) / threads;
     const int blocks = (int)(want < 4096 ? want : 4096);
     seam_kernel<<<blocks, threads, 0, s>>>(a, ctas);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------- Renyi -------
+__global__ void __launch_bounds__(256) renyi_partial_kernel(const float2* T, int64_t rows, int64_t cols,
+                                                            int64_t ldT, double alpha, double* partial) {
+    double s1 = 0.0, sa = 0.0;
+    const bool cube = (alpha == 3.0);
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const float2* row = T + r * ldT;
+        for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+            const float2 v = row[c];
+            const double p = (double)v.x * v.x + (double)v.y * v.y;    // P = |T|^2
+            s1 += p;
+            sa += cube ? p * p * p : pow(p, alpha);
+        }
+    }
+    __shared__ double r1[256], ra[256];
+    r1[threadIdx.x] = s1;
+    ra[threadIdx.x] = sa;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            r1[threadIdx.x] += r1[threadIdx.x + o];
+            ra[threadIdx.x] += ra[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        partial[2 * blockIdx.x] = r1[0];
+        partial[2 * blockIdx.x + 1] = ra[0];
+    }
+}
+
+__global__ void renyi_final_kernel(const double* partial, int n, double alpha, double* out) {
+    if (threadIdx.x != 0) return;
+    double s1 = 0.0, sa = 0.0;
+    for (int i = 0; i < n; ++i) {
+        s1 += partial[2 * i];
+        sa += partial[2 * i + 1];
+    }
+    out[0] = s1;
+    out[1] = sa;
+    out[2] = log2(sa / pow(s1, alpha)) / (1.0 - alpha);      // Eq. 32
+}
+
+cudaError_t launch_renyi(const float2* T, int64_t rows, int64_t cols, int64_t ldT, double alpha, double* partial,
+                         double* out, cudaStream_t s) {
+    renyi_partial_kernel<<<kRenyiBlocks, 256, 0, s>>>(T, rows, cols, ldT, alpha, partial);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    renyi_final_kernel<<<1, 32, 0, s>>>(partial, kRenyiBlocks, alpha, out);
     return cudaGetLastError();
 }
 

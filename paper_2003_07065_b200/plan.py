@@ -162,6 +162,26 @@ class Plan:
                                        _stream(self.device)), self._h)
         return y
 
+    # ------------------------------------------------------------------ plain STFT synthesis / analysis
+    def istft(self, S: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """sst_istft: Eq. 10-11 synthesis of the one-sided STFT S[F, >= N_f/2+1] (from stft())."""
+        if S.dim() != 2 or S.shape[0] != self.frames:
+            raise ValueError("S must be [F, ldS] with all frames")
+        if out is None:
+            out = torch.empty(self.n, dtype=torch.float32, device=self.device)
+        L.check(L.sst_istft(self._h, _ptr(S, self.device, torch.complex64, "S"), S.shape[1],
+                            _ptr(out, self.device, torch.float32, "y"), _stream(self.device)), self._h)
+        return out
+
+    def renyi(self, T: torch.Tensor, alpha: float = 3.0) -> torch.Tensor:
+        """sst_renyi: device float64 [3] = (sum |T|^2, sum |T|^(2 alpha), H_alpha) (Eq. 32)."""
+        if T.dim() != 2:
+            raise ValueError("T must be [rows, ldT]")
+        out = torch.empty(3, dtype=torch.float64, device=self.device)
+        L.check(L.sst_renyi(self._h, _ptr(T, self.device, torch.complex64, "T"), T.shape[0], T.shape[1],
+                            float(alpha), out.data_ptr(), _stream(self.device)), self._h)
+        return out
+
     # ------------------------------------------------------------------ debug / parity
     def stft(self, x: torch.Tensor, frame_begin: int = 0, frame_end: int | None = None, x_off: int = 0):
         fb, fe = self._frames(frame_begin, frame_end)
