@@ -13,7 +13,9 @@ enum FwdMode : int { kModeForward = 0, kModeStft = 1, kModeTargets = 2, kModeAbs
 // (forward) or frame pairs (inverse) in flight per CTA, N_f = 64 N2.
 __host__ __device__ constexpr int tpb_of(int n2) { return n2 == 64 ? 256 : 128; }
 __host__ __device__ constexpr int groups_of(int n2) { return tpb_of(n2) / n2; }
-__host__ __device__ constexpr int cap_of(int n2) { return 64 * (n2 + 1); }   // float2 per group buffer
+// float2 per group buffer: the 64 x (N2 + 1) padded exchange, plus N2 float2 when several groups share
+// a warp so consecutive groups start N2 float2 apart in the banks (conflict-free 64-bit half-warps)
+__host__ __device__ constexpr int cap_of(int n2) { return 64 * (n2 + 1) + (n2 < 16 ? n2 : 0); }
 __host__ __device__ constexpr int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 // forward dynamic shared memory: [G exchange buffers][taps L float2][2 input tiles][2 mbarriers]

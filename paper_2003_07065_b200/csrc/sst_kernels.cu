@@ -394,11 +394,14 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) f
             // v_max 2^-39), so the band value is bitwise reproducible.
             // N2 = 64: each of the frame's two warps squeezes into its own half of the group buffer.
             constexpr int WPG = (N2 > 32) ? N2 / 32 : 1;   // warps per group
-            constexpr int CH = CAP / 2 / WPG;              // band bins per pass (4 int32 each)
-            static_assert(CH % 4 == 0, "int4 zeroing");
+            // band bins per pass (4 int32 each); groups sharing a warp offset their planes by up to
+            // 28 ints so that the warp's 32-bit accesses spread over the banks
+            constexpr int CH = ((N2 < 32 ? 2 * CAP - 32 : 2 * CAP) / 4 / WPG) & ~3;
+            static_assert(CH % 4 == 0 && CH > 0, "int4 zeroing");
             const int lane = threadIdx.x & 31;
             const int wib = (WPG > 1) ? (tg >> 5) : 0;     // warp within the group
-            int* acc = reinterpret_cast<int*>(buf) + wib * 4 * CH;   // planar [hi_re|lo_re|hi_im|lo_im][CH]
+            const int ebank = (N2 < 32) ? ((32 - ((lane / N2) * N2) % 32) % 32) & ~3 : 0;
+            int* acc = reinterpret_cast<int*>(buf) + ebank + wib * 4 * CH;   // planar [hi_re|lo_re|hi_im|lo_im][CH]
             __shared__ float wscale[TPB / 32];
             float vmax = 0.0f;
 #pragma unroll
@@ -412,7 +415,7 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) f
             for (int l0 = 0; l0 < a.bins; l0 += CH) {
                 const int lc = min(CH, a.bins - l0);
                 {
-                    int4* z4 = reinterpret_cast<int4*>(buf);
+                    int4* z4 = reinterpret_cast<int4*>(reinterpret_cast<int*>(buf) + ebank);
                     const int lc4 = (lc + 3) >> 2;
 #pragma unroll
                     for (int q = 0; q < 4 * WPG; ++q)
@@ -460,7 +463,7 @@ __global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) f
                 group_sync<N2>(group);
                 if (valid)
                     for (int i = tg; i < lc; i += N2) {
-                        const int* a0 = reinterpret_cast<const int*>(buf);
+                        const int* a0 = reinterpret_cast<const int*>(buf) + ebank;
                         float2 t;
                         if constexpr (WPG > 1) {
                             const int w0 = (threadIdx.x >> 5) - wib;   // first warp of this group
