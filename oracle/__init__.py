@@ -37,4 +37,11 @@ from .sst import (  # noqa: F401
     hf_bound_eq38,
     hf_bound_eq46,
     renyi_entropy,
+    ridge_emission,
+    ridge_dp,
+    ridge_suppress,
+    extract_ridges,
+    zone_mask,
+    mode_full,
+    retrieve_mode,
 )

@@ -325,3 +325,84 @@ def renyi_entropy(P, alpha: float = 3.0) -> float:
     P = np.asarray(P, dtype=np.float64)
     p = P / P.sum()
     return float(np.log2(np.sum(p ** alpha)) / (1.0 - alpha))
+
+
+# --------------------------------------------------------------------------------------
+# Mode retrieval: ridge, zone, Eq. 15 and the zone-masked inverse.
+# P:L126-130 (§2.2) names "extracting TF ridges" without an algorithm; the ridge here is the
+# penalised dynamic programme of SPEC.md's reading (reading R22 of DESIGN.md):
+#   maximise  sum_m E[m, l_m] - lambda sum_m (l_{m+1} - l_m)^2,  E = log(|T| + eps),
+#   eps = 1e-12 max|T|, ties -> the lowest bin index.
+# --------------------------------------------------------------------------------------
+def ridge_emission(T):
+    """E[m, l] = log(|T[m, l]| + eps), eps = 1e-12 max|T| (R22)."""
+    A = np.abs(np.asarray(T))
+    eps = 1e-12 * A.max()
+    return np.log(A + eps)
+
+
+def ridge_dp(E, lam: float):
+    """Viterbi for the R22 objective on emissions E[F, B], written as the plain recurrence
+    V_0[l] = E[0, l],  V_m[l] = E[m, l] + max_{l'} (V_{m-1}[l'] - lam (l - l')^2)  (smallest
+    maximising l'), then traceback from the smallest l maximising V_{F-1}.  O(F B^2)."""
+    E = np.asarray(E, dtype=np.float64)
+    F, B = E.shape
+    l = np.arange(B)
+    pen = lam * (l[:, None] - l[None, :]).astype(np.float64) ** 2     # pen[l, l']
+    V = E[0].copy()
+    back = np.zeros((F, B), dtype=np.int64)
+    for m in range(1, F):
+        cand = V[None, :] - pen                                         # [l, l']
+        back[m] = np.argmax(cand, axis=1)                               # first maximiser
+        V = E[m] + cand[l, back[m]]
+    path = np.empty(F, dtype=np.int64)
+    path[-1] = int(np.argmax(V))
+    for m in range(F - 1, 0, -1):
+        path[m - 1] = back[m, path[m]]
+    return path
+
+
+def ridge_suppress(E, path, half: int, floor: float):
+    """After a ridge is found its zone +-half bins is suppressed (set to the floor emission
+    log(eps)) before the next one."""
+    E = np.array(E, dtype=np.float64, copy=True)
+    B = E.shape[1]
+    for m, c in enumerate(path):
+        E[m, max(0, c - half):min(B, c + half + 1)] = floor
+    return E
+
+
+def extract_ridges(T, lam: float, count: int, suppress: int = 3):
+    """`count` ridges found one after another by ridge_dp with zone suppression (R22)."""
+    E = ridge_emission(T)
+    floor = float(np.log(1e-12 * np.abs(np.asarray(T)).max()))
+    paths = []
+    for _ in range(count):
+        p = ridge_dp(E, lam)
+        paths.append(p)
+        E = ridge_suppress(E, p, suppress, floor)
+    return np.array(paths)
+
+
+def zone_mask(path, half: int, B: int):
+    """M_q[m] = {l : |l - path[m]| <= half} clipped to [0, B) ('offsetting the IFs in
+    both directions to form a banded area')."""
+    l = np.arange(B)
+    return np.abs(l[None, :] - np.asarray(path)[:, None]) <= half
+
+
+def mode_full(T, zone, g, c: int, nfft: int, k1: int, zoom: int):
+    """Eq. (15): x_q[m] = 1/(2 pi g(0)) Re sum_{l in M_q[m]} T[m, l], H_t = 1.  The sum
+    over the discrete band stands for the integral over omega with d omega = 2 pi / N_f per
+    source bin (T sums S coefficients), and the one-sided band counts twice except DC (R14):
+    x_q[m] = (2 / (N_f g[c])) Re sum_l w_l T[m, l],  w_l = 1/2 at z k1 + l = 0."""
+    T = np.asarray(T)
+    w = np.ones(T.shape[1])
+    j = zoom * k1 + np.arange(T.shape[1])
+    w[j == 0] = 0.5
+    return 2.0 / (nfft * g[c]) * np.real(np.sum(np.where(zone, T, 0) * w[None, :], axis=1))
+
+
+def retrieve_mode(T, zone, g, c: int, hop: int, nfft: int, zoom: int, k1: int, N: int):
+    """§2.3: T outside the zone set to zero, then the downsampled inverse Eq. (25)-(26)."""
+    return sst_inverse(np.where(zone, T, 0), g, c, hop, nfft, zoom, k1, N)

@@ -399,3 +399,87 @@ def test_band_grid_snapping():
         O.band_grid(1000.0, 100, 3.0, 50.0, 1)
     with pytest.raises(ValueError):
         O.band_grid(1000.0, 100, 0.0, 600.0, 1)
+
+
+# ------------------------------------------------------------------ f1: mode retrieval (R22)
+def test_ridge_dp_bruteforce_tiny():
+    """ridge_dp maximises sum E - lam sum (dl)^2 over all paths: brute force on tiny inputs."""
+    import itertools
+    rng = np.random.default_rng(11)
+    for F, B, lam in [(4, 5, 0.3), (3, 7, 0.05), (5, 4, 1.5)]:
+        E = rng.standard_normal((F, B))
+        best, arg = -np.inf, None
+        for p in itertools.product(range(B), repeat=F):
+            v = sum(E[m, p[m]] for m in range(F)) - lam * sum((p[m + 1] - p[m]) ** 2 for m in range(F - 1))
+            if v > best:
+                best, arg = v, p
+        assert tuple(O.ridge_dp(E, lam)) == arg
+
+
+def test_ridge_lambda_zero_is_argmax():
+    E = np.random.default_rng(2).standard_normal((30, 17))
+    assert np.array_equal(O.ridge_dp(E, 0.0), np.argmax(E, axis=1))
+
+
+def _full_sst_tone(f0=100.0, A=1.0, chirp=0.0):
+    """Small full-rate (H_t = 1) SST of a tone / chirp: fs = 512 Hz, N = 1024, N_f = 512 (1 Hz
+    bins), Gaussian sigma = 16 samples (sigma_f = 5.1 bins), L = 129."""
+    N, fs, L, sigma, nfft = 1024, 512.0, 129, 16.0, 512
+    t = np.arange(N) / fs
+    x = A * np.cos(2 * np.pi * (f0 * t + 0.5 * chirp * t * t) + 0.3)
+    g, gd, c = O.gaussian_window(L, sigma)
+    T = O.sst_forward(x, g, gd, c, 1, nfft, fs, 0.0, fs / 2, 1, 1e-8)
+    return x, T, g, c, nfft, t
+
+
+def test_ridge_tone_and_chirp_track_the_if():
+    """A tone's ridge is its bin on every interior frame; a chirp's ridge follows f0 + rate t
+    within one bin (ridges 'representing IFs')."""
+    x, T, g, c, nfft, t = _full_sst_tone()
+    p = O.extract_ridges(T, 0.01, 1)[0]
+    assert np.all(p[100:-100] == 100)
+    x, T, g, c, nfft, t = _full_sst_tone(f0=80.0, chirp=40.0)
+    p = O.extract_ridges(T, 0.01, 1)[0]
+    true = 80.0 + 40.0 * t                                      # bins of 1 Hz
+    assert np.max(np.abs(p[100:-100] - true[100:-100])) <= 1.0
+
+
+def test_ridge_suppression_finds_second_component():
+    N, fs, L, sigma, nfft = 1024, 512.0, 129, 16.0, 512
+    t = np.arange(N) / fs
+    x = np.cos(2 * np.pi * 100 * t) + 0.6 * np.cos(2 * np.pi * 180 * t)
+    g, gd, c = O.gaussian_window(L, sigma)
+    T = O.sst_forward(x, g, gd, c, 1, nfft, fs, 0.0, fs / 2, 1, 1e-8)
+    p = O.extract_ridges(T, 0.01, 2)
+    assert np.all(p[0, 100:-100] == 100) and np.all(p[1, 100:-100] == 180)
+
+
+def test_zone_mask_examples():
+    path = np.array([0, 5, 9])
+    z0 = O.zone_mask(path, 0, 10)
+    assert z0.sum() == 3 and z0[1, 5]
+    assert O.zone_mask(path, 2, 10)[0].sum() == 3          # clipped at the lower edge
+    assert O.zone_mask(path, 20, 10).all()
+
+
+def test_eq15_tone_closed_form():
+    """Eq. 15 at H_t = 1: squeezing a tone's coefficients onto its ridge and summing them back
+    returns A cos(phi) (sum_k S[m,k] = N_f g(0) x[m] for the full spectrum, one-sided doubled)."""
+    for A in (1.0, 0.25):
+        x, T, g, c, nfft, t = _full_sst_tone(A=A)
+        p = O.extract_ridges(T, 0.01, 1)[0]
+        xq = O.mode_full(T, O.zone_mask(p, 30, T.shape[1]), g, c, nfft, 0, 1)
+        s = slice(100, -100)
+        assert np.max(np.abs(xq[s] - x[s])) <= 2e-3 * A
+
+
+def test_mode_additivity():
+    """retrieve_mode is linear in the zone: disjoint zones covering the plane add up to the
+    unfiltered inverse (Eq. 25-26 is linear in T)."""
+    x, T, g, c, nfft, t = _full_sst_tone()
+    B = T.shape[1]
+    zone = O.zone_mask(O.extract_ridges(T, 0.01, 1)[0], 10, B)
+    a = O.retrieve_mode(T, zone, g, c, 1, nfft, 1, 0, x.size)
+    b = O.retrieve_mode(T, ~zone, g, c, 1, nfft, 1, 0, x.size)
+    full = O.sst_inverse(T, g, c, 1, nfft, 1, 0, x.size)
+    assert np.max(np.abs(a + b - full)) <= 1e-12 * np.max(np.abs(full))
