@@ -183,6 +183,32 @@ sst_status sst_istft(sst_plan* plan, const float* S, int64_t ldS, float* y, void
 sst_status sst_renyi(sst_plan* plan, const float* T, int64_t rows, int64_t ldT, double alpha, double* out,
                      void* stream);
 
+/* ---------------------------------------------------------------- mode retrieval ---------- */
+/* Ridge, zone and retrieval of one component (§2.2, §2.3).  The paper names
+ * ridge extraction without an algorithm; this is reading R22: maximise
+ *   sum_m E[m, l_m] - lambda sum_m (l_{m+1} - l_m)^2,  E = log(|T| + eps), eps = 1e-12 max|T|,
+ * ties to the lowest bin, `count` ridges one after another with the zone +-suppress bins of each
+ * found ridge set to log(eps) first.
+ *
+ * sst_ridge_emission: E device double [rows][B] and *floor_out (device double) = log(eps), from
+ *   T device complex64 [rows][ldT].
+ * sst_ridge: paths device int32 [count][rows] from E (modified: suppressed zones).  One CTA runs
+ *   the DP sequentially over frames (exact, O(B log B) per frame); plan-owned scratch holds
+ *   rows*B int32 backpointers.  B <= 11000 (SST_E_UNSUPPORTED beyond).
+ * sst_zone_mask: in place, T[m, l] = 0 where |l - path[m]| > half (keep_inside = 1) or
+ *   <= half (keep_inside = 0); sst_inverse of the masked T retrieves the mode (§2.3).
+ * sst_mode_full: Eq. 15 for H_t = 1 (else SST_E_INVALID_ARGUMENT, "invalid for downsampled SST",
+ *   P:L130): x[m] = (2 / (N_f g[c])) Re sum_{|l - path[m]| <= half} w_l T[m, l], w = 1/2 at DC;
+ *   x device float [rows].                                                                  */
+sst_status sst_ridge_emission(sst_plan* plan, const float* T, int64_t ldT, int64_t rows, double* E,
+                              double* floor_out, void* stream);
+sst_status sst_ridge(sst_plan* plan, double* E, int64_t rows, double lambda, int32_t count, int32_t suppress,
+                     const double* floor_in, int32_t* paths, void* stream);
+sst_status sst_zone_mask(sst_plan* plan, float* T, int64_t ldT, int64_t rows, const int32_t* path, int32_t half,
+                         int32_t keep_inside, void* stream);
+sst_status sst_mode_full(sst_plan* plan, const float* T, int64_t ldT, int64_t rows, const int32_t* path,
+                         int32_t half, float* x, void* stream);
+
 /* ---------------------------------------------------------------- debug / parity ----------- */
 
 /* S^g and S^{g'} (Eq. 9) of frames [fb, fe) for k = 0..N_f/2: S, Sd device complex64

@@ -33,6 +33,9 @@ struct sst_plan {
     float2* d_tw = nullptr;         // [N_f]
     float2* d_phz = nullptr;        // [z][64 + 2 N_f/64]
     double* d_renyi = nullptr;      // [kRenyiBlocks][2] partial sums
+    unsigned long long* d_amax2 = nullptr;   // ridge emission: max |T| (double bits)
+    int32_t* d_back = nullptr;      // ridge DP backpointers
+    size_t back_elems = 0;
     float* d_inv_head = nullptr;    // [n_head]
     float* d_inv_tail = nullptr;    // [n_tail]
     float* d_inv_per = nullptr;     // [hop]
@@ -47,7 +50,7 @@ struct sst_plan {
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(device);
-        for (void* q : {(void*)d_taps, (void*)d_tw, (void*)d_phz, (void*)d_renyi, (void*)d_inv_head, (void*)d_inv_tail,
+        for (void* q : {(void*)d_taps, (void*)d_tw, (void*)d_phz, (void*)d_renyi, (void*)d_amax2, (void*)d_back, (void*)d_inv_head, (void*)d_inv_tail,
                         (void*)d_inv_per, (void*)d_absmax, (void*)d_seam})
             if (q) cudaFree(q);
         cudaSetDevice(prev);
@@ -641,6 +644,66 @@ sst_status sst_renyi(sst_plan* plan, const float* T, int64_t rows, int64_t ldT, 
     }
     return cuda_status(plan, sst::launch_renyi(reinterpret_cast<const float2*>(T), rows, plan->lay.bins, ldT, alpha,
                                                plan->d_renyi, out, (cudaStream_t)stream), "renyi launch");
+}
+
+sst_status sst_ridge_emission(sst_plan* plan, const float* T, int64_t ldT, int64_t rows, double* E,
+                              double* floor_out, void* stream) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    if (!T || !E || !floor_out) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL T, E or floor");
+    if (rows < 1 || ldT < plan->lay.bins) return fail(plan, SST_E_INVALID_ARGUMENT, "rows < 1 or ldT < B");
+    DeviceGuard guard(plan->device);
+    if (!plan->d_amax2) {
+        cudaError_t ce = cudaMalloc((void**)&plan->d_amax2, sizeof(unsigned long long));
+        if (ce != cudaSuccess) { cudaGetLastError(); return fail(plan, SST_E_OUT_OF_MEMORY, "cudaMalloc amax"); }
+    }
+    return cuda_status(plan, sst::launch_ridge_emission(reinterpret_cast<const float2*>(T), rows, plan->lay.bins, ldT,
+                                                        plan->d_amax2, E, floor_out, (cudaStream_t)stream),
+                       "emission launch");
+}
+
+sst_status sst_ridge(sst_plan* plan, double* E, int64_t rows, double lambda, int32_t count, int32_t suppress,
+                     const double* floor_in, int32_t* paths, void* stream) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    if (!E || !floor_in || !paths) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL E, floor or paths");
+    if (rows < 1 || count < 1 || suppress < 0 || !(lambda >= 0.0) || !std::isfinite(lambda))
+        return fail(plan, SST_E_INVALID_ARGUMENT, "rows >= 1, count >= 1, suppress >= 0, finite lambda >= 0");
+    const int cols = plan->lay.bins;
+    if (cols > sst::kRidgeMaxCols) return fail(plan, SST_E_UNSUPPORTED, "ridge DP supports B <= 11000");
+    DeviceGuard guard(plan->device);
+    const size_t need = (size_t)rows * (size_t)cols;
+    if (plan->back_elems < need) {
+        if (plan->d_back) cudaFree(plan->d_back);
+        plan->d_back = nullptr;
+        plan->back_elems = 0;
+        cudaError_t ce = cudaMalloc((void**)&plan->d_back, sizeof(int32_t) * need);
+        if (ce != cudaSuccess) { cudaGetLastError(); return fail(plan, SST_E_OUT_OF_MEMORY, "cudaMalloc backpointers"); }
+        plan->back_elems = need;
+    }
+    return cuda_status(plan, sst::launch_ridge_dp(E, rows, cols, lambda, count, suppress, floor_in, plan->d_back, paths,
+                                                  (cudaStream_t)stream), "ridge launch");
+}
+
+sst_status sst_zone_mask(sst_plan* plan, float* T, int64_t ldT, int64_t rows, const int32_t* path, int32_t half,
+                         int32_t keep_inside, void* stream) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    if (!T || !path) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL T or path");
+    if (rows < 1 || ldT < plan->lay.bins || half < 0) return fail(plan, SST_E_INVALID_ARGUMENT, "rows, ldT or half");
+    DeviceGuard guard(plan->device);
+    return cuda_status(plan, sst::launch_zone_mask(reinterpret_cast<float2*>(T), rows, plan->lay.bins, ldT, path, half,
+                                                   keep_inside ? 1 : 0, (cudaStream_t)stream), "zone launch");
+}
+
+sst_status sst_mode_full(sst_plan* plan, const float* T, int64_t ldT, int64_t rows, const int32_t* path,
+                         int32_t half, float* x, void* stream) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    if (plan->lay.hop != 1) return fail(plan, SST_E_INVALID_ARGUMENT, "Eq. 15 needs H_t = 1 (invalid for downsampled SST, P:L130)");
+    if (!T || !path || !x) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL T, path or x");
+    if (rows < 1 || ldT < plan->lay.bins || half < 0) return fail(plan, SST_E_INVALID_ARGUMENT, "rows, ldT or half");
+    DeviceGuard guard(plan->device);
+    const int dc_bin = (plan->lay.k1 == 0) ? 0 : -1;                  // z k1 + l = 0
+    const double scale = 2.0 / ((double)plan->lay.nfft * plan->g[plan->lay.center]);
+    return cuda_status(plan, sst::launch_mode_full(reinterpret_cast<const float2*>(T), rows, plan->lay.bins, ldT, path,
+                                                   half, dc_bin, scale, x, (cudaStream_t)stream), "mode launch");
 }
 
 sst_status sst_inverse_finalize(sst_plan* plan, float* y, int64_t y_off, int64_t y_len, void* stream) {

@@ -111,6 +111,17 @@ int inverse_max_grid(int nfft, int hop, int L, int zoom, int device);
 
 // Renyi sums over a complex64 plane: partial[2*blockIdx] = {sum |T|^2, sum |T|^(2 alpha)},
 // then out = {sum, sum, entropy}; fixed reduction order
+// mode retrieval (ridge.cu)
+cudaError_t launch_ridge_emission(const float2* T, int64_t rows, int64_t cols, int64_t ldT,
+                                  unsigned long long* scratch, double* E, double* floor_out, cudaStream_t s);
+cudaError_t launch_ridge_dp(double* E, int64_t rows, int cols, double lam, int count, int suppress,
+                            const double* floor_in, int32_t* back, int32_t* paths, cudaStream_t s);
+cudaError_t launch_zone_mask(float2* T, int64_t rows, int cols, int64_t ldT, const int32_t* path, int half,
+                             int keep_inside, cudaStream_t s);
+cudaError_t launch_mode_full(const float2* T, int64_t rows, int cols, int64_t ldT, const int32_t* path, int half,
+                             int dc_bin, double scale, float* x, cudaStream_t s);
+constexpr int kRidgeMaxCols = 11000;   // DP rows of V, V', opt in shared memory
+
 constexpr int kRenyiBlocks = 592;
 cudaError_t launch_renyi(const float2* T, int64_t rows, int64_t cols, int64_t ldT, double alpha, double* partial,
                          double* out, cudaStream_t s);

@@ -182,6 +182,47 @@ class Plan:
                             float(alpha), out.data_ptr(), _stream(self.device)), self._h)
         return out
 
+    # ------------------------------------------------------------------ mode retrieval (f1, R22)
+    def ridge_emission(self, T: torch.Tensor):
+        """sst_ridge_emission: (E float64 [rows, B], floor float64 scalar) on the device."""
+        E = torch.empty((T.shape[0], self.bins), dtype=torch.float64, device=self.device)
+        fl = torch.empty((), dtype=torch.float64, device=self.device)
+        L.check(L.sst_ridge_emission(self._h, _ptr(T, self.device, torch.complex64, "T"), T.shape[1], T.shape[0],
+                                     E.data_ptr(), fl.data_ptr(), _stream(self.device)), self._h)
+        return E, fl
+
+    def ridge(self, E: torch.Tensor, floor: torch.Tensor, lam: float = 0.01, count: int = 1, suppress: int = 3):
+        """sst_ridge: int32 [count, rows] ridge paths (E is modified: suppressed zones)."""
+        paths = torch.empty((count, E.shape[0]), dtype=torch.int32, device=self.device)
+        L.check(L.sst_ridge(self._h, _ptr(E, self.device, torch.float64, "E"), E.shape[0], float(lam), int(count),
+                            int(suppress), _ptr(floor, self.device, torch.float64, "floor"), paths.data_ptr(),
+                            _stream(self.device)), self._h)
+        return paths
+
+    def ridges(self, T: torch.Tensor, lam: float = 0.01, count: int = 1, suppress: int = 3):
+        E, fl = self.ridge_emission(T)
+        return self.ridge(E, fl, lam, count, suppress)
+
+    def zone_mask(self, T: torch.Tensor, path: torch.Tensor, half: int, keep_inside: bool = True) -> torch.Tensor:
+        """sst_zone_mask, in place on T."""
+        L.check(L.sst_zone_mask(self._h, _ptr(T, self.device, torch.complex64, "T"), T.shape[1], T.shape[0],
+                                _ptr(path, self.device, torch.int32, "path"), int(half), int(bool(keep_inside)),
+                                _stream(self.device)), self._h)
+        return T
+
+    def retrieve_mode(self, T: torch.Tensor, path: torch.Tensor, half: int) -> torch.Tensor:
+        """§2.3: zone-masked copy of T through the downsampled inverse (Eq. 25-26)."""
+        Tm = self.zone_mask(T.clone(), path, half)
+        return self.inverse(Tm)
+
+    def mode_full(self, T: torch.Tensor, path: torch.Tensor, half: int) -> torch.Tensor:
+        """sst_mode_full: Eq. 15 (H_t = 1), float32 [rows]."""
+        x = torch.empty(T.shape[0], dtype=torch.float32, device=self.device)
+        L.check(L.sst_mode_full(self._h, _ptr(T, self.device, torch.complex64, "T"), T.shape[1], T.shape[0],
+                                _ptr(path, self.device, torch.int32, "path"), int(half), x.data_ptr(),
+                                _stream(self.device)), self._h)
+        return x
+
     # ------------------------------------------------------------------ debug / parity
     def stft(self, x: torch.Tensor, frame_begin: int = 0, frame_end: int | None = None, x_off: int = 0):
         fb, fe = self._frames(frame_begin, frame_end)

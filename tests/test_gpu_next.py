@@ -98,3 +98,77 @@ def test_renyi_errors(P):
         plan.renyi(T, 1.0)
     with pytest.raises(P.SSTError):
         plan.renyi(T, -2.0)
+
+
+# ------------------------------------------------------------------ f1: mode retrieval (R22)
+def _two_tone_plan(P, hop, nfft=512, fs=512.0, N=4096, L=129, sigma=16.0, zoom=1, noise=0.05, seed=3):
+    t = np.arange(N) / fs
+    rng = np.random.default_rng(seed)
+    x = (np.cos(2 * np.pi * (60 * t + 8 * np.sin(2 * np.pi * 0.5 * t))) + 0.6 * np.cos(2 * np.pi * 150 * t + 1.0)
+         + noise * rng.standard_normal(N)).astype(np.float32)
+    g, gd, c = O.gaussian_window(L, sigma)
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, 0.0, fs / 2, zoom, gamma=1e-6, device=0)
+    T = plan.forward(torch.from_numpy(x).to(DEV))
+    return plan, x, T, g, c
+
+
+def test_ridge_emission_matches_oracle(P):
+    plan, x, T, g, c = _two_tone_plan(P, hop=2)
+    E, fl = plan.ridge_emission(T)
+    Tn = T.cpu().numpy().astype(np.complex128)
+    Eo = O.ridge_emission(Tn)
+    assert np.max(np.abs(E.cpu().numpy() - Eo)) <= 1e-12
+    assert float(fl) == pytest.approx(np.log(1e-12 * np.abs(Tn).max()), abs=1e-12)
+
+
+@pytest.mark.parametrize("hop,zoom,lam,count", [(2, 1, 0.01, 2), (4, 2, 0.05, 2), (1, 1, 0.0, 1)])
+def test_ridge_paths_equal_oracle(P, hop, zoom, lam, count):
+    """Same emissions in, the kernel's DP (O(B log B) divide and conquer per frame) and the oracle's
+    O(B^2) recurrence take identical fp64 decisions: paths equal element by element."""
+    plan, x, T, g, c = _two_tone_plan(P, hop=hop, zoom=zoom)
+    E, fl = plan.ridge_emission(T)
+    E0 = E.cpu().numpy().copy()
+    floor = float(fl)
+    paths = plan.ridge(E, fl, lam, count, 3).cpu().numpy()
+    Ew = E0
+    for q in range(count):
+        p = O.ridge_dp(Ew, lam)
+        assert np.array_equal(paths[q], p), (q, int(np.sum(paths[q] != p)))
+        Ew = O.ridge_suppress(Ew, p, 3, floor)
+    # the two components are found: 60 +- 8 Hz and 150 Hz (1 Hz coarse bins, z fine bins each)
+    mid = slice(paths.shape[1] // 8, -paths.shape[1] // 8)
+    if count == 2:
+        assert np.all(np.abs(paths[1][mid] - 150 * zoom) <= 1 * zoom) or np.all(np.abs(paths[0][mid] - 150 * zoom) <= zoom)
+
+
+def test_zone_mask_and_retrieve_mode(P):
+    plan, x, T, g, c = _two_tone_plan(P, hop=4, zoom=2)
+    path = plan.ridges(T, 0.01, 1)[0].contiguous()
+    Tn = T.cpu().numpy().astype(np.complex128)
+    zone = O.zone_mask(path.cpu().numpy(), 10, plan.bins)
+    Tm = plan.zone_mask(T.clone(), path, 10)
+    assert np.array_equal(Tm.cpu().numpy() != 0, (Tn != 0) & zone)
+    Ti = plan.zone_mask(T.clone(), path, 10, keep_inside=False)
+    assert torch.equal(Tm + Ti, T)
+    y = plan.retrieve_mode(T, path, 10).cpu().numpy()
+    yo = O.retrieve_mode(Tn, zone, g, c, 4, 512, 2, 0, x.size)
+    assert rel(y, yo) <= 1e-4
+
+
+def test_mode_full_eq15(P):
+    plan, x, T, g, c = _two_tone_plan(P, hop=1, N=1024, noise=0.0)
+    path = plan.ridges(T, 0.01, 2)
+    Tn = T.cpu().numpy().astype(np.complex128)
+    for q in range(2):
+        xq = plan.mode_full(T, path[q].contiguous(), 20).cpu().numpy()
+        xo = O.mode_full(Tn, O.zone_mask(path[q].cpu().numpy(), 20, plan.bins), g, c, 512, 0, 1)
+        assert rel(xq, xo) <= 1e-6
+    # Eq. 15 separates the components: the 150 Hz ridge's mode is 0.6 cos(2 pi 150 t + 1)
+    t = np.arange(1024) / 512.0
+    x2 = 0.6 * np.cos(2 * np.pi * 150 * t + 1.0)
+    q2 = 0 if abs(int(path[0][512]) - 150) <= 1 else 1
+    xq = plan.mode_full(T, path[q2].contiguous(), 20).cpu().numpy()
+    assert np.max(np.abs(xq[150:-150] - x2[150:-150])) <= 0.02
+    plan4, _, T4, _, _ = _two_tone_plan(P, hop=4)
+    with pytest.raises(P.SSTError):
+        plan4.mode_full(T4, plan4.ridges(T4)[0].contiguous(), 5)
