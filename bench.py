@@ -191,6 +191,55 @@ def cpu_baseline(cfg, seconds_target=12.0):
 
 
 # ------------------------------------------------------------------------------------- our arm
+def measure_extras(P, plan, cfg, x, T, y, stream, ev, reps=5):
+    """SURVEY §8(f) rows built beyond the hot path, timed outside the step (CUDA events, after one
+    warm-up): f2 plain STFT synthesis (sst_stft + sst_istft, Eq. 10-11) and f4 Renyi entropy
+    (Eq. 32) on this workload; f1 ridge DP + Eq. 15 retrieval on configs[0] (C1, H_t = 1: the
+    ridge DP is sequential over frames, one CTA)."""
+    import torch
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        a, b = ev(), ev()
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    out = {}
+    S, Sd = plan.stft(x)
+    t_stft = timed(lambda: plan.stft(x))
+    del Sd
+    t_istft = timed(lambda: plan.istft(S, out=y))
+    K = cfg.nfft // 2 + 1
+    out["f2_stft_ms"] = t_stft
+    out["f2_istft_ms"] = t_istft
+    out["f2_istft_gbs"] = (cfg.frames * K * 8 + cfg.N * 4) / (t_istft * 1e-3) / 1e9
+    del S
+    t_ren = timed(lambda: plan.renyi(T))
+    out["f4_renyi_ms"] = t_ren
+    out["f4_renyi_gbs"] = cfg.frames * cfg.bins * 8 / (t_ren * 1e-3) / 1e9
+    # f1 on C1 (H_t = 1)
+    from gen import generate, get_config
+    c1 = get_config("C1")
+    x1 = torch.from_numpy(generate(c1)).to(x.device)
+    g1, _ = P.gaussian_window(c1.L, c1.sigma)
+    p1 = P.Plan(c1.N, c1.fs, c1.L, c1.sigma, c1.hop, c1.nfft, c1.f1, c1.f2, c1.zoom,
+                gamma=1e-6 * float(np.sum(g1)) * float(x1.abs().max()), device=x.device.index)
+    T1 = p1.forward(x1)
+
+    def ridge_and_mode():
+        paths = p1.ridges(T1, 0.01, 2)
+        p1.mode_full(T1, paths[0].contiguous(), 40)
+    out["f1_ridge2_mode_c1_ms"] = timed(ridge_and_mode)
+    out["f1_config"] = f"C1: F={c1.frames}, B={c1.bins}, 2 ridges (lambda 0.01) + Eq. 15 retrieval"
+    p1.close()
+    return out
+
+
 def run_ours(args, cfg_base):
     import torch
     import torch.distributed as dist
@@ -312,6 +361,9 @@ def run_ours(args, cfg_base):
                 "alu": {"forward_tflops": fwd_tf, "inverse_tflops": inv_tf,
                         "forward_frac": fwd_tf / fp32_peak, "inverse_frac": inv_tf / fp32_peak},
                 "per_frame": {"fwd_flops": fwd_fl, "inv_flops": inv_fl, "fwd_bytes": fwd_b, "inv_bytes": inv_b}}
+    extras = None
+    if world == 1 and not args.no_extras:
+        extras = measure_extras(P, plan, cfg, x, T, y, stream, ev)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg_base, args.cpu_seconds)
@@ -331,6 +383,7 @@ def run_ours(args, cfg_base):
             "fwd_ms": fwd_ms, "inv_ms": inv_ms,
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "extras": extras,
             "e2e": e2e,
             "clocks": clk.summary(),
             "gpu_launches": launches_per_step * args.steps,
@@ -350,6 +403,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-frames", type=int, default=256)
     args = ap.parse_args()

@@ -194,7 +194,7 @@ sst_status sst_renyi(sst_plan* plan, const float* T, int64_t rows, int64_t ldT, 
  *   T device complex64 [rows][ldT].
  * sst_ridge: paths device int32 [count][rows] from E (modified: suppressed zones).  One CTA runs
  *   the DP sequentially over frames (exact, O(B log B) per frame); plan-owned scratch holds
- *   rows*B int32 backpointers.  B <= 11000 (SST_E_UNSUPPORTED beyond).
+ *   rows*B int32 backpointers.  B <= 8000 (SST_E_UNSUPPORTED beyond).
  * sst_zone_mask: in place, T[m, l] = 0 where |l - path[m]| > half (keep_inside = 1) or
  *   <= half (keep_inside = 0); sst_inverse of the masked T retrieves the mode (§2.3).
  * sst_mode_full: Eq. 15 for H_t = 1 (else SST_E_INVALID_ARGUMENT, "invalid for downsampled SST",

@@ -13,6 +13,7 @@
 //                  +-suppress bins is set to the floor emission log(eps).
 //  zone_mask:      T outside (or inside) the zone |l - path[m]| <= half set to zero.
 //  mode_full:      Eq. 15, H_t = 1: x_q[m] = (2 / (N_f g[c])) Re sum_{l in zone} w_l T[m, l].
+#include <cuda_pipeline.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -77,7 +78,8 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
     extern __shared__ __align__(16) unsigned char sm[];
     double* V = reinterpret_cast<double*>(sm);            // [cols] previous frame
     double* Vn = V + cols;                                 // [cols] current frame
-    int* opt = reinterpret_cast<int*>(Vn + cols);          // [cols]
+    double* En = Vn + cols;                                // [cols] emission row of the frame, prefetched
+    int* opt = reinterpret_cast<int*>(En + cols);          // [cols]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = kRidgeThreads / 32;
     int S = 1;
@@ -89,9 +91,11 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
 
     for (int q = 0; q < count; ++q) {
         for (int l = tid; l < cols; l += kRidgeThreads) V[l] = E[l];
+        if (rows > 1)
+            for (int l = tid; l < cols; l += kRidgeThreads) __pipeline_memcpy_async(En + l, E + cols + l, sizeof(double));
+        __pipeline_commit();
         __syncthreads();
         for (int64_t m = 1; m < rows; ++m) {
-            const double* Em = E + m * cols;
             int32_t* bk = back + m * cols;
             for (int d = 0; d < levels; ++d) {
                 const int step = S >> (d + 1);                 // points p = step (2i + 1), p <= cols
@@ -130,14 +134,20 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
                 }
                 __syncthreads();
             }
+            __pipeline_wait_prior(0);                         // this frame's emissions (own copies)
             for (int l = tid; l < cols; l += kRidgeThreads) {
                 const int a = opt[l];
                 const double dd = (double)(l - a);
-                Vn[l] = Em[l] + (V[a] - lam * (dd * dd));
+                Vn[l] = En[l] + (V[a] - lam * (dd * dd));
                 bk[l] = a;
             }
             __syncthreads();
             for (int l = tid; l < cols; l += kRidgeThreads) V[l] = Vn[l];
+            // prefetch the next frame's emission row (each thread copies the entries it reads)
+            if (m + 1 < rows)
+                for (int l = tid; l < cols; l += kRidgeThreads)
+                    __pipeline_memcpy_async(En + l, E + (m + 1) * cols + l, sizeof(double));
+            __pipeline_commit();
             __syncthreads();
         }
         // final argmax (smallest index), traceback, suppression
@@ -179,7 +189,7 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
 
 cudaError_t launch_ridge_dp(double* E, int64_t rows, int cols, double lam, int count, int suppress,
                             const double* floor_in, int32_t* back, int32_t* paths, cudaStream_t s) {
-    const size_t smem = (size_t)cols * (2 * sizeof(double) + sizeof(int));
+    const size_t smem = (size_t)cols * (3 * sizeof(double) + sizeof(int));
     cudaError_t e = cudaFuncSetAttribute(ridge_dp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     ridge_dp_kernel<<<1, kRidgeThreads, smem, s>>>(E, rows, cols, lam, count, suppress, floor_in, back, paths);

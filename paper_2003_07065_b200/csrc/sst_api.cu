@@ -668,7 +668,7 @@ sst_status sst_ridge(sst_plan* plan, double* E, int64_t rows, double lambda, int
     if (rows < 1 || count < 1 || suppress < 0 || !(lambda >= 0.0) || !std::isfinite(lambda))
         return fail(plan, SST_E_INVALID_ARGUMENT, "rows >= 1, count >= 1, suppress >= 0, finite lambda >= 0");
     const int cols = plan->lay.bins;
-    if (cols > sst::kRidgeMaxCols) return fail(plan, SST_E_UNSUPPORTED, "ridge DP supports B <= 11000");
+    if (cols > sst::kRidgeMaxCols) return fail(plan, SST_E_UNSUPPORTED, "ridge DP supports B <= 8000");
     DeviceGuard guard(plan->device);
     const size_t need = (size_t)rows * (size_t)cols;
     if (plan->back_elems < need) {

@@ -120,9 +120,9 @@ cudaError_t launch_zone_mask(float2* T, int64_t rows, int cols, int64_t ldT, con
                              int keep_inside, cudaStream_t s);
 cudaError_t launch_mode_full(const float2* T, int64_t rows, int cols, int64_t ldT, const int32_t* path, int half,
                              int dc_bin, double scale, float* x, cudaStream_t s);
-constexpr int kRidgeMaxCols = 11000;   // DP rows of V, V', opt in shared memory
+constexpr int kRidgeMaxCols = 8000;    // DP rows of V, V', E, opt in shared memory (28 B per bin)
 
-constexpr int kRenyiBlocks = 592;
+constexpr int kRenyiBlocks = 1184;
 cudaError_t launch_renyi(const float2* T, int64_t rows, int64_t cols, int64_t ldT, double alpha, double* partial,
                          double* out, cudaStream_t s);
 

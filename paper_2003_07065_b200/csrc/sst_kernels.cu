@@ -931,13 +931,36 @@ __global__ void __launch_bounds__(256) renyi_partial_kernel(const float2* T, int
                                                             int64_t ldT, double alpha, double* partial) {
     double s1 = 0.0, sa = 0.0;
     const bool cube = (alpha == 3.0);
-    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
-        const float2* row = T + r * ldT;
-        for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
-            const float2 v = row[c];
-            const double p = (double)v.x * v.x + (double)v.y * v.y;    // P = |T|^2
-            s1 += p;
-            sa += cube ? p * p * p : pow(p, alpha);
+    auto acc = [&](float2 v) {
+        const double p = (double)v.x * v.x + (double)v.y * v.y;         // P = |T|^2
+        s1 += p;
+        sa += cube ? p * p * p : pow(p, alpha);
+    };
+    if (ldT == cols && (cols & 1) == 0 && (reinterpret_cast<uintptr_t>(T) & 15) == 0) {
+        // dense plane: one flat grid-stride pass, two coefficients per 16-byte load
+        const float4* T4 = reinterpret_cast<const float4*>(T);
+        const int64_t n4 = rows * cols / 2;
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+        int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        for (; i + 3 * stride < n4; i += 4 * stride) {                  // 4 loads in flight per thread
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldcs(T4 + i + u * stride);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                acc(make_float2(v[u].x, v[u].y));
+                acc(make_float2(v[u].z, v[u].w));
+            }
+        }
+        for (; i < n4; i += stride) {
+            const float4 v = __ldcs(T4 + i);
+            acc(make_float2(v.x, v.y));
+            acc(make_float2(v.z, v.w));
+        }
+    } else {
+        for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+            const float2* row = T + r * ldT;
+            for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) acc(row[c]);
         }
     }
     __shared__ double r1[256], ra[256];
