@@ -266,7 +266,7 @@ sst::FwdArgs fwd_args(const sst_plan* pl, const float* x, int64_t x_off, int64_t
 }
 
 int fwd_grid_for(const sst_plan* pl, int64_t nfr) {
-    const int G = sst::groups_of(pl->lay.nfft / 64);
+    const int G = sst::groups_of(pl->lay.nfft / 64, true);
     const int64_t tiles = (nfr + G - 1) / G;
     return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, pl->fwd_grid));
 }

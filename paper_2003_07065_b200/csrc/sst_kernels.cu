@@ -54,11 +54,11 @@ struct IntC {
     static constexpr int value = V;
 };
 
-template <int N2>
+template <int N2, bool FWD>
 struct Geom {
     static constexpr int N = 64 * N2;
-    static constexpr int TPB = tpb_of(N2);
-    static constexpr int G = groups_of(N2);
+    static constexpr int TPB = tpb_of(N2, FWD);
+    static constexpr int G = groups_of(N2, FWD);
     static constexpr int STRIDE = N2 + 1;         // padded exchange row (odd -> conflict-free)
     static constexpr int CAP = cap_of(N2);        // float2 per group buffer
 };
@@ -175,8 +175,8 @@ __device__ __forceinline__ TileIn tile_in(const FwdArgs& a, int64_t t, bool x_al
 // FULLWIN: L == N_f and c == N_f/2 (all of C2-C5): the packed index n = N2 n1 + tg maps to
 // tau = n (n1 < 32) or n - N (n1 >= 32) at compile time, so the gather has no checks.
 template <int N2, int MODE, bool BIG, bool FULLWIN>
-__global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) fwd_kernel(const FwdArgs a) {
-    using Gm = Geom<N2>;
+__global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 256 ? 1 : 2) fwd_kernel(const FwdArgs a) {
+    using Gm = Geom<N2, true>;
     constexpr int N = Gm::N;
     constexpr int TPB = Gm::TPB;
     constexpr int STRIDE = Gm::STRIDE;
@@ -579,8 +579,8 @@ __device__ __forceinline__ float inv_norm(int64_t s, const InvArgs& a) {
 // q / N2 in [0, RM) or [64 - RM, 64) (i.e. ceil(k2 / N2) <= RM): other rows of the step-1
 // input are compile-time zeros and cost nothing (narrow bands: C2, C3, C4 use RM = 8).
 template <int N2, bool FULLWIN, int RM>
-__global__ void __launch_bounds__(Geom<N2>::TPB, Geom<N2>::TPB == 256 ? 1 : 2) inv_kernel(const InvArgs a) {
-    using Gm = Geom<N2>;
+__global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 256 ? 1 : 2) inv_kernel(const InvArgs a) {
+    using Gm = Geom<N2, false>;
     constexpr int N = Gm::N;
     constexpr int TPB = Gm::TPB;
     constexpr int STRIDE = Gm::STRIDE;
@@ -817,20 +817,20 @@ static cudaError_t launch_fwd_b(const FwdArgs& a, int grid, cudaStream_t s) {
     auto kern = fwd_kernel<N2, MODE, BIG, FULLWIN>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, a.lay.total);
     if (e != cudaSuccess) return e;
-    kern<<<grid, Geom<N2>::TPB, a.lay.total, s>>>(a);
+    kern<<<grid, Geom<N2, true>::TPB, a.lay.total, s>>>(a);
     return cudaGetLastError();
 }
 
 template <int N2, int MODE, bool BIG>
 static cudaError_t launch_fwd_w(const FwdArgs& a, int grid, cudaStream_t s) {
-    if (a.L == Geom<N2>::N && a.c == Geom<N2>::N / 2) return launch_fwd_b<N2, MODE, BIG, true>(a, grid, s);
+    if (a.L == Geom<N2, true>::N && a.c == Geom<N2, true>::N / 2) return launch_fwd_b<N2, MODE, BIG, true>(a, grid, s);
     return launch_fwd_b<N2, MODE, BIG, false>(a, grid, s);
 }
 
 template <int N2, int MODE>
 static cudaError_t launch_fwd_t(const FwdArgs& a, int grid, cudaStream_t s) {
     if constexpr (MODE == kModeForward && N2 <= 32) {
-        if (a.bins > Geom<N2>::CAP) return launch_fwd_w<N2, MODE, true>(a, grid, s);
+        if (a.bins > Geom<N2, true>::CAP) return launch_fwd_w<N2, MODE, true>(a, grid, s);
     }
     return launch_fwd_w<N2, MODE, false>(a, grid, s);
 }
@@ -864,7 +864,7 @@ static int occ_fwd(int L, int H, int device) {
     const int smem = fwd_layout(N2, L, H).total;
     auto kern = fwd_kernel<N2, kModeForward, false, true>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Geom<N2>::TPB, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Geom<N2, true>::TPB, smem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     return (nb > 0 ? nb : 1) * sms;
 }
@@ -886,7 +886,7 @@ static cudaError_t launch_inv_b(const InvArgs& a, int grid, cudaStream_t s) {
     auto kern = inv_kernel<N2, FULLWIN, RM>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, a.lay.total);
     if (e != cudaSuccess) return e;
-    kern<<<grid, Geom<N2>::TPB, a.lay.total, s>>>(a);
+    kern<<<grid, Geom<N2, false>::TPB, a.lay.total, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -900,7 +900,7 @@ static cudaError_t launch_inv_r(const InvArgs& a, int grid, cudaStream_t s) {
 
 template <int N2>
 static cudaError_t launch_inv_t(const InvArgs& a, int grid, cudaStream_t s) {
-    if (a.L == Geom<N2>::N && a.c == Geom<N2>::N / 2) return launch_inv_r<N2, true>(a, grid, s);
+    if (a.L == Geom<N2, false>::N && a.c == Geom<N2, false>::N / 2) return launch_inv_r<N2, true>(a, grid, s);
     return launch_inv_r<N2, false>(a, grid, s);
 }
 
@@ -1021,7 +1021,7 @@ static int occ_inv(int hop, int L, int zoom, int device) {
     const int smem = inv_layout(N2, L, hop, zoom).total;
     auto kern = inv_kernel<N2, true, 64>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Geom<N2>::TPB, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Geom<N2, false>::TPB, smem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     return (nb > 0 ? nb : 1) * sms;
 }
