@@ -325,3 +325,30 @@ def test_error_codes(P):
         plan.forward(xd, out=bad)
     with pytest.raises(TypeError):
         plan.forward(xd.double())
+
+
+@pytest.mark.parametrize("kind", ["zeros", "dc", "nyquist"])
+def test_degenerate_signals(P, kind):
+    """Degenerate inputs: an all-zero record (every coefficient masked at gamma = 0: T = 0, x_hat = 0
+    exactly), a constant (DC only) and an alternating (fs/2) record, against the oracle."""
+    N, fs, L, sigma, hop, nfft, f1, f2, z = (5000, 1000.0, 128, 16.0, 3, 128, 0.0, 500.0, 2)
+    if kind == "zeros":
+        x = np.zeros(N, np.float32)
+    elif kind == "dc":
+        x = np.full(N, 0.75, np.float32)
+    else:
+        x = (0.5 * (-1.0) ** np.arange(N)).astype(np.float32)
+    g, gd, c = O.gaussian_window(L, sigma)
+    gamma = 0.0 if kind == "zeros" else 1e-6
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=gamma, device=0)
+    xd = torch.from_numpy(x).to(DEV)
+    T = plan.forward(xd)
+    y = plan.inverse(T).cpu().numpy()
+    Tn = T.cpu().numpy()
+    To = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, gamma)
+    if kind == "zeros":
+        assert not np.any(Tn) and not np.any(y)
+        return
+    assert rel(Tn, To) <= 1e-3
+    yo = O.sst_inverse(Tn.astype(np.complex128), g, c, hop, nfft, z, 0, N)
+    assert rel(y, yo) <= 1e-4
