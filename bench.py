@@ -405,7 +405,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--ref-frames", type=int, default=256)
+    ap.add_argument("--ref-frames", type=int, default=2048)
     args = ap.parse_args()
     if args.warmup < 3:
         print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
