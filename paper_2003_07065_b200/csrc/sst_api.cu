@@ -136,7 +136,7 @@ sst_status validate(const sst_params* p, sst_layout* lay, std::string& msg) {
     if (!(k1 >= 0 && k1 < k2 && k2 <= p->nfft / 2)) { msg = "band outside [0, N_f/2]"; return SST_E_INVALID_ARGUMENT; }
     // library limits
     if (!is_pow2(p->nfft)) { msg = "N_f must be a power of two (P:L93)"; return SST_E_UNSUPPORTED; }
-    if (p->nfft < 128 || p->nfft > 4096) { msg = "this build supports 128 <= N_f <= 4096"; return SST_E_UNSUPPORTED; }
+    if (p->nfft < 128 || p->nfft > 8192) { msg = "this build supports 128 <= N_f <= 8192"; return SST_E_UNSUPPORTED; }
     if (p->zoom > 64 || (int64_t)p->zoom * p->nfft > (1 << 20)) { msg = "z <= 64 and z N_f <= 2^20 supported"; return SST_E_UNSUPPORTED; }
     // coverage (R20): every n in [0, N) needs d[n] > 0
     const int64_t N = p->n;

@@ -351,6 +351,43 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                 load_unit(u, A, B);
                 unpack_unit(u, A, B);
             }
+        } else if constexpr (N2 == 128) {
+            // N_f = 8192: the 128-point column DFT of column c is split between threads (c, hh):
+            // hh = 0 takes the even rows, hh = 1 the odd rows (times W_128^k); the buffer then holds
+            // E_c[k] | W O_c[k] and Z[c + 64 k2] = E + W O (k2 < 64), E - W O (k2 >= 64)
+            {
+                const int c = tg & 63, hh = tg >> 6;
+                float2 A[64];
+#pragma unroll
+                for (int m = 0; m < 64; ++m) A[m] = buf[c * STRIDE + 2 * m + hh];
+                group_sync<N2>(group);
+                Fft<64, -1>::run(A);
+#pragma unroll
+                for (int k = 0; k < 64; ++k) {
+                    float2 t = A[k];
+                    if (hh && k) t = cmul(t, __ldg(a.tw + k * N2 + 64));   // W_N^{64 k} = W_128^k
+                    buf[c * STRIDE + 64 * hh + k] = t;
+                }
+            }
+            group_sync<N2>(group);
+            auto Xp = [&](int c, int k) { return cadd(buf[c * STRIDE + k], buf[c * STRIDE + 64 + k]); };  // X_c[k]
+            auto Xm = [&](int c, int k) { return csub(buf[c * STRIDE + k], buf[c * STRIDE + 64 + k]); };  // X_c[64 + k]
+            const int j = tg & 31, h = tg >> 5;
+            const int cA = j, cB = (j == 0) ? 32 : 64 - j;
+            const bool dc = (j == 0);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int k2 = 16 * h + i;                  // < 64: bins cA + 64 k2 <= N/2
+                const float2 za = Xp(cA, k2);
+                // partner N - k: column cB, index 127 - k2 (DC column: column 0, index 128 - k2)
+                const float2 zbA = dc ? (k2 == 0 ? Xp(0, 0) : Xm(0, 64 - k2)) : Xm(cB, 63 - k2);
+                on_bin(i, cA + 64 * k2, za, zbA, true);
+                const float2 zb2 = Xp(cB, k2);
+                const float2 zbB = dc ? Xm(32, 63 - k2) : Xm(cA, 63 - k2);
+                on_bin(16 + i, cB + 64 * k2, zb2, zbB, true);
+            }
+            const float2 zn = Xm(0, 0);                     // column 0, k2 = 64: Nyquist
+            on_bin(NB - 1, N / 2, zn, zn, tg == 0);
         } else {
             // N2 == 64: column DFT per thread, then unpack through shared memory
             {
@@ -678,32 +715,71 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
                 buf[kk * STRIDE + tg] = t;
             }
             group_sync<N2>(group);
-            constexpr int COLS = 64 / N2;
-            float2 u[COLS][N2];
+            if constexpr (N2 == 128) {
+                // N_f = 8192: 128-point column IDFT of column c split over (c, hh) as in the forward
+                const int c = tg & 63, hh = tg >> 6;
+                {
+                    float2 A[64];
 #pragma unroll
-            for (int ci = 0; ci < COLS; ++ci)
+                    for (int m = 0; m < 64; ++m) A[m] = buf[c * STRIDE + 2 * m + hh];
+                    group_sync<N2>(group);
+                    Fft<64, +1>::run(A);
 #pragma unroll
-                for (int n2 = 0; n2 < N2; ++n2) u[ci][n2] = buf[(tg + N2 * ci) * STRIDE + n2];
-            group_sync<N2>(group);
-            const bool rot = b != 0;
-            const float2* pb = a.phz + b * (64 + 2 * N2);              // phase tables of residue b
-#pragma unroll
-            for (int ci = 0; ci < COLS; ++ci) {
-                const int col = tg + N2 * ci;
-                Fft<N2, +1>::run(u[ci]);
-                const float2 fb = __ldg(pb + col);                      // e(b col)
-#pragma unroll
-                for (int k2 = 0; k2 < N2; ++k2) {
-                    const int p = col + 64 * k2;                  // output index tau mod N
-                    float2 y = u[ci][k2];
-                    if constexpr (FULLWIN) {
-                        // tau = p (k2 < N2/2) or p - N: compile-time split; e(b tau) = e(b col) e(b (64 k2 [- N]))
-                        if (rot) y = cmul(y, cmul(fb, __ldg(pb + 64 + (k2 < N2 / 2 ? 0 : N2) + k2)));
-                    } else {
-                        const bool wrap = p > last_in;
-                        if (rot && (!wrap || p - N >= -c)) y = cmul(y, cmul(fb, __ldg(pb + 64 + (wrap ? N2 : 0) + k2)));
+                    for (int k = 0; k < 64; ++k) {
+                        float2 t = A[k];
+                        if (hh && k) t = cmulc(t, __ldg(a.tw + k * N2 + 64));   // W_128^{-k}
+                        buf[c * STRIDE + 64 * hh + k] = t;
                     }
+                }
+                group_sync<N2>(group);
+                float2 Y[64];                                     // outputs p = c + 64 k2, k2 = 64 hh + k
+#pragma unroll
+                for (int k = 0; k < 64; ++k) {
+                    const float2 e = buf[c * STRIDE + k], o = buf[c * STRIDE + 64 + k];
+                    Y[k] = hh ? csub(e, o) : cadd(e, o);
+                }
+                group_sync<N2>(group);
+                const bool rot = b != 0;
+                const float2* pb = a.phz + b * (64 + 2 * N2);          // phase tables of residue b
+                const float2 fb = __ldg(pb + c);                        // e(b c)
+#pragma unroll
+                for (int k = 0; k < 64; ++k) {
+                    const int k2 = 64 * hh + k;
+                    const int p = c + 64 * k2;
+                    float2 y = Y[k];
+                    const bool wrap = p > last_in;                      // tau = p - N
+                    if (rot && (!wrap || p - N >= -a.c))
+                        y = cmul(y, cmul(fb, __ldg(pb + 64 + (wrap ? N2 : 0) + k2)));   // e^{i 2 pi b tau/(z N)}
                     buf[p] = y;
+                }
+            } else {
+                constexpr int COLS = 64 / N2;
+                float2 u[COLS][N2];
+#pragma unroll
+                for (int ci = 0; ci < COLS; ++ci)
+#pragma unroll
+                    for (int n2 = 0; n2 < N2; ++n2) u[ci][n2] = buf[(tg + N2 * ci) * STRIDE + n2];
+                group_sync<N2>(group);
+                const bool rot = b != 0;
+                const float2* pb = a.phz + b * (64 + 2 * N2);              // phase tables of residue b
+#pragma unroll
+                for (int ci = 0; ci < COLS; ++ci) {
+                    const int col = tg + N2 * ci;
+                    Fft<N2, +1>::run(u[ci]);
+                    const float2 fb = __ldg(pb + col);                      // e(b col)
+#pragma unroll
+                    for (int k2 = 0; k2 < N2; ++k2) {
+                        const int p = col + 64 * k2;                  // output index tau mod N
+                        float2 y = u[ci][k2];
+                        if constexpr (FULLWIN) {
+                            // tau = p (k2 < N2/2) or p - N: compile-time split; e(b tau) = e(b col) e(b (64 k2 [- N]))
+                            if (rot) y = cmul(y, cmul(fb, __ldg(pb + 64 + (k2 < N2 / 2 ? 0 : N2) + k2)));
+                        } else {
+                            const bool wrap = p > last_in;
+                            if (rot && (!wrap || p - N >= -c)) y = cmul(y, cmul(fb, __ldg(pb + 64 + (wrap ? N2 : 0) + k2)));
+                        }
+                        buf[p] = y;
+                    }
                 }
             }
             __syncthreads();
@@ -854,6 +930,7 @@ cudaError_t launch_forward(const FwdArgs& a, int mode, int grid, cudaStream_t s)
         case 1024: if constexpr (SST_HAS(16)) return launch_fwd_mode<16>(a, mode, grid, s); break;
         case 2048: if constexpr (SST_HAS(32)) return launch_fwd_mode<32>(a, mode, grid, s); break;
         case 4096: if constexpr (SST_HAS(64)) return launch_fwd_mode<64>(a, mode, grid, s); break;
+        case 8192: if constexpr (SST_HAS(128)) return launch_fwd_mode<128>(a, mode, grid, s); break;
     }
     return cudaErrorInvalidValue;
 }
@@ -877,6 +954,7 @@ int forward_max_grid(int nfft, int L, int H, int device) {
         case 1024: if constexpr (SST_HAS(16)) return occ_fwd<16>(L, H, device); break;
         case 2048: if constexpr (SST_HAS(32)) return occ_fwd<32>(L, H, device); break;
         case 4096: if constexpr (SST_HAS(64)) return occ_fwd<64>(L, H, device); break;
+        case 8192: if constexpr (SST_HAS(128)) return occ_fwd<128>(L, H, device); break;
     }
     return -1;
 }
@@ -912,6 +990,7 @@ cudaError_t launch_inverse(const InvArgs& a, int grid, cudaStream_t s) {
         case 1024: if constexpr (SST_HAS(16)) return launch_inv_t<16>(a, grid, s); break;
         case 2048: if constexpr (SST_HAS(32)) return launch_inv_t<32>(a, grid, s); break;
         case 4096: if constexpr (SST_HAS(64)) return launch_inv_t<64>(a, grid, s); break;
+        case 8192: if constexpr (SST_HAS(128)) return launch_inv_t<128>(a, grid, s); break;
     }
     return cudaErrorInvalidValue;
 }
@@ -1034,6 +1113,7 @@ int inverse_max_grid(int nfft, int hop, int L, int zoom, int device) {
         case 1024: if constexpr (SST_HAS(16)) return occ_inv<16>(hop, L, zoom, device); break;
         case 2048: if constexpr (SST_HAS(32)) return occ_inv<32>(hop, L, zoom, device); break;
         case 4096: if constexpr (SST_HAS(64)) return occ_inv<64>(hop, L, zoom, device); break;
+        case 8192: if constexpr (SST_HAS(128)) return occ_inv<128>(hop, L, zoom, device); break;
     }
     return -1;
 }

@@ -41,6 +41,10 @@ SMALL = [
     (50000, 51200.0, 4096, 512.0, 32, 4096, 0.0, 6400.0, 2),
     (20000, 1024.0, 301, 40.0, 10, 512, 100.0, 400.0, 2),
     (30000, 1000.0, 256, 30.0, 6, 256, 0.0, 500.0, 5),
+    # N_f = 8192: the paper's §5.1 shape (fs 44.1 kHz, L = 5745, H_t = 1149, band 1282..1765 df, z = 8;
+    # P:L427) on a short record, and a full-band L < N_f case
+    (60000, 44100.0, 5745, 882.0, 1149, 8192, 1282 * 44100.0 / 8192, 1765 * 44100.0 / 8192, 8),
+    (30000, 8192.0, 4001, 500.0, 64, 8192, 0.0, 4096.0, 1),
 ]
 
 
