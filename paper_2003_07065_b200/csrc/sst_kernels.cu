@@ -28,15 +28,6 @@
 #include "fft.cuh"
 #include "sst_internal.h"
 
-#ifndef SST_SQZ
-#define SST_SQZ 1
-#endif
-#ifndef SST_NOMERGE
-#define SST_NOMERGE 1
-#endif
-#ifndef SST_ANYSKIP
-#define SST_ANYSKIP 1
-#endif
 #ifdef SST_DEV_N2
 #define SST_HAS(n2) ((n2) == SST_DEV_N2)
 #else
@@ -419,7 +410,6 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
 
         // ---- a7 band store (DIRECT), or a6 + a7 in chunks of CAP bins (STORE)
         float2* trow = (MODE == kModeForward) ? a.T + fi * a.ldT : nullptr;
-#if SST_SQZ == 1
         if constexpr (STORE) {
             // a6 as exact fixed-point integer sums with native shared-memory integer atomics
             // (float atomics on shared memory are compare-and-swap loops on sm_100a).  Per warp and
@@ -464,37 +454,18 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                     const int lr = bl[i] - l0;
                     const bool in = bl[i] >= 0 && lr >= 0 && lr < lc;
                     if (!__any_sync(0xffffffffu, in)) continue;      // warp-uniform: nothing lands here
-                    // Adjacent lanes hold adjacent source bins k, so a ridge squeezing into one target
-                    // is a run of equal l across lanes: a segmented warp scan leaves the run's sum in
-                    // its last lane, the only one that touches shared memory.
-                    const int l = in ? lr : -1 - lane;                // unique if inactive
-                    float vr = bsr[i], vi = bsi[i];
-                    const bool gstart = (N2 >= 32) ? (lane == 0) : (lane % N2 == 0);
-                    const bool gend = (N2 >= 32) ? (lane == 31) : (lane % N2 == N2 - 1);
-                    const int lp = __shfl_up_sync(0xffffffffu, l, 1);
-                    const bool same_prev = !gstart && lp == l;
-                    bool emit = in;
-                    if (!SST_NOMERGE && __any_sync(0xffffffffu, same_prev)) {
-                        unsigned f = same_prev ? 0u : 1u;          // 1 = segment head
-#pragma unroll
-                        for (int d = 1; d < 32; d <<= 1) {
-                            const float ur = __shfl_up_sync(0xffffffffu, vr, d);
-                            const float ui = __shfl_up_sync(0xffffffffu, vi, d);
-                            const unsigned fu = __shfl_up_sync(0xffffffffu, f, d);
-                            if (lane >= d && !f) { vr += ur; vi += ui; f |= fu; }
-                        }
-                        const int ln = __shfl_down_sync(0xffffffffu, l, 1);
-                        emit = emit && (gend || ln != l);           // run tail carries the run sum
-                    }
-                    if (emit) {                                     // a6: T_acc[l] += S (Eq. 27/28)
+                    // lanes hitting the same target (a ridge's run of source bins) are serialised by the
+                    // shared-memory atomic unit; a warp scan merging runs first measured slower
+                    const float vr = bsr[i] * scale, vi = bsi[i] * scale;
+                    if (in) {                                         // a6: T_acc[l] += S (Eq. 27/28)
                         // volatile: keep the conversions inside this rarely-taken branch
                         long long xr, xi;
-                        asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xr) : "f"(vr * scale));
-                        asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xi) : "f"(vi * scale));
-                        atomicAdd(acc + l, (int)(xr >> 20));
-                        atomicAdd(acc + CH + l, (int)(xr & 0xFFFFF));
-                        atomicAdd(acc + 2 * CH + l, (int)(xi >> 20));
-                        atomicAdd(acc + 3 * CH + l, (int)(xi & 0xFFFFF));
+                        asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xr) : "f"(vr));
+                        asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xi) : "f"(vi));
+                        atomicAdd(acc + lr, (int)(xr >> 20));
+                        atomicAdd(acc + CH + lr, (int)(xr & 0xFFFFF));
+                        atomicAdd(acc + 2 * CH + lr, (int)(xi >> 20));
+                        atomicAdd(acc + 3 * CH + lr, (int)(xi & 0xFFFFF));
                     }
                 }
                 group_sync<N2>(group);
@@ -522,64 +493,6 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                 group_sync<N2>(group);
             }
         }
-#else
-        if constexpr (STORE) {
-            for (int l0 = 0; l0 < a.bins; l0 += CAP) {
-                const int lc = min(CAP, a.bins - l0);
-                for (int i = tg; i < lc; i += N2) buf[i] = make_float2(0.0f, 0.0f);
-                group_sync<N2>(group);
-#pragma unroll
-                for (int i = 0; i < NB; ++i) {
-                    // Adjacent lanes hold adjacent source bins k, so a ridge squeezing into one target
-                    // shows up as a run of equal l across lanes: merge runs with a segmented warp scan
-                    // and let only the run's last lane touch shared memory (same-address atomics
-                    // serialise).  Steps with no run (noise) take the plain path.
-                    const int lane = threadIdx.x & 31;
-                    const int lr = bl[i] - l0;
-                    const bool in = bl[i] >= 0 && lr >= 0 && lr < lc;
-                    if (SST_ANYSKIP && !__any_sync(0xffffffffu, in)) continue;
-                    const int l = in ? lr : -1 - lane;   // unique if inactive
-                    float vr = bsr[i], vi = bsi[i];
-                    const bool gstart = (N2 >= 32) ? (lane == 0) : (lane % N2 == 0);
-                    const bool gend = (N2 >= 32) ? (lane == 31) : (lane % N2 == N2 - 1);
-                    const int lp = __shfl_up_sync(0xffffffffu, l, 1);
-                    const bool same_prev = !gstart && lp == l;
-                    bool emit = l >= 0;
-                    if (SST_SQZ == 5) { if (emit) { buf[l].x += vr; } continue; }
-                    if (SST_SQZ != 4 && __any_sync(0xffffffffu, same_prev)) {
-                        unsigned f = same_prev ? 0u : 1u;          // 1 = segment head
-#pragma unroll
-                        for (int d = 1; d < 32; d <<= 1) {
-                            const float ur = __shfl_up_sync(0xffffffffu, vr, d);
-                            const float ui = __shfl_up_sync(0xffffffffu, vi, d);
-                            const unsigned fu = __shfl_up_sync(0xffffffffu, f, d);
-                            if (lane >= d && !f) { vr += ur; vi += ui; f |= fu; }
-                        }
-                        const int ln = __shfl_down_sync(0xffffffffu, l, 1);
-                        emit = emit && (gend || ln != l);           // run tail carries the run sum
-                    }
-                    if ((SST_SQZ == 3 || SST_SQZ == 4) && emit) { float2 t = buf[l]; t.x += vr; t.y += vi; buf[l] = t; }
-                    if (SST_SQZ == 6) {
-                        const int key = emit ? group * CAP + l : -1 - lane;
-                        const unsigned peers = __match_any_sync(0xffffffffu, key);
-                        const int rank = __popc(peers & ((1u << lane) - 1u));
-                        for (int r = 0; __any_sync(0xffffffffu, emit && rank >= r); ++r) {
-                            if (emit && rank == r) { float2 t = buf[l]; t.x += vr; t.y += vi; buf[l] = t; }
-                            __syncwarp();
-                        }
-                    }
-                    if (SST_SQZ == 0 && emit) {
-                        atomicAdd(&buf[l].x, vr);
-                        atomicAdd(&buf[l].y, vi);
-                    }
-                }
-                group_sync<N2>(group);
-                if (valid)
-                    for (int i = tg; i < lc; i += N2) trow[l0 + i] = buf[i];
-                group_sync<N2>(group);
-            }
-        }
-#endif
         __syncthreads();   // tile input buffer and group buffers free for the next tile
     }
 
