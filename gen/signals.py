@@ -221,3 +221,13 @@ def eq30_true_ifs(N: int = 8192, fs: float = 1024.0):
     f2 = np.where(t < 4, 250 - 25 * t, 250 - 50 * t + 6.25 * t ** 2)
     f3 = 370 + 50 * np.cos(0.75 * np.pi * t) - 50 * np.cos(0.5 * np.pi * t)
     return f1, f2, f3
+
+
+def eq30_noisy(snr_db: float, seed: int, N: int = 8192, fs: float = 1024.0):
+    """Eq. (30) sum plus white Gaussian noise at `snr_db` relative to its mean power (the §3.3
+    reconstruction experiments); returns (x fp32, (x1, x2, x3) fp64)."""
+    x1, x2, x3 = eq30_signal(N, fs)
+    x = x1 + x2 + x3
+    p = np.mean(x ** 2)
+    w = np.random.default_rng(seed).standard_normal(N) * np.sqrt(p / 10 ** (snr_db / 10))
+    return (x + w).astype(np.float32), (x1, x2, x3)
