@@ -1,0 +1,83 @@
+"""Host-to-host SST round trip with copy/compute overlap (public API helper).
+
+``roundtrip(plan, x_host, y_host, T)`` takes a pinned host record x, runs the forward (T stays in
+HBM) and the inverse, and leaves x_hat in the pinned host buffer y_host.  The record is cut into
+`chunks` frame ranges; three CUDA streams overlap, chunk by chunk,
+  copy-in (H2D of the chunk's new samples) -> sst_forward + sst_inverse_accumulate of the chunk ->
+  sst_inverse_finalize of the samples no later frame touches -> copy-out (D2H of those samples),
+ordered with CUDA events, so the PCIe/C2C transfers hide under the kernels.  Every transform step
+runs in libsst.so; this module only orders launches.  Frames are independent (Eq. 7-9); the
+inverse's overlap-add (Eq. 26) is linear, so accumulating chunk by chunk and normalising each
+sample once all its frames are in gives the single-call result up to fp32 re-association.
+"""
+
+from __future__ import annotations
+
+import torch
+
+
+class RoundTrip:
+    """Reusable device buffers + streams for repeated round trips of one plan."""
+
+    def __init__(self, plan, chunks: int = 8):
+        self.plan = plan
+        lay = plan.layout
+        self.N, self.H, self.c, self.L, self.F = lay["n"], lay["hop"], lay["center"], lay["win_len"], lay["frames"]
+        self.chunks = max(1, min(chunks, self.F))
+        dev = plan.device
+        self.x = torch.empty(self.N, dtype=torch.float32, device=dev)
+        self.y = torch.empty(self.N, dtype=torch.float32, device=dev)
+        self.s_in = torch.cuda.Stream(dev)
+        self.s_out = torch.cuda.Stream(dev)
+        F = self.F
+        self.cuts = [F * i // self.chunks for i in range(self.chunks + 1)]
+
+    def _span_hi(self, fe):
+        return min(self.N, (fe - 1) * self.H - self.c + self.L)
+
+    def run(self, x_host: torch.Tensor, y_host: torch.Tensor, T: torch.Tensor):
+        plan, H, c, N = self.plan, self.H, self.c, self.N
+        comp = torch.cuda.current_stream(plan.device)
+        # y is accumulated: clear it on the compute stream (ordered before the first accumulate)
+        self.y.zero_()
+        start = torch.cuda.Event()
+        start.record(comp)
+        self.s_in.wait_event(start)
+        self.s_out.wait_event(start)
+        copied = 0            # x samples [0, copied) are on the device (or queued)
+        finalized = 0         # y samples [0, finalized) are final
+        for i in range(self.chunks):
+            fb, fe = self.cuts[i], self.cuts[i + 1]
+            hi = self._span_hi(fe)
+            with torch.cuda.stream(self.s_in):
+                if hi > copied:
+                    self.x[copied:hi].copy_(x_host[copied:hi], non_blocking=True)
+                    copied = hi
+                ready = torch.cuda.Event()
+                ready.record(self.s_in)
+            comp.wait_event(ready)
+            plan.forward(self.x, fb, fe, out=T[fb:fe])
+            lo = max(0, fb * H - c)
+            plan.inverse_accumulate(T[fb:fe], fb, fe, self.y[lo:hi], y_off=lo)
+            # samples below fe*H - c receive no frame >= fe (frame m starts at m H - c)
+            fin = N if i == self.chunks - 1 else min(N, max(0, fe * H - c))
+            if fin > finalized:
+                plan.inverse_finalize(self.y[finalized:fin], y_off=finalized)
+                done = torch.cuda.Event()
+                done.record(comp)
+                self.s_out.wait_event(done)
+                with torch.cuda.stream(self.s_out):
+                    y_host[finalized:fin].copy_(self.y[finalized:fin], non_blocking=True)
+                finalized = fin
+        end = torch.cuda.Event()
+        end.record(self.s_out)
+        comp.wait_event(end)
+        end_in = torch.cuda.Event()
+        end_in.record(self.s_in)
+        comp.wait_event(end_in)
+        return y_host
+
+
+def roundtrip(plan, x_host: torch.Tensor, y_host: torch.Tensor, T: torch.Tensor, chunks: int = 8):
+    """One host->host forward + inverse with overlapped transfers (see module doc)."""
+    return RoundTrip(plan, chunks).run(x_host, y_host, T)

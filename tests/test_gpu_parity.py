@@ -387,3 +387,26 @@ def test_cuda_graph_capture_replays_bitwise(P):
     graph.replay()
     torch.cuda.synchronize()
     assert torch.equal(T, T0) and torch.equal(y, y0)
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 8])
+def test_pipelined_host_roundtrip(P, chunks):
+    """pipeline.RoundTrip (chunked H2D / forward / inverse_accumulate / finalize / D2H on three
+    streams) equals the device-resident single calls: T bitwise, x_hat to fp32 re-association."""
+    from paper_2003_07065_b200.pipeline import RoundTrip
+    spec = SMALL[4]
+    N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c = _case(spec)
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=1e-4, device=0)
+    xd = torch.from_numpy(x).to(DEV)
+    T_ref = plan.forward(xd)
+    y_ref = plan.inverse(T_ref).cpu().numpy()
+    xh = torch.from_numpy(x).pin_memory()
+    yh = torch.zeros(N, dtype=torch.float32).pin_memory()
+    T = torch.empty_like(T_ref)
+    rt = RoundTrip(plan, chunks=chunks)
+    for _ in range(2):                    # reuse of buffers and streams
+        rt.run(xh, yh, T)
+        torch.cuda.synchronize()
+        assert torch.equal(T, T_ref)
+        assert rel(yh.numpy(), y_ref) <= 1e-6
