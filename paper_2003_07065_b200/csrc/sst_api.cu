@@ -138,6 +138,16 @@ sst_status validate(const sst_params* p, sst_layout* lay, std::string& msg) {
     if (!is_pow2(p->nfft)) { msg = "N_f must be a power of two (P:L93)"; return SST_E_UNSUPPORTED; }
     if (p->nfft < 128 || p->nfft > 8192) { msg = "this build supports 128 <= N_f <= 8192"; return SST_E_UNSUPPORTED; }
     if (p->zoom > 64 || (int64_t)p->zoom * p->nfft > (1 << 20)) { msg = "z <= 64 and z N_f <= 2^20 supported"; return SST_E_UNSUPPORTED; }
+    {
+        // shared-memory footprint of the forward / inverse CTAs (227 KB per CTA on sm_100)
+        constexpr int kMaxSmem = 227 * 1024;
+        const int n2 = p->nfft / 64;
+        if (p->hop <= L && (sst::fwd_layout(n2, L, p->hop).total > kMaxSmem ||
+                            sst::inv_layout(n2, L, p->hop, p->zoom).total > kMaxSmem)) {
+            msg = "window / hop too large for this build's shared-memory tiles (227 KB per CTA)";
+            return SST_E_UNSUPPORTED;
+        }
+    }
     // coverage (R20): every n in [0, N) needs d[n] > 0
     const int64_t N = p->n;
     const int64_t F = frames_of(N, p->hop);

@@ -85,6 +85,8 @@ BASE = dict(n=4096, fs=1024.0, win_len=257, sigma=32.0, hop=1, nfft=4096, f1=0.0
     ({"zoom": 65}, 3),
     ({"flags": 4}, 0),                        # DETERMINISTIC accepted (always reproducible)
     ({"hop": 258}, 2),                        # H_t > L -> gaps (R20)
+    ({"win_len": 4096, "sigma": 512.0, "hop": 4096, "n": 4097 * 4096}, 3),   # tiles beyond 227 KB smem
+    ({"nfft": 8192, "n": 8192, "win_len": 5745, "sigma": 882.0, "hop": 1149}, 0),   # §5.1 shape
     ({"win_len": 64, "sigma": 8.0, "hop": 64, "nfft": 4096, "n": 4136}, 2),   # tail uncovered
 ])
 def test_validation_codes(P, change, status):
