@@ -311,6 +311,74 @@ def test_config_inverse_sampled(P, name):
         assert rel(y[n0:n1], yo) <= 1e-4, n0
 
 
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_config_inverse_windows(P, name):
+    """C4 / C5 at full size (T of the whole record is 64 / 256 GiB): the forward of the frames
+    covering sampled output windows, sst_inverse_accumulate of those frames into a window buffer and
+    sst_inverse_finalize, against the oracle's inverse of the same T rows; both record edges."""
+    cfg = get_config(name)
+    x = signal(name)
+    g, gd, c = O.gaussian_window(cfg.L, cfg.sigma)
+    plan = make_plan(P, cfg, config_gamma(cfg, x))
+    xd = torch.from_numpy(x).to(DEV)
+    rng = np.random.default_rng(4)
+    W = 8 * cfg.L
+    for n0 in [0, cfg.N - W] + list(rng.integers(0, cfg.N - W, size=2)):
+        n0 = int(n0)
+        n1 = n0 + W
+        fb = max(0, (n0 + c - cfg.L) // cfg.hop)
+        fe = min(cfg.frames, (n1 - 1 + c) // cfg.hop + 1)
+        T = plan.forward(xd, fb, fe)
+        lo = max(0, fb * cfg.hop - c)
+        hi = min(cfg.N, (fe - 1) * cfg.hop - c + cfg.L)
+        y = torch.zeros(hi - lo, dtype=torch.float32, device=DEV)
+        plan.inverse_accumulate(T, fb, fe, y, y_off=lo)
+        plan.inverse_finalize(y[n0 - lo:n1 - lo], y_off=n0)
+        yo = O.sst_inverse(T.cpu().numpy().astype(np.complex128), g, c, cfg.hop, cfg.nfft, cfg.zoom, cfg.k1,
+                           cfg.N, frame_begin=fb, n0=n0, n1=n1)
+        assert rel(y[n0 - lo:n1 - lo].cpu().numpy(), yo) <= 1e-4, (name, n0)
+
+
+EXTREME = [
+    # (N, fs, L, sigma, hop, nfft, f1, f2, z): smallest N_f with z = 64 (z N_f = 8192), a short
+    # window far below N_f, hop = L (no overlap), hop = 1 with a narrow band at the top edge
+    (3000, 1024.0, 96, 12.0, 5, 128, 0.0, 512.0, 64),
+    (20000, 4096.0, 9, 1.5, 2, 512, 0.0, 2048.0, 2),
+    (16256, 2048.0, 256, 32.0, 256, 256, 256.0, 768.0, 3),
+    (6000, 1000.0, 128, 16.0, 1, 128, 437.5, 500.0, 7),
+]
+
+
+@pytest.mark.parametrize("spec", EXTREME, ids=[f"nf{s[5]}_L{s[2]}_h{s[4]}_z{s[8]}" for s in EXTREME])
+def test_extreme_parameters(P, spec):
+    N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c = _case(spec)
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=1e-5, device=0)
+    xd = torch.from_numpy(x).to(DEV)
+    S, Sd = plan.stft(xd)
+    So = O.stft(x.astype(np.float64), g, c, hop, nfft)
+    assert rel(S.cpu().numpy(), So) <= 1e-5
+    T = plan.forward(xd)
+    To, So64, Sdo64, lo = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, 1e-5, debug=True)
+    lg = plan.targets(xd).cpu().numpy()
+    Tmap = O.squeeze(So64, lg.astype(np.int64), T.shape[1])
+    assert rel(T.cpu().numpy(), Tmap) <= 1e-5
+    _, _, fhat = O.if_estimate(So64, Sdo64, nfft, 1e-5)
+    st = flip_stats(lg, lo, So64, fhat, plan.layout["k1"], z)
+    ds = decision_stats(lg, S.cpu().numpy(), Sd.cpu().numpy(), 1e-5, nfft, plan.layout["k1"], T.shape[1], z)
+    e = rel(T.cpu().numpy(), To)
+    # decisions on the kernel's own spectra: exact up to 1e-4 bins (R21); against the fp64 spectra
+    # the flip rate grows with z (the fp32 error of r is magnified z times on the fine grid) and a
+    # 9-tap window makes r ill-conditioned, so these deliberately extreme cases allow z/8 x the
+    # north-star rate, and a plane error above 1e-3 only from that handful of flips
+    assert ds["far"] <= 1e-4 and ds["bad_mask"] == 0, ds
+    assert st["frac"] <= 1e-4 * max(1.0, z / 8), (e, st)
+    assert e <= 1e-3 or st["frac"] <= 2e-5 * max(1.0, z / 8), (e, st)
+    y = plan.inverse(T).cpu().numpy()
+    yo = O.sst_inverse(T.cpu().numpy().astype(np.complex128), g, c, hop, nfft, z, plan.layout["k1"], N)
+    assert rel(y, yo) <= 1e-4
+
+
 def test_error_codes(P):
     spec = SMALL[3]
     N, fs, L, sigma, hop, nfft, f1, f2, z = spec
