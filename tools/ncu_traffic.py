@@ -1,12 +1,12 @@
-"""Write profiles/traffic.json from an ncu --set full capture of bench.py's kernels:
-    python tools/ncu_traffic.py rep.ncu-rep WORKLOAD FRAMES"""
+"""Write profiles/traffic.json (or OUT) from an ncu --set full capture of bench.py's kernels:
+    python tools/ncu_traffic.py rep.ncu-rep WORKLOAD FRAMES [OUT]"""
 import csv, io, json, os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rep, workload, frames = sys.argv[1], sys.argv[2], int(sys.argv[3])
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h, units = rows[0], rows[1]
-path = os.path.join(ROOT, "profiles", "traffic.json")
+path = sys.argv[4] if len(sys.argv) > 4 else os.path.join(ROOT, "profiles", "traffic.json")
 t = json.load(open(path)) if os.path.exists(path) else {}
 for r in rows[2:]:
     d = dict(zip(h, r))
