@@ -86,7 +86,6 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
     while (S <= cols) S <<= 1;                             // S > cols: every p in [1, cols] has a level
     int levels = 0;
     while ((1 << levels) < S) ++levels;
-    __shared__ int s_last;
     const double floor_e = *floor_in;
 
     for (int q = 0; q < count; ++q) {
@@ -170,7 +169,6 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
                     cur = back[m * cols + cur];
                     path[m - 1] = cur;
                 }
-                s_last = 0;
             }
         }
         __syncthreads();
