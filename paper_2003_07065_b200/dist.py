@@ -32,6 +32,8 @@ class Shard:
     seam_in: int      # length of the left seam received from rank-1 (0 for rank 0)
     seam_out: int     # length of the right seam sent to rank+1 (0 for the last rank)
 
+    frames_total: int = 0   # F of the whole record
+
     @property
     def frames(self) -> int:
         return self.frame_end - self.frame_begin
@@ -65,7 +67,7 @@ def shard(n: int, hop: int, win_len: int, center: int, world: int, rank: int) ->
         lo = max(0, fe * hop - center)
         hi = min(n, (fe - 1) * hop - center + win_len)
         seam_out = max(0, hi - lo)
-    return Shard(rank, world, fb, fe, span_lo, span_hi, own_lo, own_hi, seam_in, seam_out)
+    return Shard(rank, world, fb, fe, span_lo, span_hi, own_lo, own_hi, seam_in, seam_out, F)
 
 
 def exchange_seams(y_span: torch.Tensor, sh: Shard, hop: int, center: int, group=None) -> torch.Tensor:
@@ -111,6 +113,31 @@ def gather_owned(y_own: torch.Tensor, sh: Shard, n: int, dst: int = 0, group=Non
     if sh.rank != dst:
         return None
     return torch.cat([b[:int(s.item())] for b, s in zip(bufs, sizes)])[:n]
+
+
+def gather_band(T_local: torch.Tensor, sh: Shard, dst: int = 0, group=None):
+    """Collect the ranks' band rows T[frame_begin:frame_end, :B] into the whole-record plane on
+    ``dst`` (row order = rank order = frame order; SURVEY §8(e) 'optional band gather', for
+    verification and small records -- excluded from throughput).  Complex tensors travel as their
+    real view; ranks' row counts may differ by one.  Returns [F, B] on dst, None elsewhere."""
+    if sh.world == 1:
+        return T_local
+    rows_per = [frames_of_rank(sh, r) for r in range(sh.world)]
+    mx = max(rows_per)
+    real = torch.view_as_real(T_local.contiguous())                  # [rows, B, 2]
+    pad = torch.zeros((mx,) + tuple(real.shape[1:]), dtype=real.dtype, device=real.device)
+    pad[:real.shape[0]] = real
+    bufs = [torch.zeros_like(pad) for _ in range(sh.world)]
+    dist.all_gather(bufs, pad, group=group)
+    if sh.rank != dst:
+        return None
+    return torch.view_as_complex(torch.cat([b[:n] for b, n in zip(bufs, rows_per)]).contiguous())
+
+
+def frames_of_rank(sh: Shard, r: int) -> int:
+    """Frame count of rank r under the same partition as ``shard``."""
+    F = sh.frames_total
+    return F * (r + 1) // sh.world - F * r // sh.world
 
 
 def max_over_ranks(value: float, device, group=None) -> float:

@@ -71,8 +71,9 @@ def _worker(rank, world, port, case, out_q):
         own = own / torch.from_numpy(C * d_own)
         full = D.gather_owned(own.contiguous(), sh, N)
         mx = D.max_over_ranks(float(rank), torch.device("cpu"))
+        Tg = D.gather_band(torch.from_numpy(T[sh.frame_begin:sh.frame_end].astype(np.complex64)), sh)
         if rank == 0:
-            out_q.put((full.numpy(), mx))
+            out_q.put((full.numpy(), mx, Tg.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -88,7 +89,7 @@ def test_sharded_inverse_equals_single(world, case):
     procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
     for p in procs:
         p.start()
-    full, mx = q.get(timeout=120)
+    full, mx, Tg = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -96,6 +97,7 @@ def test_sharded_inverse_equals_single(world, case):
     assert full.shape == (N,)
     err = np.max(np.abs(full - ref)) / np.max(np.abs(ref))
     assert err < 1e-12, err
+    assert np.array_equal(Tg, T.astype(np.complex64))              # band gather restores the plane
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 5, 8])
