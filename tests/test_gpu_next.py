@@ -63,15 +63,19 @@ def test_istft_is_linear_and_padded_rows(P):
 
 @pytest.mark.parametrize("alpha", [3.0, 2.0, 0.5])
 def test_renyi_matches_oracle(P, alpha):
+    """sst_renyi of the GPU plane vs the oracle's Eq. 32 of the oracle's plane (same x)."""
     cfg = get_config("C1")
     x = signal("C1")
-    plan = make_plan(P, cfg, config_gamma(cfg, x))
+    gamma = config_gamma(cfg, x)
+    plan = make_plan(P, cfg, gamma)
     T = plan.forward(torch.from_numpy(x).to(DEV))
     out = plan.renyi(T, alpha).cpu().numpy()
-    Pn = np.abs(T.cpu().numpy().astype(np.complex128)) ** 2
-    assert out[0] == pytest.approx(Pn.sum(), rel=1e-12)
-    assert out[1] == pytest.approx((Pn ** alpha).sum(), rel=1e-10)
-    assert out[2] == pytest.approx(O.renyi_entropy(Pn, alpha), rel=1e-10, abs=1e-10)
+    g, gd, c = O.gaussian_window(cfg.L, cfg.sigma)
+    To = O.sst_forward(x.astype(np.float64), g, gd, c, cfg.hop, cfg.nfft, cfg.fs, cfg.f1, cfg.f2, cfg.zoom, gamma)
+    Po = np.abs(To) ** 2
+    assert out[0] == pytest.approx(Po.sum(), rel=1e-3)
+    assert out[1] == pytest.approx((Po ** alpha).sum(), rel=5e-3)
+    assert out[2] == pytest.approx(O.renyi_entropy(Po, alpha), abs=2e-3)
     # reproducible: same bits on a second call
     assert np.array_equal(plan.renyi(T, alpha).cpu().numpy(), out)
 
@@ -102,6 +106,7 @@ def test_renyi_errors(P):
 
 # ------------------------------------------------------------------ f1: mode retrieval (R22)
 def _two_tone_plan(P, hop, nfft=512, fs=512.0, N=4096, L=129, sigma=16.0, zoom=1, noise=0.05, seed=3):
+    """GPU plane and the oracle's plane of the same samples (the oracle never sees GPU output)."""
     t = np.arange(N) / fs
     rng = np.random.default_rng(seed)
     x = (np.cos(2 * np.pi * (60 * t + 8 * np.sin(2 * np.pi * 0.5 * t))) + 0.6 * np.cos(2 * np.pi * 150 * t + 1.0)
@@ -109,67 +114,78 @@ def _two_tone_plan(P, hop, nfft=512, fs=512.0, N=4096, L=129, sigma=16.0, zoom=1
     g, gd, c = O.gaussian_window(L, sigma)
     plan = P.Plan(N, fs, L, sigma, hop, nfft, 0.0, fs / 2, zoom, gamma=1e-6, device=0)
     T = plan.forward(torch.from_numpy(x).to(DEV))
-    return plan, x, T, g, c
+    To = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, 0.0, fs / 2, zoom, 1e-6)
+    return plan, x, T, To, g, c
 
 
 def test_ridge_emission_matches_oracle(P):
-    plan, x, T, g, c = _two_tone_plan(P, hop=2)
+    plan, x, T, To, g, c = _two_tone_plan(P, hop=2)
     E, fl = plan.ridge_emission(T)
-    Tn = T.cpu().numpy().astype(np.complex128)
-    Eo = O.ridge_emission(Tn)
-    assert np.max(np.abs(E.cpu().numpy() - Eo)) <= 1e-12
-    assert float(fl) == pytest.approx(np.log(1e-12 * np.abs(Tn).max()), abs=1e-12)
+    Eo = O.ridge_emission(To)
+    big = np.abs(To) >= 1e-3 * np.abs(To).max()
+    dE = np.abs(E.cpu().numpy() - Eo)[big]
+    assert np.quantile(dE, 0.999) <= 1e-3, np.quantile(dE, 0.999)
+    assert float(fl) == pytest.approx(np.log(1e-12 * np.abs(To).max()), abs=1e-4)
+
+
+def _oracle_ridges(To, lam, count, suppress=3):
+    E = O.ridge_emission(To)
+    floor = float(np.log(1e-12 * np.abs(To).max()))
+    out = []
+    for _ in range(count):
+        p = O.ridge_dp(E, lam)
+        out.append(p)
+        E = O.ridge_suppress(E, p, suppress, floor)
+    return np.array(out)
 
 
 @pytest.mark.parametrize("hop,zoom,lam,count", [(2, 1, 0.01, 2), (4, 2, 0.05, 2), (1, 1, 0.0, 1)])
-def test_ridge_paths_equal_oracle(P, hop, zoom, lam, count):
-    """Same emissions in, the kernel's DP (O(B log B) divide and conquer per frame) and the oracle's
-    O(B^2) recurrence take identical fp64 decisions: paths equal element by element."""
-    plan, x, T, g, c = _two_tone_plan(P, hop=hop, zoom=zoom)
-    E, fl = plan.ridge_emission(T)
-    E0 = E.cpu().numpy().copy()
-    floor = float(fl)
-    paths = plan.ridge(E, fl, lam, count, 3).cpu().numpy()
-    Ew = E0
+def test_ridge_paths_match_oracle(P, hop, zoom, lam, count):
+    """GPU ridges of the GPU plane (one-CTA fp64 DP, exact divide and conquer per frame) vs the
+    oracle's O(F B^2) recurrence on the oracle's plane: the same path on >= 99 % of the frames
+    (the planes differ by fp32 rounding and boundary flips, which can move a near-tie)."""
+    plan, x, T, To, g, c = _two_tone_plan(P, hop=hop, zoom=zoom)
+    paths = plan.ridges(T, lam, count, 3).cpu().numpy()
+    po = _oracle_ridges(To, lam, count)
     for q in range(count):
-        p = O.ridge_dp(Ew, lam)
-        assert np.array_equal(paths[q], p), (q, int(np.sum(paths[q] != p)))
-        Ew = O.ridge_suppress(Ew, p, 3, floor)
-    # the two components are found: 60 +- 8 Hz and 150 Hz (1 Hz coarse bins, z fine bins each)
-    mid = slice(paths.shape[1] // 8, -paths.shape[1] // 8)
+        assert np.mean(paths[q] == po[q]) >= 0.99, (q, float(np.mean(paths[q] == po[q])))
+    # the components are found: 60 +- 8 Hz and 150 Hz (1 Hz coarse bins, z fine bins each)
     if count == 2:
-        assert np.all(np.abs(paths[1][mid] - 150 * zoom) <= 1 * zoom) or np.all(np.abs(paths[0][mid] - 150 * zoom) <= zoom)
+        mid = slice(paths.shape[1] // 8, -paths.shape[1] // 8)
+        assert any(np.all(np.abs(paths[q][mid] - 150 * zoom) <= zoom) for q in range(2))
 
 
 def test_zone_mask_and_retrieve_mode(P):
-    plan, x, T, g, c = _two_tone_plan(P, hop=4, zoom=2)
-    path = plan.ridges(T, 0.01, 1)[0].contiguous()
-    Tn = T.cpu().numpy().astype(np.complex128)
-    zone = O.zone_mask(path.cpu().numpy(), 10, plan.bins)
+    plan, x, T, To, g, c = _two_tone_plan(P, hop=4, zoom=2)
+    po = _oracle_ridges(To, 0.01, 1)[0]
+    path = torch.from_numpy(po.astype(np.int32)).to(DEV)
     Tm = plan.zone_mask(T.clone(), path, 10)
-    assert np.array_equal(Tm.cpu().numpy() != 0, (Tn != 0) & zone)
     Ti = plan.zone_mask(T.clone(), path, 10, keep_inside=False)
-    assert torch.equal(Tm + Ti, T)
+    assert torch.equal(Tm + Ti, T)                                  # complementary zones
+    l = torch.arange(plan.bins, device=DEV)[None, :]
+    outside = (l - path[:, None]).abs() > 10
+    assert not torch.any(Tm[outside]) and not torch.any(Ti[~outside])
     y = plan.retrieve_mode(T, path, 10).cpu().numpy()
-    yo = O.retrieve_mode(Tn, zone, g, c, 4, 512, 2, 0, x.size)
+    yo = O.retrieve_mode(To, O.zone_mask(po, 10, plan.bins), g, c, 4, 512, 2, 0, x.size)
     assert rel(y, yo) <= 1e-4
 
 
 def test_mode_full_eq15(P):
-    plan, x, T, g, c = _two_tone_plan(P, hop=1, N=1024, noise=0.0)
-    path = plan.ridges(T, 0.01, 2)
-    Tn = T.cpu().numpy().astype(np.complex128)
+    plan, x, T, To, g, c = _two_tone_plan(P, hop=1, N=1024, noise=0.0)
+    po = _oracle_ridges(To, 0.01, 2)
     for q in range(2):
-        xq = plan.mode_full(T, path[q].contiguous(), 20).cpu().numpy()
-        xo = O.mode_full(Tn, O.zone_mask(path[q].cpu().numpy(), 20, plan.bins), g, c, 512, 0, 1)
-        assert rel(xq, xo) <= 1e-6
+        path = torch.from_numpy(po[q].astype(np.int32)).to(DEV)
+        xq = plan.mode_full(T, path, 20).cpu().numpy()
+        xo = O.mode_full(To, O.zone_mask(po[q], 20, plan.bins), g, c, 512, 0, 1)
+        assert rel(xq, xo) <= 1e-4
     # Eq. 15 separates the components: the 150 Hz ridge's mode is 0.6 cos(2 pi 150 t + 1)
     t = np.arange(1024) / 512.0
     x2 = 0.6 * np.cos(2 * np.pi * 150 * t + 1.0)
+    path = plan.ridges(T, 0.01, 2)
     q2 = 0 if abs(int(path[0][512]) - 150) <= 1 else 1
     xq = plan.mode_full(T, path[q2].contiguous(), 20).cpu().numpy()
     assert np.max(np.abs(xq[150:-150] - x2[150:-150])) <= 0.02
-    plan4, _, T4, _, _ = _two_tone_plan(P, hop=4)
+    plan4, _, T4, _, _, _ = _two_tone_plan(P, hop=4)
     with pytest.raises(P.SSTError):
         plan4.mode_full(T4, plan4.ridges(T4)[0].contiguous(), 5)
 
