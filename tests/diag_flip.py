@@ -5,12 +5,12 @@ Compares, on the C1-like parity case, the r (reassignment frequency, Eq. 36) err
   (b) cuFFT complex64 of the separately windowed frames (torch.fft; yardstick only),
   (c) our kernel's fp32 target arithmetic (sst_targets),
 against the fp64 oracle, for coefficients with |S| >= 1e-2 max.
-    python tools/diag_flip.py [frames]
+    python tests/diag_flip.py [frames]
 """
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))   # repo root (tests/ -> ..)
 sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
