@@ -231,3 +231,29 @@ def eq30_noisy(snr_db: float, seed: int, N: int = 8192, fs: float = 1024.0):
     p = np.mean(x ** 2)
     w = np.random.default_rng(seed).standard_normal(N) * np.sqrt(p / 10 ** (snr_db / 10))
     return (x + w).astype(np.float32), (x1, x2, x3)
+
+
+def s52_milling(seed: int = 52, N: int = 573440, fs: float = 10240.0):
+    """Stand-in for the §5.2 milling vibration record (fs = 10240 Hz, 56 s,
+    N = 573440, spindle 9600 r/min, chatter near 1200-1400 Hz from about 28 s).  Synthetic and
+    invented -- not the dataset: harmonics 1-6 of a 160 Hz spindle whose speed fluctuates weakly
+    and quickly (the 4th harmonic stays inside 630-640 Hz, the paper's Fig. 16(e) band), a chatter
+    component whose IF drifts 1310 -> 1345 Hz and whose amplitude rises smoothly around 28 s, and
+    white noise at 10 dB below the clean power.  Returns fp32 x."""
+    rng = np.random.default_rng(seed)
+    t = np.arange(N, dtype=np.float64) / fs
+    a1, a2 = 0.08 * rng.uniform(0.8, 1.2), 0.05 * rng.uniform(0.8, 1.2)
+    f1, f2 = rng.uniform(2.0, 3.0), rng.uniform(6.0, 8.0)
+    # spindle IF 158.9 + a1 sin + a2 sin (Hz); phase = closed-form integral
+    th = 2 * np.pi * (158.9 * t - a1 / (2 * np.pi * f1) * np.cos(2 * np.pi * f1 * t)
+                      - a2 / (2 * np.pi * f2) * np.cos(2 * np.pi * f2 * t))
+    x = np.zeros(N)
+    for h, amp in zip(range(1, 7), (1.0, 0.5, 0.3, 0.4, 0.15, 0.1)):
+        x += amp * np.cos(h * th + rng.uniform(0, 2 * np.pi))
+    T_rec = N / fs
+    ch_phase = 2 * np.pi * (1310.0 * t + 35.0 * t ** 2 / (2 * T_rec))
+    ch_amp = 0.6 / (1.0 + np.exp(-(t - 28.0) / 1.5))
+    x += ch_amp * np.cos(ch_phase + rng.uniform(0, 2 * np.pi))
+    p = np.mean(x ** 2)
+    x += rng.standard_normal(N) * np.sqrt(p / 10.0)
+    return x.astype(np.float32)

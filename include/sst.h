@@ -70,7 +70,9 @@ typedef struct {
     double sigma;         /* Gaussian sigma in samples for the packing scale alpha = sigma*sqrt 2
                              (R18); <= 0 -> alpha = sqrt(sum g^2 / sum g'^2)                  */
     int32_t hop;          /* H_t >= 1                                                  */
-    int32_t nfft;         /* N_f: power of two, L <= N_f <= N; 128..8192 here    */
+    int32_t nfft;         /* N_f: power of two, L <= N_f <= N; 128..65536 here:
+                             <= 8192 fused single-kernel path, 16384..65536 the multi-pass path
+                             (same ABI and results contract; the paper's §5.2 uses 2^15) */
     double f1, f2;        /* band [f1, f2) in Hz, 0 <= f1 < f2 <= fs/2, on the grid fs/N_f (R9)*/
     int32_t zoom;         /* subdivision z >= 1 (Eq. 28-29)                                    */
     double gamma;         /* threshold on |S^g| (Eq. 13, R6), >= 0; absolute unless RELATIVE  */

@@ -41,6 +41,13 @@ struct sst_plan {
     float* d_inv_per = nullptr;     // [hop]
     float* d_absmax = nullptr;      // scratch scalar
     float* d_seam = nullptr;        // [inv_max_grid][2][seam_len]
+    // multi-pass large-N_f path (N_f > kMaxFusedNfft)
+    bool mp = false;
+    float2* d_twN = nullptr;        // [N_f] W_N^k
+    float2* d_mp0 = nullptr;        // FFT scratch, mp_elems float2 each
+    float2* d_mp1 = nullptr;
+    float* d_wf = nullptr;          // [2 mp_inv_pairs][L] windowed frames
+    int64_t mp_fwd_frames = 0, mp_inv_pairs = 0;
     int32_t n_head = 0, n_tail = 0;
     int fwd_grid = 0, inv_grid = 0;
     const float* ext_absmax = nullptr;
@@ -51,7 +58,7 @@ struct sst_plan {
         cudaGetDevice(&prev);
         cudaSetDevice(device);
         for (void* q : {(void*)d_taps, (void*)d_tw, (void*)d_phz, (void*)d_renyi, (void*)d_amax2, (void*)d_back, (void*)d_inv_head, (void*)d_inv_tail,
-                        (void*)d_inv_per, (void*)d_absmax, (void*)d_seam})
+                        (void*)d_inv_per, (void*)d_absmax, (void*)d_seam, (void*)d_twN, (void*)d_mp0, (void*)d_mp1, (void*)d_wf})
             if (q) cudaFree(q);
         cudaSetDevice(prev);
     }
@@ -136,13 +143,13 @@ sst_status validate(const sst_params* p, sst_layout* lay, std::string& msg) {
     if (!(k1 >= 0 && k1 < k2 && k2 <= p->nfft / 2)) { msg = "band outside [0, N_f/2]"; return SST_E_INVALID_ARGUMENT; }
     // library limits
     if (!is_pow2(p->nfft)) { msg = "N_f must be a power of two (P:L93)"; return SST_E_UNSUPPORTED; }
-    if (p->nfft < 128 || p->nfft > 8192) { msg = "this build supports 128 <= N_f <= 8192"; return SST_E_UNSUPPORTED; }
+    if (p->nfft < 128 || p->nfft > sst::kMaxNfft) { msg = "this build supports 128 <= N_f <= 65536"; return SST_E_UNSUPPORTED; }
     if (p->zoom > 64 || (int64_t)p->zoom * p->nfft > (1 << 20)) { msg = "z <= 64 and z N_f <= 2^20 supported"; return SST_E_UNSUPPORTED; }
     {
         // shared-memory footprint of the forward / inverse CTAs (227 KB per CTA on sm_100)
         constexpr int kMaxSmem = 227 * 1024;
         const int n2 = p->nfft / 64;
-        if (p->hop <= L && (sst::fwd_layout(n2, L, p->hop).total > kMaxSmem ||
+        if (p->hop <= L && p->nfft <= sst::kMaxFusedNfft && (sst::fwd_layout(n2, L, p->hop).total > kMaxSmem ||
                             sst::inv_layout(n2, L, p->hop, p->zoom).total > kMaxSmem)) {
             msg = "window / hop too large for this build's shared-memory tiles (227 KB per CTA)";
             return SST_E_UNSUPPORTED;
@@ -281,6 +288,59 @@ int fwd_grid_for(const sst_plan* pl, int64_t nfr) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, pl->fwd_grid));
 }
 
+// forward-family launch on either path; the multi-pass path runs in chunks of mp_fwd_frames
+cudaError_t launch_fwd_any(const sst_plan* pl, const sst::FwdArgs& a, int mode, cudaStream_t st) {
+    if (!pl->mp) return sst::launch_forward(a, mode, fwd_grid_for(pl, a.frame_end - a.frame_begin), st);
+    const int64_t K = pl->lay.nfft / 2 + 1;
+    for (int64_t c0 = a.frame_begin; c0 < a.frame_end; c0 += pl->mp_fwd_frames) {
+        sst::FwdArgs b = a;
+        const int64_t off = c0 - a.frame_begin;
+        b.frame_begin = c0;
+        b.frame_end = std::min<int64_t>(a.frame_end, c0 + pl->mp_fwd_frames);
+        if (b.T) b.T += off * a.ldT;
+        if (b.S) b.S += off * K;
+        if (b.Sd) b.Sd += off * K;
+        if (b.lout) b.lout += off * K;
+        cudaError_t e = sst::launch_mp_forward(b, mode, pl->d_twN, pl->d_mp0, pl->d_mp1, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+// y (+)= the inverse of frames [fb, fe) on the multi-pass path (chunks of 2 mp_inv_pairs frames)
+cudaError_t mp_inverse_accumulate(const sst_plan* pl, const float2* T, int64_t ldT, int64_t fb, int64_t fe,
+                                  int32_t k1, int32_t bins, int32_t zoom, float* y, int64_t y_off, int64_t y_len,
+                                  cudaStream_t st) {
+    sst::MpInvArgs a{};
+    a.ldT = ldT;
+    a.n = pl->lay.n;
+    a.hop = pl->lay.hop;
+    a.L = pl->lay.win_len;
+    a.c = pl->lay.center;
+    a.nfft = pl->lay.nfft;
+    a.zoom = zoom;
+    a.k1 = k1;
+    a.bins = bins;
+    a.taps = pl->d_taps;
+    a.twN = pl->d_twN;
+    a.inv_n = (float)(1.0 / pl->lay.nfft);
+    a.buf0 = pl->d_mp0;
+    a.buf1 = pl->d_mp1;
+    a.wf = pl->d_wf;
+    a.y = y;
+    a.y_off = y_off;
+    a.y_len = y_len;
+    const int64_t step = 2 * pl->mp_inv_pairs;        // buffers hold mp_inv_pairs x plan z >= zoom transforms
+    for (int64_t c0 = fb; c0 < fe; c0 += step) {
+        a.frame_begin = c0;
+        a.frame_end = std::min<int64_t>(fe, c0 + step);
+        a.T = T + (c0 - fb) * ldT;
+        cudaError_t e = sst::launch_mp_inverse_accumulate(a, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 }  // namespace
 
 extern "C" {
@@ -414,14 +474,37 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
     }
     cudaError_t ce = cudaMalloc((void**)&pl->d_absmax, sizeof(float));
     if (ce != cudaSuccess) { delete pl; cudaGetLastError(); return fail(nullptr, SST_E_OUT_OF_MEMORY, "cudaMalloc absmax"); }
-    pl->fwd_grid = sst::forward_max_grid(Nf, L, H, device);
-    pl->inv_grid = sst::inverse_max_grid(Nf, H, L, z, device);
-    const int32_t seam_len = std::max(0, L - H);
-    if (seam_len > 0) {
-        ce = cudaMalloc((void**)&pl->d_seam, sizeof(float) * (size_t)pl->inv_grid * 2 * seam_len);
-        if (ce != cudaSuccess) { delete pl; cudaGetLastError(); return fail(nullptr, SST_E_OUT_OF_MEMORY, "cudaMalloc seams"); }
+    if (Nf > sst::kMaxFusedNfft) {
+        // multi-pass path: W_N table and scratch for a bounded chunk of frames (kMpScratch per buffer)
+        pl->mp = true;
+        std::vector<float2> twN(Nf);
+        for (int32_t k = 0; k < Nf; ++k) {
+            const double a = -2.0 * kPi * k / Nf;
+            twN[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+        }
+        if ((s = upload(pl, &pl->d_twN, twN)) != SST_OK) { msg = pl->err; delete pl; return fail(nullptr, s, msg); }
+        constexpr int64_t kMpScratch = 128ll << 20;
+        const int64_t F = pl->lay.frames, per = (int64_t)Nf * 8;
+        pl->mp_fwd_frames = std::max<int64_t>(1, std::min<int64_t>(F, kMpScratch / per));
+        pl->mp_inv_pairs = std::max<int64_t>(1, std::min<int64_t>((F + 1) / 2, kMpScratch / (per * z)));
+        const size_t elems = (size_t)std::max<int64_t>(pl->mp_fwd_frames, pl->mp_inv_pairs * z) * Nf;
+        if (cudaMalloc((void**)&pl->d_mp0, elems * sizeof(float2)) != cudaSuccess ||
+            cudaMalloc((void**)&pl->d_mp1, elems * sizeof(float2)) != cudaSuccess ||
+            cudaMalloc((void**)&pl->d_wf, sizeof(float) * (size_t)(2 * pl->mp_inv_pairs) * L) != cudaSuccess) {
+            cudaGetLastError();
+            delete pl;
+            return fail(nullptr, SST_E_OUT_OF_MEMORY, "cudaMalloc multi-pass scratch");
+        }
+    } else {
+        pl->fwd_grid = sst::forward_max_grid(Nf, L, H, device);
+        pl->inv_grid = sst::inverse_max_grid(Nf, H, L, z, device);
+        const int32_t seam_len = std::max(0, L - H);
+        if (seam_len > 0) {
+            ce = cudaMalloc((void**)&pl->d_seam, sizeof(float) * (size_t)pl->inv_grid * 2 * seam_len);
+            if (ce != cudaSuccess) { delete pl; cudaGetLastError(); return fail(nullptr, SST_E_OUT_OF_MEMORY, "cudaMalloc seams"); }
+        }
+        if (pl->fwd_grid <= 0 || pl->inv_grid <= 0) { delete pl; return fail(nullptr, SST_E_CUDA, "occupancy query failed"); }
     }
-    if (pl->fwd_grid <= 0 || pl->inv_grid <= 0) { delete pl; return fail(nullptr, SST_E_CUDA, "occupancy query failed"); }
     pl->err.clear();
     if (pl->lay.hf_bound > 0 && pl->lay.hf > pl->lay.hf_bound) {
         char buf[256];
@@ -467,13 +550,13 @@ static sst_status run_forward_mode(sst_plan* plan, int mode, const float* x, int
             m.absmax_out = plan->d_absmax;
             sst_status s = cuda_status(plan, cudaMemsetAsync(plan->d_absmax, 0, sizeof(float), st), "memset");
             if (s != SST_OK) return s;
-            s = cuda_status(plan, sst::launch_forward(m, sst::kModeAbsmax, fwd_grid_for(plan, fe - fb), st), "absmax launch");
+            s = cuda_status(plan, launch_fwd_any(plan, m, sst::kModeAbsmax, st), "absmax launch");
             if (s != SST_OK) return s;
             a.absmax_dev = plan->d_absmax;
         }
     }
     (void)x; (void)x_off; (void)x_len;
-    return cuda_status(plan, sst::launch_forward(a, mode, fwd_grid_for(plan, fe - fb), st), "forward launch");
+    return cuda_status(plan, launch_fwd_any(plan, a, mode, st), "forward launch");
 }
 
 sst_status sst_forward(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len, int64_t frame_begin,
@@ -507,7 +590,7 @@ sst_status sst_stft(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len
     a.gamma2x4 = -1.0f;   // report every bin
     a.src_lo = 0;
     a.src_hi = plan->lay.nfft / 2 + 1;
-    return cuda_status(plan, sst::launch_forward(a, sst::kModeStft, fwd_grid_for(plan, fe - fb), (cudaStream_t)stream),
+    return cuda_status(plan, launch_fwd_any(plan, a, sst::kModeStft, (cudaStream_t)stream),
                        "stft launch");
 }
 
@@ -540,7 +623,7 @@ sst_status sst_absmax(sst_plan* plan, const float* x, int64_t x_off, int64_t x_l
     sst::FwdArgs a = fwd_args(plan, x, x_off, x_len, fb, fe);
     a.absmax_out = out;
     a.gamma2x4 = -1.0f;
-    return cuda_status(plan, sst::launch_forward(a, sst::kModeAbsmax, fwd_grid_for(plan, fe - fb), st), "absmax launch");
+    return cuda_status(plan, launch_fwd_any(plan, a, sst::kModeAbsmax, st), "absmax launch");
 }
 
 static sst::InvArgs inv_args(const sst_plan* pl, const float* T, int64_t ldT, int64_t fb, int64_t fe, float* y,
@@ -598,6 +681,16 @@ static sst::InvArgs istft_args(const sst_plan* pl, const float* S, int64_t ldS, 
 
 static sst_status run_inverse(sst_plan* plan, const float* T, int64_t ldT, int64_t fb, int64_t fe, float* y, int64_t y_off,
                               int64_t y_len, int normalize, void* stream) {
+    if (plan->mp) {
+        cudaStream_t st = (cudaStream_t)stream;
+        sst_status s = SST_OK;
+        if (normalize) s = cuda_status(plan, cudaMemsetAsync(y, 0, sizeof(float) * (size_t)y_len, st), "memset");
+        if (s != SST_OK) return s;
+        s = cuda_status(plan, mp_inverse_accumulate(plan, reinterpret_cast<const float2*>(T), ldT, fb, fe, plan->lay.k1,
+                                                    plan->lay.bins, plan->lay.zoom, y, y_off, y_len, st), "inverse launch");
+        if (s != SST_OK || !normalize) return s;
+        return sst_inverse_finalize(plan, y, y_off, y_len, stream);
+    }
     int grid = 0;
     sst::InvArgs a = inv_args(plan, T, ldT, fb, fe, y, y_off, y_len, normalize, &grid);
     cudaStream_t st = (cudaStream_t)stream;
@@ -632,9 +725,20 @@ sst_status sst_istft(sst_plan* plan, const float* S, int64_t ldS, float* y, void
     if (!S || !y) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL S or y");
     if (ldS < plan->lay.nfft / 2 + 1) return fail(plan, SST_E_INVALID_ARGUMENT, "ldS < N_f/2 + 1");
     DeviceGuard guard(plan->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (plan->mp) {
+        const int64_t N = plan->lay.n;
+        sst_status s = cuda_status(plan, cudaMemsetAsync(y, 0, sizeof(float) * (size_t)N, st), "memset");
+        if (s != SST_OK) return s;
+        s = cuda_status(plan, mp_inverse_accumulate(plan, reinterpret_cast<const float2*>(S), ldS, 0, plan->lay.frames, 0,
+                                                    plan->lay.nfft / 2 + 1, 1, y, 0, N, st), "istft launch");
+        if (s != SST_OK) return s;
+        return cuda_status(plan, sst::launch_finalize(y, 0, N, N, plan->lay.hop, plan->lay.center, plan->d_inv_head,
+                                                      plan->n_head, plan->d_inv_tail, plan->n_tail, plan->d_inv_per,
+                                                      (float)plan->cst, st), "istft finalize");
+    }
     int grid = 0;
     sst::InvArgs a = istft_args(plan, S, ldS, y, &grid);
-    cudaStream_t st = (cudaStream_t)stream;
     sst_status s = cuda_status(plan, sst::launch_inverse(a, grid, st), "istft launch");
     if (s != SST_OK) return s;
     return cuda_status(plan, sst::launch_inverse_seams(a, grid, st), "istft seam launch");
@@ -723,7 +827,7 @@ sst_status sst_inverse_finalize(sst_plan* plan, float* y, int64_t y_off, int64_t
     DeviceGuard guard(plan->device);
     return cuda_status(plan,
                        sst::launch_finalize(y, y_off, y_len, plan->lay.n, plan->lay.hop, plan->lay.center, plan->d_inv_head,
-                                            plan->n_head, plan->d_inv_tail, plan->n_tail, plan->d_inv_per,
+                                            plan->n_head, plan->d_inv_tail, plan->n_tail, plan->d_inv_per, 1.0f,
                                             (cudaStream_t)stream),
                        "finalize launch");
 }

@@ -101,6 +101,31 @@ struct InvArgs {
     int64_t frames_per_cta;           // contiguous chunk per CTA (>= ceil(L/hop))
 };
 
+// Large-N_f multi-pass path (multipass.cu), used for kMaxFusedNfft < N_f <= kMaxNfft
+constexpr int kMaxFusedNfft = 8192;
+constexpr int kMaxNfft = 65536;
+constexpr int kMpBinChunk = 8192;      // band bins per squeeze pass (16 B each in shared memory)
+
+struct MpInvArgs {
+    const float2* T; int64_t ldT;     // row 0 = frame_begin
+    int64_t n;
+    int64_t frame_begin, frame_end;
+    int32_t hop, L, c, nfft, zoom, k1, bins;
+    const float2* taps;               // .x = g
+    const float2* twN;                // [nfft] W_N^k
+    float inv_n;                      // 1 / N_f
+    float2* buf0; float2* buf1;       // [ceil(F/2) z][nfft] each
+    float* wf;                        // [F][L] windowed frames
+    float* y; int64_t y_off, y_len;   // y += (accumulate)
+};
+
+void mp_factor(int nfft, int* r1, int* m);
+int mp_bins_chunk(int bins);
+// frames [frame_begin, frame_end) of the forward in one batch (scratch for all of them)
+cudaError_t launch_mp_forward(const FwdArgs& a, int mode, const float2* twN, float2* buf0, float2* buf1,
+                              cudaStream_t s);
+cudaError_t launch_mp_inverse_accumulate(const MpInvArgs& a, cudaStream_t s);
+
 // launchers (return cudaGetLastError())
 cudaError_t launch_forward(const FwdArgs& a, int mode, int grid, cudaStream_t s);
 int forward_max_grid(int nfft, int L, int H, int device);
@@ -109,7 +134,7 @@ cudaError_t launch_inverse(const InvArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_inverse_seams(const InvArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_finalize(float* y, int64_t y_off, int64_t y_len, int64_t n, int32_t hop, int32_t c,
                             const float* inv_head, int32_t n_head, const float* inv_tail, int32_t n_tail,
-                            const float* inv_per, cudaStream_t s);
+                            const float* inv_per, float out_scale, cudaStream_t s);
 int inverse_max_grid(int nfft, int hop, int L, int zoom, int device);
 
 // Renyi sums over a complex64 plane: partial[2*blockIdx] = {sum |T|^2, sum |T|^(2 alpha)},

@@ -81,7 +81,9 @@ BASE = dict(n=4096, fs=1024.0, win_len=257, sigma=32.0, hop=1, nfft=4096, f1=0.0
     ({"fs": 0.0}, 1),
     ({"flags": 64}, 1),                       # unknown flag
     ({"nfft": 3000}, 3),                      # not a power of two
-    ({"nfft": 16384, "n": 16384}, 3),         # outside this build's N_f range (<= 8192)
+    ({"nfft": 131072, "n": 131072}, 3),       # outside this build's N_f range (<= 65536)
+    ({"nfft": 32768, "n": 573440, "fs": 10240.0, "win_len": 8193, "sigma": 1024.0, "hop": 667,
+      "f1": 1200.0, "f2": 1400.0}, 0),        # §5.2 shape: multi-pass path
     ({"zoom": 65}, 3),
     ({"flags": 4}, 0),                        # DETERMINISTIC accepted (always reproducible)
     ({"hop": 258}, 2),                        # H_t > L -> gaps (R20)

@@ -1,0 +1,202 @@
+"""GPU parity of the large-N_f multi-pass path (8192 < N_f <= 65536) against the
+fp64 oracle.  Shapes: the paper's §5.2 chatter analysis (fs = 10240 Hz, N = 573440,
+sigma = 0.1 s, N_f = 2^15, H = 667 with band 1200-1400 Hz, and H = 200 with band 630-640 Hz, z = 20;
+reading R19 takes the printed "H_f" as H_t) on the synthetic stand-in gen.signals.s52_milling, an
+N_f = 2^14 selective case and an N_f = 2^16 full-band case whose B = 32768 bins exceed one shared-
+memory squeeze pass.  Same tolerances as test_gpu_parity.py; the oracle sees only x and its window.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+import oracle as O  # noqa: E402
+from gen.signals import s52_milling  # noqa: E402
+from tests._helpers import flip_stats, rel  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+S52_N, S52_FS, S52_SIGMA = 573440, 10240.0, 1024.0
+S52_L = 8 * 1024 + 1                      # +-4 sigma (the paper's window length is unstated)
+
+# (name, N, fs, L, sigma, hop, nfft, f1, f2, z)
+BIG = [
+    ("s52_chatter", S52_N, S52_FS, S52_L, S52_SIGMA, 667, 32768, 1200.0, 1400.0, 1),
+    ("s52_spindle_z20", S52_N, S52_FS, S52_L, S52_SIGMA, 200, 32768, 630.0, 640.0, 20),
+    ("nf16k_sel_z3", 200000, 16384.0, 4001, 500.0, 256, 16384, 1000.0, 3000.0, 3),
+    ("nf64k_full", 300000, 65536.0, 20001, 2500.0, 4096, 65536, 0.0, 32768.0, 1),
+]
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2003_07065_b200 as P
+    return P
+
+
+def _sig(name, N, fs):
+    if name.startswith("s52"):
+        return s52_milling(52, N, fs)
+    rng = np.random.default_rng(N)
+    t = np.arange(N) / fs
+    x = 0.5 * np.cos(2 * np.pi * (0.05 * fs * t + 0.01 * fs * t * t / t[-1]))
+    for f in rng.uniform(0.03, 0.45, size=5) * fs:
+        x += rng.uniform(0.3, 1.0) * np.cos(2 * np.pi * f * t + rng.uniform(0, 6.28))
+    x += 0.1 * rng.standard_normal(N)
+    return x.astype(np.float32)
+
+
+def _setup(P, spec, gamma=None):
+    name, N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x = _sig(name, N, fs)
+    g, gd, c = O.gaussian_window(L, sigma)
+    if gamma is None:
+        gamma = 1e-6 * float(np.sum(g)) * float(np.abs(x).max())     # reading R6 (bound from x)
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=gamma, device=0)
+    return x, g, gd, c, gamma, plan
+
+
+def _windows(F, size=24):
+    return [(0, min(F, size)), (F // 2 - size // 2, F // 2 + size // 2), (max(0, F - size), F)]
+
+
+@pytest.mark.parametrize("spec", BIG, ids=[s[0] for s in BIG])
+def test_mp_stft_parity(P, spec):
+    name, N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c, gamma, plan = _setup(P, spec)
+    xd = torch.from_numpy(x).to(DEV)
+    for fb, fe in _windows(plan.frames):
+        S, Sd = plan.stft(xd, fb, fe)
+        fr = np.arange(fb, fe)
+        So = O.stft(x.astype(np.float64), g, c, hop, nfft, frames=fr)
+        Sdo = O.stft(x.astype(np.float64), gd, c, hop, nfft, frames=fr)
+        print(name, "stft", fb, rel(S.cpu().numpy(), So), rel(Sd.cpu().numpy(), Sdo))
+        assert rel(S.cpu().numpy(), So) <= 1e-5, (fb, rel(S.cpu().numpy(), So))
+        assert rel(Sd.cpu().numpy(), Sdo) <= 1e-5, (fb, rel(Sd.cpu().numpy(), Sdo))
+
+
+@pytest.mark.parametrize("spec", BIG, ids=[s[0] for s in BIG])
+def test_mp_forward_parity_and_flips(P, spec):
+    name, N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c, gamma, plan = _setup(P, spec)
+    xd = torch.from_numpy(x).to(DEV)
+    Tall = plan.forward(xd).cpu().numpy()
+    assert Tall.shape == (plan.frames, plan.bins)
+    for fb, fe in _windows(plan.frames):
+        fr = np.arange(fb, fe)
+        lg = plan.targets(xd, fb, fe).cpu().numpy()
+        To, S, Sd, lo = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, gamma,
+                                      frames=fr, debug=True)
+        _, _, fhat = O.if_estimate(S, Sd, nfft, gamma)
+        st = flip_stats(lg, lo, S, fhat, plan.layout["k1"], z, Sd, nfft, plan.layout["alpha"], gamma)
+        assert st["frac"] <= 1e-4, (fb, st)
+        assert st["far"] <= 1e-4 and st["bad_mask"] == 0, (fb, st)
+        e = rel(Tall[fb:fe], To)
+        print(name, "forward", fb, e, st)
+        assert e <= 1e-3 or st["frac"] <= 1e-5, (fb, e, st)
+
+
+@pytest.mark.parametrize("spec", [BIG[0], BIG[2]], ids=[BIG[0][0], BIG[2][0]])
+def test_mp_inverse_whole(P, spec):
+    """Whole-record forward + inverse vs the oracle's inverse (Eq. 25-26) of the oracle's T; the
+    paper reconstructs the 1300-1400 Hz part of the §5.2 record this way (Fig. 17)."""
+    name, N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c, gamma, plan = _setup(P, spec)
+    xd = torch.from_numpy(x).to(DEV)
+    y = plan.inverse(plan.forward(xd)).cpu().numpy()
+    To = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, gamma)
+    yo = O.sst_inverse(To, g, c, hop, nfft, z, plan.layout["k1"], N)
+    print(name, "inverse", rel(y, yo))
+    assert rel(y, yo) <= 1e-4, rel(y, yo)
+
+
+@pytest.mark.parametrize("spec", [BIG[1], BIG[3]], ids=[BIG[1][0], BIG[3][0]])
+def test_mp_inverse_windows(P, spec):
+    """inverse_accumulate of the frames covering sampled output windows + inverse_finalize,
+    against the oracle's forward + inverse of those frames (both record edges)."""
+    name, N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c, gamma, plan = _setup(P, spec)
+    xd = torch.from_numpy(x).to(DEV)
+    W = 2 * L
+    for n0 in (0, N // 2, N - W):
+        n1 = n0 + W
+        fb = max(0, (n0 + c - L) // hop)
+        fe = min(plan.frames, (n1 - 1 + c) // hop + 1)
+        T = plan.forward(xd, fb, fe)
+        lo = max(0, fb * hop - c)
+        hi = min(N, (fe - 1) * hop - c + L)
+        y = torch.zeros(hi - lo, dtype=torch.float32, device=DEV)
+        plan.inverse_accumulate(T, fb, fe, y, y_off=lo)
+        plan.inverse_finalize(y[n0 - lo:n1 - lo], y_off=n0)
+        To = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, gamma, frames=np.arange(fb, fe))
+        yo = O.sst_inverse(To, g, c, hop, nfft, z, plan.layout["k1"], N, frame_begin=fb, n0=n0, n1=n1)
+        e = rel(y[n0 - lo:n1 - lo].cpu().numpy(), yo)
+        print(name, "inverse window", n0, e)
+        assert e <= 1e-4, (n0, e)
+
+
+def test_mp_istft_round_trip(P):
+    """Eq. 10-11 synthesis of the analysis is exact (pin P4) on the multi-pass path too."""
+    spec = BIG[2]
+    name, N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c, gamma, plan = _setup(P, spec)
+    S, _ = plan.stft(torch.from_numpy(x).to(DEV))
+    y = plan.istft(S).cpu().numpy()
+    assert rel(y, x.astype(np.float64)) <= 1e-5
+
+
+def test_mp_bitwise_chunking_and_repeat(P):
+    """The forward is chunked internally (scratch for 512 frames at N_f = 2^15): frame sub-ranges
+    and repeated calls give bitwise the same T (exact fixed-point squeeze)."""
+    spec = BIG[0]
+    x, g, gd, c, gamma, plan = _setup(P, spec)
+    xd = torch.from_numpy(x).to(DEV)
+    T1 = plan.forward(xd)
+    T2 = plan.forward(xd)
+    assert torch.equal(T1, T2)
+    F = plan.frames
+    parts = [plan.forward(xd, a, b) for a, b in ((0, 300), (300, 301), (301, F))]
+    assert torch.equal(torch.cat(parts), T1)
+    # x slice with an offset
+    fb, fe = 500, 560
+    lo = fb * spec[5] - c
+    hi = min(spec[1], (fe - 1) * spec[5] - c + spec[3])
+    Ts = plan.forward(xd[lo:hi].contiguous(), fb, fe, x_off=lo)
+    assert torch.equal(Ts, T1[fb:fe])
+
+
+def test_mp_relative_gamma_and_absmax(P):
+    """SST_GAMMA_RELATIVE on the multi-pass path: the absmax pre-pass matches the oracle's max|S|,
+    and the forward with gamma = 1e-3 max|S| matches the oracle at its own (fp64) threshold."""
+    spec = BIG[2]
+    name, N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x = _sig(name, N, fs)
+    g, gd, c = O.gaussian_window(L, sigma)
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=1e-3, flags=P.SST_GAMMA_RELATIVE, device=0)
+    xd = torch.from_numpy(x).to(DEV)
+    amax = float(plan.absmax(xd).cpu())
+    So = O.stft(x.astype(np.float64), g, c, hop, nfft)
+    ref = float(np.abs(So).max())
+    assert abs(amax - ref) <= 1e-5 * ref
+    T = plan.forward(xd).cpu().numpy()
+    lg = plan.targets(xd).cpu().numpy()
+    gamma = 1e-3 * ref
+    To, S, Sd, lo = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, gamma, debug=True)
+    _, _, fhat = O.if_estimate(S, Sd, nfft, gamma)
+    st = flip_stats(lg, lo, S, fhat, plan.layout["k1"], z, Sd, nfft, plan.layout["alpha"], gamma)
+    assert st["frac"] <= 1e-4 and st["far"] <= 1e-4, st
+    # mask disagreements must sit within what separates the two sides from the threshold: the fp32
+    # STFT's error in |S| (the R21 error model, eta/2 per bin of frame m) plus the fp32 rounding of
+    # the GPU's max|S| (<= 1e-5 relative)
+    aS = np.abs(S)
+    zn2 = 2.0 / nfft * np.sum(aS ** 2 + plan.layout["alpha"] ** 2 * np.abs(Sd) ** 2, axis=1, keepdims=True)
+    eta = 4.0 * 2.0 ** -24 * np.sqrt(np.log2(nfft)) * np.sqrt(zn2)
+    mdiff = (lg == -1) != (lo == -1)
+    assert mdiff.sum() <= 1e-4 * mdiff.size
+    assert not (mdiff & (np.abs(aS - gamma) > eta / 2 + 2e-5 * gamma)).any()
+    e = rel(T, To)
+    assert e <= 1e-3 or st["frac"] <= 1e-5, (e, st)

@@ -173,11 +173,13 @@ def test_absmax_and_relative_gamma(P):
     T = plan.forward(xd).cpu().numpy()
     To = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, 0.05 * float(np.abs(So).max()))
     assert rel(T, To) <= 1e-3
-    # externally supplied max (as all-reduced over ranks)
-    ext = torch.tensor(2.0 * m, dtype=torch.float32, device=DEV)
+    # externally supplied max (as all-reduced over ranks); the oracle's threshold comes from its own
+    # max, never from the GPU's
+    ref = float(np.abs(So).max())
+    ext = torch.tensor(2.0 * ref, dtype=torch.float32, device=DEV)
     plan.set_absmax(ext)
     T2 = plan.forward(xd).cpu().numpy()
-    To2 = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, 0.1 * m)
+    To2 = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, 0.1 * ref)
     assert rel(T2, To2) <= 1e-3
 
 
