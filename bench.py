@@ -237,6 +237,17 @@ def measure_extras(P, plan, cfg, x, T, y, stream, ev, reps=5):
     out["f1_ridge2_mode_c1_ms"] = timed(ridge_and_mode)
     out["f1_config"] = f"C1: F={c1.frames}, B={c1.bins}, 2 ridges (lambda 0.01) + Eq. 15 retrieval"
     p1.close()
+    # f3: the paper's §5.2 Fig. 16(c) shape (N_f = 2^15, H_t = 667, 1200-1400 Hz) on the synthetic
+    # stand-in, through the multi-pass large-N_f path
+    from gen.signals import s52_milling
+    x5 = torch.from_numpy(s52_milling()).to(x.device)
+    p5 = P.Plan(573440, 10240.0, 8193, 1024.0, 667, 32768, 1200.0, 1400.0, 1, gamma=1e-6, device=x.device.index)
+    T5 = torch.empty((p5.frames, p5.bins), dtype=torch.complex64, device=x.device)
+    y5 = torch.empty(573440, dtype=torch.float32, device=x.device)
+    out["f3_s52_forward_ms"] = timed(lambda: p5.forward(x5, out=T5))
+    out["f3_s52_inverse_ms"] = timed(lambda: p5.inverse(T5, out=y5))
+    out["f3_config"] = f"§5.2 Fig. 16(c) shape: N=573440, N_f=32768, H_t=667, F={p5.frames}, B={p5.bins} (paper: 0.8 s MATLAB)"
+    p5.close()
     return out
 
 

@@ -125,6 +125,56 @@ struct FftComposite {
     }
 };
 
+// x * W_8^e for the transform direction (compile-time e): swaps / sign flips and at most one
+// add + scale, W_8^{odd} = h (+-1 +- i)
+template <int DIR>
+__device__ __forceinline__ float2 mul_w8(float2 x, int e) {
+    const float h = 0.70710678118654752440f;
+    switch (e & 7) {
+        case 0: return x;
+        case 2: return rot90<DIR>(x);
+        case 4: return make_float2(-x.x, -x.y);
+        case 6: { const float2 r = rot90<DIR>(x); return make_float2(-r.x, -r.y); }
+        case 1: return cscale(cadd(x, rot90<DIR>(x)), h);
+        case 3: return cscale(csub(rot90<DIR>(x), x), h);
+        case 5: return cscale(cadd(x, rot90<DIR>(x)), -h);
+        default: return cscale(csub(x, rot90<DIR>(x)), h);
+    }
+}
+
+// 64-point DFT of an input that is zero outside rows [0, 8 NZ) and [64 - 8 NZ, 64) (the inverse's
+// narrow-band sub-spectra, RM = 8 NZ): as FftComposite<64, 8>, but each first-stage 8-point DFT
+// has only 2 NZ nonzero inputs (n1 in [0, NZ) and [8 - NZ, 8)) and is a direct sum.
+template <int DIR, int NZ>
+struct FftSparse64 {
+    __device__ __forceinline__ static void run(float2 (&a)[64]) {
+        float2 b[8][8];
+#pragma unroll
+        for (int n2 = 0; n2 < 8; ++n2) {
+#pragma unroll
+            for (int k1 = 0; k1 < 8; ++k1) {
+                float2 acc = a[n2];
+#pragma unroll
+                for (int n1 = 1; n1 < 8; ++n1) {
+                    if (n1 >= NZ && n1 < 8 - NZ) continue;
+                    acc = cadd(acc, mul_w8<DIR>(a[8 * n1 + n2], n1 * k1));
+                }
+                const int e = n2 * k1;
+                b[n2][k1] = (e == 0) ? acc : cmul(acc, twiddle<64, DIR>(e));
+            }
+        }
+#pragma unroll
+        for (int k1 = 0; k1 < 8; ++k1) {
+            float2 u[8];
+#pragma unroll
+            for (int n2 = 0; n2 < 8; ++n2) u[n2] = b[n2][k1];
+            Fft<8, DIR>::run(u);
+#pragma unroll
+            for (int k2 = 0; k2 < 8; ++k2) a[k1 + 8 * k2] = u[k2];
+        }
+    }
+};
+
 template <int DIR>
 struct Fft<16, DIR> {
     __device__ __forceinline__ static void run(float2 (&a)[16]) { FftComposite<16, 4, DIR>::run(a); }

@@ -587,7 +587,8 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
                 v[n1] = inb ? make_float2(ta.x - tb.y, ta.y + tb.x)    // H_A + i H_B
                             : make_float2(ta.x + tb.y, tb.x - ta.y);   // conj H_A + i conj H_B
             }
-            Fft<64, +1>::run(v);
+            if constexpr (RM == 8 || RM == 16) FftSparse64<+1, RM / 8>::run(v);   // zero rows skipped
+            else Fft<64, +1>::run(v);
 #pragma unroll
             for (int kk = 0; kk < 64; ++kk) {
                 float2 t = v[kk];

@@ -3,6 +3,7 @@ multi-pass large-N_f path, on the synthetic stand-in gen.signals.s52_milling (no
 Context, not targets: the paper's 0.8 s / 3 s are MATLAB on an i5-8250 "after 20 averages".
 
     python tools/s52_timing.py [out.json]
+    python tools/s52_timing.py --once     # one forward + one inverse of the Fig. 16(c) shape (for ncu)
 """
 import json
 import os
@@ -36,7 +37,17 @@ def timed(fn, reps=20):
     return a.elapsed_time(b) / reps
 
 
+def once():
+    x = torch.from_numpy(s52_milling(52, N, FS)).cuda()
+    s = SHAPES["fig16c_chatter_Ht667_1200_1400"]
+    pl = P.Plan(N, FS, L, SIGMA, s["hop"], 32768, s["f1"], s["f2"], s["zoom"], gamma=1e-6, device=0)
+    pl.inverse(pl.forward(x))
+    torch.cuda.synchronize()
+
+
 def main():
+    if "--once" in sys.argv:
+        return once()
     x = torch.from_numpy(s52_milling(52, N, FS)).cuda()
     res = {"signal": "gen.signals.s52_milling (synthetic stand-in), N = 573440, fs = 10240 Hz, sigma = 0.1 s, "
                      "L = 8193, N_f = 2^15", "note": "20-call averages, CUDA events"}
