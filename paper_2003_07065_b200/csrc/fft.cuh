@@ -142,10 +142,11 @@ __device__ __forceinline__ float2 mul_w8(float2 x, int e) {
     }
 }
 
-// 64-point DFT of an input that is zero outside rows [0, 8 NZ) and [64 - 8 NZ, 64) (the inverse's
-// narrow-band sub-spectra, RM = 8 NZ): as FftComposite<64, 8>, but each first-stage 8-point DFT
-// has only 2 NZ nonzero inputs (n1 in [0, NZ) and [8 - NZ, 8)) and is a direct sum.
-template <int DIR, int NZ>
+// 64-point DFT of an input that is zero outside rows [0, RM) and [64 - RM, 64) (the inverse's
+// narrow-band sub-spectra): as FftComposite<64, 8>, but each first-stage 8-point sub-DFT
+// (inputs a[8 n1 + n2], n1 = 0..7) is a direct sum over its nonzero inputs only -- the packed
+// FP32x2 intrinsics are opaque to the compiler, so it would not drop the zero terms by itself.
+template <int DIR, int RM>
 struct FftSparse64 {
     __device__ __forceinline__ static void run(float2 (&a)[64]) {
         float2 b[8][8];
@@ -153,14 +154,18 @@ struct FftSparse64 {
         for (int n2 = 0; n2 < 8; ++n2) {
 #pragma unroll
             for (int k1 = 0; k1 < 8; ++k1) {
-                float2 acc = a[n2];
+                float2 acc = make_float2(0.0f, 0.0f);
+                bool first = true;
 #pragma unroll
-                for (int n1 = 1; n1 < 8; ++n1) {
-                    if (n1 >= NZ && n1 < 8 - NZ) continue;
-                    acc = cadd(acc, mul_w8<DIR>(a[8 * n1 + n2], n1 * k1));
+                for (int n1 = 0; n1 < 8; ++n1) {
+                    const int n = 8 * n1 + n2;
+                    if (n >= RM && n < 64 - RM) continue;             // compile-time zero row
+                    const float2 t = mul_w8<DIR>(a[n], n1 * k1);
+                    acc = first ? t : cadd(acc, t);
+                    first = false;
                 }
                 const int e = n2 * k1;
-                b[n2][k1] = (e == 0) ? acc : cmul(acc, twiddle<64, DIR>(e));
+                b[n2][k1] = (e == 0 || first) ? acc : cmul(acc, twiddle<64, DIR>(e));
             }
         }
 #pragma unroll

@@ -480,6 +480,13 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
 }
 
 // ------------------------------------------------------------------------------- inverse ------
+// 1/(C d[s]) given r = (s + c) mod hop
+__device__ __forceinline__ float inv_norm_r(int64_t s, int r, const InvArgs& a) {
+    if (s < a.n_head) return __ldg(a.inv_head + s);
+    if (s >= a.n - a.n_tail) return __ldg(a.inv_tail + (s - (a.n - a.n_tail)));
+    return __ldg(a.inv_per + r);
+}
+
 __device__ __forceinline__ float inv_norm(int64_t s, const InvArgs& a) {
     if (s < a.n_head) return __ldg(a.inv_head + s);
     if (s >= a.n - a.n_tail) return __ldg(a.inv_tail + (s - (a.n - a.n_tail)));
@@ -494,7 +501,7 @@ __device__ __forceinline__ float inv_norm(int64_t s, const InvArgs& a) {
 // g[tau + c]/N and adds frame A (real part) and frame B (imaginary part) into the OLA ring.
 // RM: every nonzero sub-spectrum entry q (band [k1, k2) or mirror [N - k2, N)) has
 // q / N2 in [0, RM) or [64 - RM, 64) (i.e. ceil(k2 / N2) <= RM): other rows of the step-1
-// input are compile-time zeros and cost nothing (narrow bands: C2, C3, C4 use RM = 8).
+// input are compile-time zeros and cost nothing (narrow bands: C2, C3 use RM = 5, C4 RM = 8).
 template <int N2, bool FULLWIN, int RM>
 __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 256 ? 1 : 2) inv_kernel(const InvArgs a) {
     using Gm = Geom<N2, false>;
@@ -587,7 +594,7 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
                 v[n1] = inb ? make_float2(ta.x - tb.y, ta.y + tb.x)    // H_A + i H_B
                             : make_float2(ta.x + tb.y, tb.x - ta.y);   // conj H_A + i conj H_B
             }
-            if constexpr (RM == 8 || RM == 16) FftSparse64<+1, RM / 8>::run(v);   // zero rows skipped
+            if constexpr (RM < 32) FftSparse64<+1, RM>::run(v);   // zero rows skipped
             else Fft<64, +1>::run(v);
 #pragma unroll
             for (int kk = 0; kk < 64; ++kk) {
@@ -735,6 +742,7 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
             } else if (!last_cta && s >= right_start) {
                 a.seam[((int64_t)blockIdx.x * 2 + 1) * a.seam_len + (s - right_start)] = val;
             } else if (a.normalize) {
+                // (a per-sample 32-bit mod_pos here measured 4 % slower on C4: one more live register)
                 a.y[s - a.y_off] = val * inv_norm(s, a) * a.out_scale;
             } else {
                 a.y[s - a.y_off] += val;
@@ -761,10 +769,16 @@ __global__ void seam_kernel(const InvArgs a, int ctas) {
 }
 
 __global__ void finalize_kernel(float* y, int64_t y_off, int64_t y_len, InvArgs a) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < y_len; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // r = (s + c) mod hop, advanced incrementally (one 64-bit modulo per thread)
+    int r = (int)(((y_off + i + a.c) % a.hop + a.hop) % a.hop);
+    const int step = (int)(stride % a.hop);
+    for (; i < y_len; i += stride) {
         const int64_t s = y_off + i;
-        if (s < 0 || s >= a.n) continue;
-        y[i] *= inv_norm(s, a) * a.out_scale;
+        if (s >= 0 && s < a.n) y[i] *= inv_norm_r(s, r, a) * a.out_scale;
+        r += step;
+        r -= (r >= a.hop) ? a.hop : 0;
     }
 }
 
@@ -852,6 +866,7 @@ static cudaError_t launch_inv_b(const InvArgs& a, int grid, cudaStream_t s) {
 template <int N2, bool FULLWIN>
 static cudaError_t launch_inv_r(const InvArgs& a, int grid, cudaStream_t s) {
     const int rows = (a.k1 + a.bins / a.zoom + N2 - 1) / N2;   // ceil(k2 / N2)
+    if (rows <= 5) return launch_inv_b<N2, FULLWIN, 5>(a, grid, s);   // C2, C3
     if (rows <= 8) return launch_inv_b<N2, FULLWIN, 8>(a, grid, s);
     if (rows <= 16) return launch_inv_b<N2, FULLWIN, 16>(a, grid, s);
     return launch_inv_b<N2, FULLWIN, 64>(a, grid, s);
