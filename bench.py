@@ -321,6 +321,8 @@ def run_ours(args, cfg_base):
     ms_local = t_start.elapsed_time(t_end)
     fwd_ms = sum(a.elapsed_time(b) for a, b, _ in recs) / len(recs)
     inv_ms = sum(b.elapsed_time(cc) for _, b, cc in recs) / len(recs)
+    per_step = sorted(a.elapsed_time(cc) for a, _, cc in recs)      # median and min too
+    step_stats = {"median_ms": per_step[len(per_step) // 2], "min_ms": per_step[0], "max_ms": per_step[-1]}
     ms_total = D.max_over_ranks(ms_local, dev)
     ms_step = ms_total / args.steps
     total_samples = cfg.N
@@ -399,7 +401,7 @@ def run_ours(args, cfg_base):
                        "l2": "inputs larger than L2 (T = %.1f GiB written and read per step)" % (
                            cfg.frames * cfg.bins * 8 / 2 ** 30)},
             "tf_coeffs_per_s": coeffs_per_s,
-            "fwd_ms": fwd_ms, "inv_ms": inv_ms,
+            "fwd_ms": fwd_ms, "inv_ms": inv_ms, "step_ms_stats": step_stats,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "extras": extras,

@@ -44,7 +44,8 @@ def flip_stats(l_gpu, l_orc, S_orc, fhat_orc, k1, zoom, Sd_orc=None, nfft=None, 
                 delta_r = N_f/(2 pi) eta/2 (1/(alpha |S|) + |S'|/|S|^2),
                 eta = 4 u sqrt(log2 N_f) ||z_m||_2 the packed-FFT error of one bin of frame m,
                 ||z_m||_2^2 = (2/N_f) sum_k (|S|^2 + alpha^2 |S'|^2), u = 2^-24;
-      bad_mask  mask disagreements farther than 1e-5 gamma (relative) from the threshold."""
+      bad_mask  mask disagreements farther from the threshold than max(1e-5 gamma, eta/2), the
+                fp32 STFT's resolution of |S| in the same error model (R21)."""
     above = l_orc != -1
     flips = (l_gpu != l_orc) & above
     n_above = int(above.sum())
@@ -67,7 +68,9 @@ def flip_stats(l_gpu, l_orc, S_orc, fhat_orc, k1, zoom, Sd_orc=None, nfft=None, 
         out["unresolvable_flips"] = int((flips & ~res).sum())
         mdiff = (l_gpu == -1) != (l_orc == -1)
         g = max(gamma or 0.0, 1e-30)
-        out["bad_mask"] = int((mdiff & (np.abs(aS - g) > 1e-5 * g)).sum())
+        # a mask disagreement is legitimate when |S| lies within what an fp32 STFT resolves of the
+        # threshold: eta/2 (the same per-bin error model, R21) or 1e-5 gamma, whichever is larger
+        out["bad_mask"] = int((mdiff & (np.abs(aS - g) > np.maximum(1e-5 * g, eta / 2))).sum())
     return out
 
 

@@ -200,3 +200,63 @@ def test_mp_relative_gamma_and_absmax(P):
     assert not (mdiff & (np.abs(aS - gamma) > eta / 2 + 2e-5 * gamma)).any()
     e = rel(T, To)
     assert e <= 1e-3 or st["frac"] <= 1e-5, (e, st)
+
+
+# edge shapes of the multi-pass path: a full-length window (L = N_f, even, c = N_f/2) on a record of
+# exactly N_f samples; a short window (L = N_f/8: mostly zero gather) with a non-power-of-two z and a
+# band not starting at DC; two frames; a single frame with the window centre at tap 0.  (A 101-tap
+# window zero-padded 160x gives 1.4e-4 flips at z = 7 -- r is ill-conditioned there, the regime the
+# extreme cases of test_gpu_parity.py document -- so it is not used as a parity case.)
+EDGE = [
+    ("nf16k_fullwin", 16384, 16384.0, 16384, 2048.0, 4096, 16384, 0.0, 8192.0, 1),
+    ("nf16k_shortwin_z7", 50000, 16384.0, 2001, 250.0, 37, 16384, 2000.0, 2500.0, 7),
+    ("nf32k_two_frames", 32768, 32768.0, 32768, 4096.0, 16384, 32768, 1000.0, 5000.0, 2),
+    ("nf32k_one_frame_c0", 32768, 32768.0, 32768, 8192.0, 32768, 32768, 1000.0, 5000.0, 2, 0),
+]
+
+
+def _sig_sweep(N, fs, seed):
+    """Three crossing-free linear chirps plus noise: every ridge moves from frame to frame, unlike
+    a stationary tone, whose ridge coefficient sits at the same distance from a rounding boundary in
+    every frame (one unlucky tone then flips a large coefficient in all frames at once)."""
+    rng = np.random.default_rng(seed)
+    t = np.arange(N) / fs
+    x = np.zeros(N)
+    for lo, hi in ((0.05, 0.09), (0.12, 0.16), (0.25, 0.40)):
+        f0, f1 = lo * fs, hi * fs
+        x += rng.uniform(0.5, 1.0) * np.cos(2 * np.pi * (f0 * t + 0.5 * (f1 - f0) * t * t / t[-1]) + rng.uniform(0, 6.28))
+    x += 0.05 * rng.standard_normal(N)
+    return x.astype(np.float32)
+
+
+@pytest.mark.parametrize("spec", EDGE, ids=[s[0] for s in EDGE])
+def test_mp_edge_shapes(P, spec):
+    name, N, fs, L, sigma, hop, nfft, f1, f2, z = spec[:10]
+    center = spec[10] if len(spec) > 10 else None
+    x = _sig_sweep(N, fs, N + L)
+    g, gd, c = O.gaussian_window(L, sigma, center)
+    So = O.stft(x.astype(np.float64), g, c, hop, nfft)
+    Sdo = O.stft(x.astype(np.float64), gd, c, hop, nfft)
+    gamma = 1e-6 * float(np.abs(So).max())
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=gamma, device=0, center=c)
+    xd = torch.from_numpy(x).to(DEV)
+    S, Sd = plan.stft(xd)
+    assert rel(S.cpu().numpy(), So) <= 1e-5 and rel(Sd.cpu().numpy(), Sdo) <= 1e-5
+    T = plan.forward(xd).cpu().numpy()
+    lg = plan.targets(xd).cpu().numpy()
+    To, S2, Sd2, lo = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, gamma, debug=True)
+    _, _, fhat = O.if_estimate(S2, Sd2, nfft, gamma)
+    st = flip_stats(lg, lo, S2, fhat, plan.layout["k1"], z, Sd2, nfft, plan.layout["alpha"], gamma)
+    assert st["frac"] <= 1e-4 and st["far"] <= 1e-4 and st["bad_mask"] == 0, st
+    e = rel(T, To)
+    # when a ridge's true IF crosses a fine-bin boundary, its whole bell of large coefficients sits on
+    # that boundary at once (L << N_f oversamples the bell), so the legitimate boundary flips of one
+    # frame can move most of its energy by one bin: then every large flip must be a boundary flip and
+    # the frames without flips must meet the plane tolerance
+    ff = ((lg != lo) & (lo != -1)).any(axis=1)
+    e_clean = rel(T[~ff], To[~ff])
+    assert e <= 1e-3 or (st["far_big"] <= 1e-4 and e_clean <= 1e-3), (e, e_clean, st)
+    y = plan.inverse(plan.forward(xd)).cpu().numpy()
+    yo = O.sst_inverse(To, g, c, hop, nfft, z, plan.layout["k1"], N)
+    print(name, "T", e, "frames without flips", e_clean, "inverse", rel(y, yo), st)
+    assert rel(y, yo) <= 1e-4, rel(y, yo)
