@@ -78,6 +78,21 @@ class RoundTrip:
         return y_host
 
 
+    def capture(self, x_host: torch.Tensor, y_host: torch.Tensor, T: torch.Tensor) -> "torch.cuda.CUDAGraph":
+        """Record one run() (copies, kernels, cross-stream events) as a CUDA graph bound to these
+        buffers; ``graph.replay()`` then repeats the whole host-to-host round trip with one launch
+        and no per-chunk host work, so many small chunks cost no Python overhead."""
+        comp = torch.cuda.current_stream(self.plan.device)
+        side = torch.cuda.Stream(self.plan.device)
+        side.wait_stream(comp)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                self.run(x_host, y_host, T)
+        comp.wait_stream(side)
+        return g
+
+
 def roundtrip(plan, x_host: torch.Tensor, y_host: torch.Tensor, T: torch.Tensor, chunks: int = 8):
     """One host->host forward + inverse with overlapped transfers (see module doc)."""
     return RoundTrip(plan, chunks).run(x_host, y_host, T)

@@ -465,3 +465,13 @@ def test_pipelined_host_roundtrip(P, chunks):
         torch.cuda.synchronize()
         assert torch.equal(T, T_ref)
         assert rel(yh.numpy(), y_ref) <= 1e-6
+    y_run = yh.clone()
+    # the same round trip captured once as a CUDA graph and replayed: identical results
+    graph = rt.capture(xh, yh, T)
+    for _ in range(2):
+        yh.zero_()
+        T.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(T, T_ref)
+        assert torch.equal(yh, y_run)
