@@ -21,7 +21,8 @@ for r in rows[hi + 1:]:
     seq.append((r[ki], v * scale))
 bench = json.load(open(sys.argv[2])) if len(sys.argv) > 2 else None
 # the step ends at the last whole-record inverse (plus its seam launch)
-last_whole = max(i for i, (k, ms) in enumerate(seq) if "inv_kernel" in k and ms > 1.0)
+inv_max = max(ms for k, ms in seq if "inv_kernel" in k)
+last_whole = max(i for i, (k, ms) in enumerate(seq) if "inv_kernel" in k and ms > 0.5 * inv_max)
 step, e2e = seq[:last_whole + 2], seq[last_whole + 2:]
 
 
