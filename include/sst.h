@@ -123,7 +123,11 @@ int32_t sst_abi_version(void);
 
 /* Create a plan on CUDA device `device`: validates p, snaps the band (R9), uploads window taps
  * (g, alpha*g'), twiddle tables and inverse normalisation tables (1/(C d[n]), R2/R15), sizes
- * the launch.  *out receives the plan (NULL on failure).  Synchronous, host-blocking.       */
+ * the launch.  *out receives the plan (NULL on failure).  Synchronous, host-blocking.
+ * N_f > 8192 (multi-pass path): the plan also owns two FFT scratch buffers of
+ * min(F, 2^27 / (8 N_f)) frames (at least z N_f complex per frame pair) -- at most ~2 x 128 MiB
+ * -- and 2 L floats per buffered frame pair; calls on such a plan are ordered on the stream they
+ * are given, and, like every plan, it is not thread-safe (one stream at a time).             */
 sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out);
 sst_status sst_plan_layout(const sst_plan* plan, sst_layout* out);
 /* Set the absolute threshold gamma (>= 0) used by later sst_forward / sst_targets calls.     */
