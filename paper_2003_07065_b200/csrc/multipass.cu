@@ -16,7 +16,9 @@
 // inverse's split of the z N_f IDFT) is gathered from T in pass 1, transformed by
 // passes 1-2 (conjugate twiddles), combined over b with e^{i 2 pi b tau/(z N)}, windowed by
 // g[tau + c]/N_f (a9), and overlap-added by a gather kernel (one thread per output sample,
-// frames in ascending order: no atomics, deterministic) (a10, Eq. 26).
+// frames in ascending order: no atomics, deterministic) (a10, Eq. 26).  For narrow bands with a
+// large z (B L small against z N_f log N_f, e.g. the §5.2 Fig. 16(e) shape, z = 20) the plan
+// picks a direct band sum per frame instead (mp_direct_kernel), with the same windowing and OLA.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -288,6 +290,64 @@ __global__ void __launch_bounds__(256) mp_combine_kernel(const MpInvArgs a, cons
     if (fA + 1 < a.frame_end - a.frame_begin) a.wf[(fA + 1) * a.L + j] = w * v.y;
 }
 
+// a9 as a direct band sum (narrow bands, large z): per frame and tau,
+//   r~[tau] = (2/N_f) Re sum_l w_l T[l] e(j_l tau),  j_l = z k1 + l,  e(x) = exp(2 pi i x/(z N_f)),
+// which is the z N_f-point IDFT of the conjugate-mirrored band (Eq. 25, R14: w = 1/2 with
+// the imaginary part dropped at j = 0 and j = z N_f/2), windowed by g[tau + c].  Blocked Horner in
+// w = e(tau) over 32 bins, blocks joined by phasors e(32 lb tau) whose arguments are reduced
+// exactly in integers (no accumulated phase error beyond one 32-term block).
+__global__ void __launch_bounds__(256) mp_direct_kernel(const MpInvArgs a) {
+    extern __shared__ __align__(16) float2 trow[];                     // [B]
+    const int64_t f = blockIdx.x;
+    const int B = a.bins;
+    const int64_t zN = (int64_t)a.zoom * a.nfft;
+    const int64_t j0 = (int64_t)a.zoom * a.k1;
+    for (int l = threadIdx.x; l < B; l += 256) {
+        float2 t = a.T[f * a.ldT + l];
+        if (j0 + l == 0 || 2 * (j0 + l) == zN) t = make_float2(0.5f * t.x, 0.0f);
+        trow[l] = t;
+    }
+    __syncthreads();
+    const int jj = blockIdx.y * 256 + threadIdx.x;                    // tau + c
+    if (jj >= a.L) return;
+    const int64_t tau = jj - a.c;
+    const float izN = 1.0f / (float)zN;
+    auto e_of = [&](int64_t r) {                                        // e(r), 0 <= r < z N (exact in fp32)
+        float sn, cs;
+        sincospif(2.0f * (float)r * izN, &sn, &cs);
+        return make_float2(cs, sn);
+    };
+    auto red = [&](int64_t x) { int64_t r = x % zN; return r < 0 ? r + zN : r; };
+    const float2 w = e_of(red(tau));
+    const int64_t step = red(32 * tau);
+    int64_t rb = 0;                                                     // 32 lb tau mod z N
+    float2 acc = make_float2(0.0f, 0.0f);
+    for (int l0 = 0; l0 < B; l0 += 32) {
+        const int n = min(32, B - l0);
+        float2 h = trow[l0 + n - 1];
+        if (n == 32) {
+#pragma unroll
+            for (int ll = 30; ll >= 0; --ll) {
+                const float2 t = trow[l0 + ll];
+                h = make_float2(fmaf(h.x, w.x, fmaf(-h.y, w.y, t.x)), fmaf(h.x, w.y, fmaf(h.y, w.x, t.y)));
+            }
+        } else {
+            for (int ll = n - 2; ll >= 0; --ll) {
+                const float2 t = trow[l0 + ll];
+                h = make_float2(fmaf(h.x, w.x, fmaf(-h.y, w.y, t.x)), fmaf(h.x, w.y, fmaf(h.y, w.x, t.y)));
+            }
+        }
+        const float2 ph = e_of(rb);
+        acc.x = fmaf(h.x, ph.x, fmaf(-h.y, ph.y, acc.x));
+        acc.y = fmaf(h.x, ph.y, fmaf(h.y, ph.x, acc.y));
+        rb += step;
+        rb -= (rb >= zN) ? zN : 0;
+    }
+    const float2 base = e_of(red(j0 * tau));
+    const float re = acc.x * base.x - acc.y * base.y;
+    a.wf[f * a.L + jj] = 2.0f * __ldg(&a.taps[jj].x) * a.inv_n * re;
+}
+
 // a10: y[s] += sum over the chunk's frames m covering s of wf[m][s - m H + c] (ascending m)
 __global__ void __launch_bounds__(256) mp_ola_kernel(const MpInvArgs a, int64_t lo, int64_t hi) {
     const int64_t s = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -358,6 +418,11 @@ cudaError_t launch_mp_forward(const FwdArgs& f, int mode, const float2* twN, flo
 cudaError_t launch_mp_inverse_accumulate(const MpInvArgs& a, cudaStream_t s) {
     const int64_t nfr = a.frame_end - a.frame_begin;
     if (nfr <= 0) return cudaSuccess;
+    cudaError_t e;
+    if (a.direct) {
+        mp_direct_kernel<<<dim3((unsigned)nfr, (unsigned)((a.L + 255) / 256)), 256, (size_t)a.bins * 8, s>>>(a);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    } else {
     const int64_t pairs = (nfr + 1) / 2;
     MpPass p{};
     p.count = pairs * a.zoom;
@@ -371,13 +436,14 @@ cudaError_t launch_mp_inverse_accumulate(const MpInvArgs& a, cudaStream_t s) {
     p.k1 = a.k1;
     p.bins = a.bins;
     p.out = a.buf0;
-    cudaError_t e = run_pass<kLoadInv, +1>(p, 1, s);
+    e = run_pass<kLoadInv, +1>(p, 1, s);
     if (e != cudaSuccess) return e;
     p.in = a.buf0;
     p.out = a.buf1;
     if ((e = run_pass<kLoadBuf, +1>(p, 2, s)) != cudaSuccess) return e;
     mp_combine_kernel<<<dim3((unsigned)pairs, (unsigned)((a.L + 255) / 256)), 256, 0, s>>>(a, a.buf1);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     const int64_t lo = a.frame_begin * a.hop - a.c > 0 ? a.frame_begin * a.hop - a.c : 0;
     int64_t hi = (a.frame_end - 1) * a.hop - a.c + a.L;
     if (hi > a.n) hi = a.n;

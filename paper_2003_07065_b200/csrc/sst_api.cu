@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -330,6 +331,14 @@ cudaError_t mp_inverse_accumulate(const sst_plan* pl, const float2* T, int64_t l
     a.y = y;
     a.y_off = y_off;
     a.y_len = y_len;
+    // direct band sum when its cost B L (complex FMAs per frame) is below the FFT path's, measured
+    // on B200 at ~4.3 z N_f log2 N_f in the same units; SST_MP_INVERSE=fft|direct overrides (tests)
+    const double lg = std::log2((double)pl->lay.nfft);
+    a.direct = ((double)bins * pl->lay.win_len < 4.3 * zoom * (double)pl->lay.nfft * lg && bins <= 6144) ? 1 : 0;
+    if (const char* ov = std::getenv("SST_MP_INVERSE")) {
+        if (!std::strcmp(ov, "fft")) a.direct = 0;
+        else if (!std::strcmp(ov, "direct") && bins <= 6144) a.direct = 1;
+    }
     const int64_t step = 2 * pl->mp_inv_pairs;        // buffers hold mp_inv_pairs x plan z >= zoom transforms
     for (int64_t c0 = fb; c0 < fe; c0 += step) {
         a.frame_begin = c0;

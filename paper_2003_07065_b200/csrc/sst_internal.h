@@ -117,6 +117,7 @@ struct MpInvArgs {
     float2* buf0; float2* buf1;       // [ceil(F/2) z][nfft] each
     float* wf;                        // [F][L] windowed frames
     float* y; int64_t y_off, y_len;   // y += (accumulate)
+    int direct;                       // 1: direct band sum per frame (mp_direct_kernel) instead of FFTs
 };
 
 void mp_factor(int nfft, int* r1, int* m);

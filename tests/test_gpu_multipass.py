@@ -260,3 +260,29 @@ def test_mp_edge_shapes(P, spec):
     yo = O.sst_inverse(To, g, c, hop, nfft, z, plan.layout["k1"], N)
     print(name, "T", e, "frames without flips", e_clean, "inverse", rel(y, yo), st)
     assert rel(y, yo) <= 1e-4, rel(y, yo)
+
+
+@pytest.mark.parametrize("path", ["fft", "direct"])
+@pytest.mark.parametrize("spec", [BIG[1], BIG[2]], ids=[BIG[1][0], BIG[2][0]])
+def test_mp_inverse_both_paths(P, spec, path, monkeypatch):
+    """Both inverse formulations of the multi-pass path (residue-split FFTs, direct band sum; the
+    plan picks one by cost) against the oracle on an output window in the middle of the record."""
+    monkeypatch.setenv("SST_MP_INVERSE", path)
+    name, N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c, gamma, plan = _setup(P, spec)
+    xd = torch.from_numpy(x).to(DEV)
+    n0 = N // 3
+    n1 = n0 + 2 * L
+    fb = max(0, (n0 + c - L) // hop)
+    fe = min(plan.frames, (n1 - 1 + c) // hop + 1)
+    T = plan.forward(xd, fb, fe)
+    lo = max(0, fb * hop - c)
+    hi = min(N, (fe - 1) * hop - c + L)
+    y = torch.zeros(hi - lo, dtype=torch.float32, device=DEV)
+    plan.inverse_accumulate(T, fb, fe, y, y_off=lo)
+    plan.inverse_finalize(y[n0 - lo:n1 - lo], y_off=n0)
+    To = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, gamma, frames=np.arange(fb, fe))
+    yo = O.sst_inverse(To, g, c, hop, nfft, z, plan.layout["k1"], N, frame_begin=fb, n0=n0, n1=n1)
+    e = rel(y[n0 - lo:n1 - lo].cpu().numpy(), yo)
+    print(name, path, e)
+    assert e <= 1e-4, e
