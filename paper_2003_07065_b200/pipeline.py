@@ -13,6 +13,8 @@ sample once all its frames are in gives the single-call result up to fp32 re-ass
 
 from __future__ import annotations
 
+import gc
+
 import torch
 
 
@@ -85,10 +87,22 @@ class RoundTrip:
         comp = torch.cuda.current_stream(self.plan.device)
         side = torch.cuda.Stream(self.plan.device)
         side.wait_stream(comp)
+        with torch.cuda.stream(side):                 # warm-up on the capture stream (torch's advice)
+            self.run(x_host, y_host, T)
+        side.synchronize()
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(side):
-            with torch.cuda.graph(g, stream=side):
-                self.run(x_host, y_host, T)
+        # no garbage collection inside the capture: a finaliser that frees device memory (a plan,
+        # a tensor of another stream) would invalidate it; torch.cuda.graph collects right before
+        gc_on = gc.isenabled()
+        gc.disable()
+        try:
+            with torch.cuda.stream(side):
+                # thread_local: only this thread's capture-unsafe calls invalidate the capture
+                with torch.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
+                    self.run(x_host, y_host, T)
+        finally:
+            if gc_on:
+                gc.enable()
         comp.wait_stream(side)
         return g
 

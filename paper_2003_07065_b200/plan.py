@@ -69,6 +69,21 @@ def _stream(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+_DEFERRED: list = []        # plan handles whose destruction was requested during a graph capture
+
+
+def _capturing() -> bool:
+    try:
+        return torch.cuda.is_available() and torch.cuda.is_current_stream_capturing()
+    except Exception:
+        return False
+
+
+def _flush_deferred():
+    while _DEFERRED and not _capturing():
+        L.sst_plan_destroy(_DEFERRED.pop())
+
+
 class Plan:
     """sst_plan wrapper.  Parameters follow sst_params (include/sst.h); sigma in samples."""
 
@@ -81,6 +96,7 @@ class Plan:
         self.device = dev
         p, keep = make_params(n, fs, win_len, sigma, hop, nfft, f1, f2, zoom, gamma, flags, g, gd, center)
         self._keep = keep
+        _flush_deferred()
         h = ctypes.c_void_p()
         L.check(L.sst_plan_create(ctypes.byref(p), dev.index, ctypes.byref(h)))
         self._h = h
@@ -248,9 +264,16 @@ class Plan:
 
     # ------------------------------------------------------------------ lifetime
     def close(self):
-        if getattr(self, "_h", None):
-            L.sst_plan_destroy(self._h)
+        h = getattr(self, "_h", None)
+        if h:
             self._h = None
+            if _capturing():
+                # sst_plan_destroy frees device memory, which would invalidate a CUDA graph being
+                # captured (e.g. a finaliser run by the garbage collector mid-capture): defer it
+                _DEFERRED.append(h)
+            else:
+                L.sst_plan_destroy(h)
+        _flush_deferred()
 
     def __del__(self):
         try:
