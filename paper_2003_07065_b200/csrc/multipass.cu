@@ -6,7 +6,7 @@
 //   N_f = R1 M.  Pass 1: for every column a in [0, M) a P = R1-point DFT of x[a + M i], times
 //   W_N^{a k1}, stored at [k1][a].  Pass 2: for every row k1 a P = M-point DFT over a, stored at
 //   k1 + R1 k2 (natural order).  Each CTA owns 16 adjacent columns / rows, so every global load
-//   and store moves 128-byte segments, and runs a radix-2 Stockham (autosort) FFT over them in
+//   and store moves 128-byte segments, and runs a radix-4 Stockham (autosort) FFT over them in
 //   shared memory with twiddles rounded once from fp64 (the plan's W_N table).
 // Forward: pass 1 gathers and packs the frame on the fly (a1: z[n] = u (g + i alpha g'), circular
 // placement, as in the fused kernel), pass 2 writes the spectrum, and one CTA per frame then does
@@ -117,20 +117,40 @@ __global__ void __launch_bounds__(kPassThreads) mp_pass_kernel(const MpPass a) {
         }
     }
     __syncthreads();
-    // radix-2 Stockham: y[q + s(2p)] = u + v, y[q + s(2p+1)] = (u - v) W_n^p, n = P/s
+    // Stockham (autosort) FFT over the 16 columns: radix-4 stages, then one radix-2 stage when
+    // log2 P is odd.  Radix 4 at length n = P/s: for p < m = n/4, q < s, with A..D = x[q + s(p + j m)],
+    //   y[q + s(4p + k)] = X_k W_n^{p k},  X = the 4-point DFT of (A, B, C, D)
     float2* x = s0;
     float2* y = s1;
     const int tstep = a.N / P;
+    int s = 1, ls = 0;
 #pragma unroll 1
-    for (int s = 1, ls = 0; s < P; s <<= 1, ++ls) {
-        const int m = P / (2 * s);
-        for (int bf = tid; bf < kTile * P / 2; bf += kPassThreads) {
+    for (; 4 * s <= P; s <<= 2, ls += 2) {
+        const int m = P / (4 * s);
+        for (int bf = tid; bf < kTile * P / 4; bf += kPassThreads) {
             const int al = bf & 15, rest = bf >> 4;
             const int q = rest & (s - 1), p = rest >> ls;
-            const float2 u = x[(q + s * p) * kTS + al], v = x[(q + s * (p + m)) * kTS + al];
-            const float2 w = tw_at<DIR>(a.twN, (int64_t)p * s * tstep);
-            y[(q + 2 * s * p) * kTS + al] = make_float2(u.x + v.x, u.y + v.y);
-            y[(q + 2 * s * p + s) * kTS + al] = c_mul(make_float2(u.x - v.x, u.y - v.y), w);
+            const int i0 = (q + s * p) * kTS + al, im = s * m * kTS;
+            const float2 A = x[i0], B = x[i0 + im], C = x[i0 + 2 * im], D = x[i0 + 3 * im];
+            const float2 apc = make_float2(A.x + C.x, A.y + C.y), amc = make_float2(A.x - C.x, A.y - C.y);
+            const float2 bpd = make_float2(B.x + D.x, B.y + D.y), bmd = make_float2(B.x - D.x, B.y - D.y);
+            const float2 jb = DIR < 0 ? make_float2(bmd.y, -bmd.x) : make_float2(-bmd.y, bmd.x);   // -+i (B - D)
+            const int64_t e = (int64_t)p * s * tstep;                       // W_n^p = W_N^{p s N/P}
+            const int o0 = (q + 4 * s * p) * kTS + al, os = s * kTS;
+            y[o0] = make_float2(apc.x + bpd.x, apc.y + bpd.y);
+            y[o0 + os] = c_mul(make_float2(amc.x + jb.x, amc.y + jb.y), tw_at<DIR>(a.twN, e));
+            y[o0 + 2 * os] = c_mul(make_float2(apc.x - bpd.x, apc.y - bpd.y), tw_at<DIR>(a.twN, 2 * e));
+            y[o0 + 3 * os] = c_mul(make_float2(amc.x - jb.x, amc.y - jb.y), tw_at<DIR>(a.twN, 3 * e));
+        }
+        __syncthreads();
+        float2* tmp = x; x = y; y = tmp;
+    }
+    if (s < P) {                                                        // last radix-2 stage (n = 2)
+        for (int bf = tid; bf < kTile * P / 2; bf += kPassThreads) {
+            const int al = bf & 15, q = bf >> 4;
+            const float2 u = x[q * kTS + al], v = x[(q + s) * kTS + al];
+            y[q * kTS + al] = make_float2(u.x + v.x, u.y + v.y);
+            y[(q + s) * kTS + al] = make_float2(u.x - v.x, u.y - v.y);
         }
         __syncthreads();
         float2* tmp = x; x = y; y = tmp;
