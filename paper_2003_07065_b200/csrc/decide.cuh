@@ -1,6 +1,14 @@
 // Per-bin decision shared by the fused forward (sst_kernels.cu) and the multi-pass large-N_f
 // forward (multipass.cu): unpack (a3), mask (Eq. 13), reassignment frequency (Eq. 36) and target
-// bin (Eq. 28, R10, R17), so both paths take every integer decision with the same fp32 arithmetic.
+// bin (Eq. 28, R10, R17), so both paths take every integer decision with the same arithmetic.
+//
+// Reading R23: the fp32 decision is final only where the fp32 packed FFT provably
+// cannot have moved it.  Each decision carries an error margin from the FFT's error model
+// (R21: one bin of the packed fp32 FFT of frame m is off by at most eta = 4 u sqrt(log2 N_f) ||z_m||,
+// calibrated on the configs at <= 0.95 of the model, taken 8 x here); a bin whose fp32 target lies
+// closer than that margin to a rounding boundary (Eq. 28) or whose |S| lies that close to gamma
+// (Eq. 13) is re-decided from S, S' recomputed in fp64 by the direct Eq. 8 sum --
+// warp-cooperative, rare (measured well under one bin per frame on C2-C5).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -10,9 +18,6 @@
 
 namespace sst {
 
-// Per source bin k with Za = Z[k], Zb = Z[N-k]: returns target l (>= 0), -1 masked, -2 out of band.
-// S = (P, Q)/2 with P = Re Za + Re Zb, Q = Im Za - Im Zb;  S' = (U, -V)/(2 alpha) with
-// U = Im Za + Im Zb, V = Re Za - Re Zb;  -Im(S'/S) = (V P + U Q) / (alpha (P^2 + Q^2)).
 // (hi 2^20 + lo) * s for the squeeze's limb sums: one fused rounding of the two converted limbs
 // (|hi| < 2^30, 0 <= lo < 2^31.01), i.e. within an fp32 ulp of the exact integer sum
 __device__ __forceinline__ float limbs_to_float(int hi, int lo, float s) {
@@ -25,23 +30,100 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return r;
 }
 
-// Branch-free (the 33 bins of a thread interleave): select chains instead of early returns.
-__device__ __forceinline__ int bin_target(const FwdArgs& a, float gam4, int k, float2 za, float2 zb, float2& PQ,
-                                          float2& UV, float& mag4) {
+// Per source bin k with Za = Z[k], Zb = Z[N-k]: returns target l (>= 0), -1 masked, -2 out of band.
+// S = (P, Q)/2 with P = Re Za + Re Zb, Q = Im Za - Im Zb;  S' = (U, -V)/(2 alpha) with
+// U = Im Za + Im Zb, V = Re Za - Re Zb;  -Im(S'/S) = (V P + U Q) / (alpha (P^2 + Q^2)).
+// Branch-free (the bins of a thread interleave): select chains instead of early returns.
+// cm, km: the frame's R23 margins (see fwd_margins); unsure = the fp32 result is not final.
+__device__ __forceinline__ int bin_target(const FwdArgs& a, float gam4, float cm, float km, int k, float2 za,
+                                          float2 zb, float2& PQ, float2& UV, float& mag4, bool& unsure) {
     PQ = __fadd2_rn(za, make_float2(zb.x, -zb.y));                           // (P, Q) = 2 S
     UV = __fadd2_rn(make_float2(za.y, za.x), make_float2(zb.y, -zb.x));      // (U, V) = 2 alpha (Re, -Im) S'
     const float2 sq = __fmul2_rn(PQ, PQ);
     mag4 = sq.x + sq.y;                                                      // 4 |S|^2
-    const bool keep = (mag4 > gam4) && k >= a.src_lo && k < a.src_hi;        // mask (Eq. 13)
+    const bool src = k >= a.src_lo && k < a.src_hi;
+    const bool keep = (mag4 > gam4) && src;                                  // mask (Eq. 13)
     const float2 vu = __fmul2_rn(make_float2(UV.y, UV.x), PQ);              // (V P, U Q)
     // z r: RF in fine bins (Eq. 36), r = -Im(S'/S) N_f/(2 pi) = (V P + U Q)/(P^2 + Q^2) * N_f/(2 pi alpha)
-    const float zr = (vu.x + vu.y) * rcp_approx(mag4) * a.zr_scale;
+    const float rsq = rcp_approx(mag4);
+    const float zr = (vu.x + vu.y) * rsq * a.zr_scale;
     const bool fin = fabsf(zr) <= 1073741824.0f;                             // non-finite or huge (R17)
     const bool pos = zr >= -(float)(a.zoom * k);                             // k + r >= 0
     const int base = pos ? a.zoom * (k - a.k1) : -a.zoom * (k + a.k1);      // |k + r| = -(k + r) otherwise
-    const int l = base + __float2int_rd(pos ? zr + 0.5f : 0.5f - zr);       // Eq. 28 (R10, R17)
+    const float t = pos ? zr + 0.5f : 0.5f - zr;                            // fine position - base
+    const float fl = floorf(t);
+    const int l = base + (int)fl;                                            // Eq. 28 (R10, R17)
     const int lin = ((unsigned)l < (unsigned)a.bins && fin) ? l : -2;
+    // R23 margin of the fine position: z delta r = cm (1/|2S| + (|U|+|V|)/|2S|^2) (R21 error model)
+    const float rs = rsqrtf(mag4);
+    const float mg = cm * fmaf(fabsf(UV.x) + fabsf(UV.y), rsq, rs);
+    const float fr = t - fl;
+    const float pf = (float)base + t;                                        // fine position + 1/2
+    const bool near_l = fminf(fr, 1.0f - fr) < mg && pf > -mg && pf < (float)a.bins + mg;
+    unsure = src && ((keep && near_l) || fabsf(mag4 - gam4) < km);
     return keep ? lin : -1;
+}
+
+// R23 margins of one frame from its packed-input norm ||z_m||_2 (nrm2 = ||z_m||^2):
+//   cm: margin factor of the fine position (cflag = 8 zr_scale 4 u sqrt(log2 N_f), set by the plan);
+//   km: margin of 4|S|^2 around 4 gamma^2 (|S| off by at most kd = 8 * 2 u sqrt(log2 N_f) ||z_m||).
+__device__ __forceinline__ void fwd_margins(const FwdArgs& a, float gam4, float nrm2, float& cm, float& km) {
+    const float nrm = sqrtf(nrm2);
+    cm = a.cflag * nrm;
+    const float kd = a.kflag * nrm;
+    km = 4.0f * kd * fmaf(2.0f, 0.5f * sqrtf(fmaxf(gam4, 0.0f)), kd);
+    if (!a.redecide) { cm = 0.0f; km = -1.0f; }
+}
+
+// fp64 S, S' of bin k of one frame by the direct Eq. 8 sum
+//   S[m,k] = sum_{j=0}^{L-1} x[m H - c + j] g[j] e^{-i 2 pi k (j - c)/N_f}   (and g' for S'),
+// warp-cooperative: all 32 lanes call it with the same k and frame; lane-strided taps, fixed
+// xor-tree reduction (deterministic).  xat(j) returns the frame's sample j as float (zero outside
+// the record).  taps64[j] = (g[j], g'[j]); tw64[e] = exp(-2 pi i e / N_f), both fp64.
+template <class XF>
+__device__ __forceinline__ void stft_bin_fp64(XF xat, const double2* __restrict__ taps64,
+                                              const double2* __restrict__ tw64, int nfft, int L, int c, int k,
+                                              double& sr, double& si, double& dr, double& di) {
+    const int lane = threadIdx.x & 31;
+    const unsigned msk = (unsigned)nfft - 1u;
+    sr = si = dr = di = 0.0;
+#pragma unroll 4
+    for (int j = lane; j < L; j += 32) {
+        const double xv = (double)xat(j);
+        const double2 w = __ldg(taps64 + j);
+        const double2 e = __ldg(tw64 + (((unsigned)k * (unsigned)(j - c)) & msk));
+        const double p = xv * w.x, q = xv * w.y;
+        sr = fma(p, e.x, sr);
+        si = fma(p, e.y, si);
+        dr = fma(q, e.x, dr);
+        di = fma(q, e.y, di);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sr += __shfl_xor_sync(0xffffffffu, sr, o);
+        si += __shfl_xor_sync(0xffffffffu, si, o);
+        dr += __shfl_xor_sync(0xffffffffu, dr, o);
+        di += __shfl_xor_sync(0xffffffffu, di, o);
+    }
+}
+
+// The oracle's decision (Eq. 13, 36, 28; R8, R10) in fp64 on the fp64 S, S'.
+__device__ __forceinline__ int decide_fp64(const FwdArgs& a, double gamma, int k, double sr, double si, double dr,
+                                           double di) {
+    if (!(k >= a.src_lo && k < a.src_hi)) return -1;
+    const double mag = sr * sr + si * si;
+    if (!(sqrt(mag) > gamma)) return -1;                                     // |S| > gamma (Eq. 13)
+    const double im = di * sr - dr * si;                                     // Im(S' conj S)
+    const double r = -im / mag * ((double)a.nfft / 6.283185307179586476925);   // Eq. 36
+    const double fh = fabs((double)k + r);                                   // Eq. 13 (R8)
+    const double p = (double)a.zoom * (fh - (double)a.k1) + 0.5;             // Eq. 28 (R10)
+    if (!(p >= 0.0 && p < (double)a.bins)) return -2;
+    return (int)floor(p);
+}
+
+// gamma of the launch in fp64 (absolute, or relative to the device max |S|)
+__device__ __forceinline__ double launch_gamma64(const FwdArgs& a) {
+    return a.absmax_dev ? a.gamma_rel_d * (double)__ldg(a.absmax_dev) : a.gamma_d;
 }
 
 }  // namespace sst

@@ -10,7 +10,19 @@
 
 namespace sst {
 
-__constant__ float2 c_w64[64];   // W_64^e = exp(-2 pi i e / 64), rounded from fp64 (set by upload_w64)
+// Uploaders of every translation unit's constant twiddle table (sst_api.cu calls them all once per
+// device).  The kernels are compiled as several separate CUDA modules (one per N2 and direction, for
+// a parallel build), each with its own copy of c_w64.
+void register_w64_uploader(cudaError_t (*fn)(const float2*));
+
+namespace {
+__constant__ float2 c_w64[64];   // W_64^e = exp(-2 pi i e / 64), rounded from fp64 (set at plan creation)
+cudaError_t upload_w64_this_tu(const float2* w) { return cudaMemcpyToSymbol(c_w64, w, sizeof(float2) * 64); }
+struct W64Registrar {
+    W64Registrar() { register_w64_uploader(&upload_w64_this_tu); }
+};
+const W64Registrar w64_registrar;
+}  // namespace
 
 // Complex arithmetic on sm_100a's packed FP32x2 pipe (FADD2 / FMUL2 / FFMA2): one instruction per
 // complex add, two per complex multiply; swaps and sign flips fold into operand modifiers.

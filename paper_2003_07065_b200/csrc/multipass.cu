@@ -203,7 +203,21 @@ __device__ __forceinline__ float block_max(float v, float* red) {
     return m;
 }
 
-// a3-a7 for one frame of the spectrum Z (natural order, N_f entries): one CTA per frame
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    float m = 0.0f;
+    for (int w = 0; w < kBinThreads / 32; ++w) m += red[w];
+    return m;
+}
+
+// a3-a7 for one frame of the spectrum Z (natural order, N_f entries): one CTA per frame.
+// Forward / targets: every bin is decided once (decide.cuh) into the frame's target row (a.lout in
+// targets mode, the plan's scratch otherwise); bins flagged by R23 are then re-decided in fp64 from
+// the direct Eq. 8 sum, one warp per bin, before the squeeze reads the row.
 template <int MODE>
 __global__ void __launch_bounds__(kBinThreads) mp_bins_kernel(const FwdArgs a, const float2* Zall, int ch) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -217,67 +231,112 @@ __global__ void __launch_bounds__(kBinThreads) mp_bins_kernel(const FwdArgs a, c
         const float gm = a.gamma_rel * __ldg(a.absmax_dev);
         gam4 = 4.0f * gm * gm;
     }
-    auto decide = [&](int k, float2& PQ, float2& UV, float& mag4) {
-        return bin_target(a, gam4, k, Z[k], Z[(N - k) & (N - 1)], PQ, UV, mag4);
+    // frame sample j = x[(frame_begin + fi) H - c + j], zero outside the record / slice
+    const int64_t s0 = (a.frame_begin + fi) * a.hop - a.c;
+    const int64_t v_lo = a.x_off > 0 ? a.x_off : 0;
+    const int64_t v_hi = a.n < a.x_off + a.x_len ? a.n : a.x_off + a.x_len;
+    auto xat = [&](int j) -> float {
+        const int64_t sj = s0 + j;
+        return (sj >= v_lo && sj < v_hi) ? __ldg(a.x + (sj - a.x_off)) : 0.0f;
     };
-    if constexpr (MODE == kModeStft || MODE == kModeTargets) {
+    if constexpr (MODE == kModeStft || MODE == kModeAbsmax) {
+        float vmax = 0.0f;
         for (int k = threadIdx.x; k < K; k += kBinThreads) {
             float2 PQ, UV;
             float mag4;
-            const int l = decide(k, PQ, UV, mag4);
+            bool unsure;
+            bin_target(a, gam4, 0.0f, -1.0f, k, Z[k], Z[(N - k) & (N - 1)], PQ, UV, mag4, unsure);
             if constexpr (MODE == kModeStft) {
                 a.S[fi * K + k] = make_float2(0.5f * PQ.x, 0.5f * PQ.y);
                 a.Sd[fi * K + k] = make_float2(UV.x * a.inv_alpha2, -UV.y * a.inv_alpha2);
             } else {
-                a.lout[fi * K + k] = l;
+                vmax = fmaxf(vmax, mag4);
             }
         }
-    } else if constexpr (MODE == kModeAbsmax) {
-        float vmax = 0.0f;
-        for (int k = threadIdx.x; k < K; k += kBinThreads) {
-            float2 PQ, UV;
-            float mag4;
-            decide(k, PQ, UV, mag4);
-            vmax = fmaxf(vmax, mag4);
+        if constexpr (MODE == kModeAbsmax) {
+            const float m = block_max(vmax, red);
+            if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned int*>(a.absmax_out), __float_as_uint(0.5f * sqrtf(m)));
         }
-        const float m = block_max(vmax, red);
-        if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned int*>(a.absmax_out), __float_as_uint(0.5f * sqrtf(m)));
+        return;
     } else {
-        // a6: exact fixed-point sums.  v_max < 2^ex bounds the kept |Re S|, |Im S| of the frame;
-        // each value is scaled by 2^(39 - ex) and rounded to an int64 (|X| < 2^39); at most
-        // N_f/2 + 1 <= 2^15 + 1 terms per target keep every sum below 2^55, so the integer sums
-        // are exact in any order and the band row is bitwise reproducible.
-        float vmax = 0.0f;
+        int32_t* lrow = (MODE == kModeTargets ? a.lout : a.lscratch) + fi * K;
+        // R23 margins from ||z_m||^2 = sum_j x_j^2 (g_j^2 + alpha^2 g'_j^2)
+        float e = 0.0f;
+        for (int j = threadIdx.x; j < a.L; j += kBinThreads) {
+            const float xv = xat(j);
+            const float2 w = __ldg(a.taps + j);
+            e = fmaf(xv * xv, fmaf(w.x, w.x, w.y * w.y), e);
+        }
+        const float nrm2 = block_sum(e, red);
+        float cm, km;
+        fwd_margins(a, gam4, nrm2, cm, km);
         for (int k = threadIdx.x; k < K; k += kBinThreads) {
             float2 PQ, UV;
             float mag4;
-            if (decide(k, PQ, UV, mag4) >= 0) vmax = fmaxf(vmax, 0.5f * fmaxf(fabsf(PQ.x), fabsf(PQ.y)));
+            bool unsure;
+            const int l = bin_target(a, gam4, cm, km, k, Z[k], Z[(N - k) & (N - 1)], PQ, UV, mag4, unsure);
+            lrow[k] = unsure ? -4 : l;                                 // -4: pending fp64 decision
         }
-        const float m = block_max(vmax, red);
-        const int ex = max(-87, (int)((__float_as_uint(m) >> 23) & 0xff) - 126);
-        const float scale = __uint_as_float((unsigned)(127 + 39 - ex) << 23);
-        const float iscale = __uint_as_float((unsigned)(127 - 39 + ex) << 23);
-        float2* trow = a.T + fi * a.ldT;
-        for (int l0 = 0; l0 < a.bins; l0 += ch) {
-            const int lc = min(ch, a.bins - l0);
-            for (int i = threadIdx.x; i < 2 * lc; i += kBinThreads) acc[i] = 0;
-            __syncthreads();
-            for (int k = threadIdx.x; k < K; k += kBinThreads) {
-                float2 PQ, UV;
-                float mag4;
-                const int lr = decide(k, PQ, UV, mag4) - l0;
-                if (lr >= 0 && lr < lc) {                                   // -1/-2 give lr < 0 for l0 = 0
-                    long long xr, xi;
-                    asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xr) : "f"(0.5f * PQ.x * scale));
-                    asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xi) : "f"(0.5f * PQ.y * scale));
-                    atomicAdd(reinterpret_cast<unsigned long long*>(acc + 2 * lr), (unsigned long long)xr);
-                    atomicAdd(reinterpret_cast<unsigned long long*>(acc + 2 * lr + 1), (unsigned long long)xi);
+        __syncthreads();
+        {
+            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            const double gam64 = launch_gamma64(a);
+            for (int b0 = warp * 32; b0 < K; b0 += kBinThreads) {
+                const int k0 = b0 + lane;
+                unsigned ball = __ballot_sync(0xffffffffu, k0 < K && lrow[k0] == -4);
+                while (ball) {
+                    const int k = b0 + __ffs(ball) - 1;
+                    ball &= ball - 1;
+                    double sr, si, dr, di;
+                    stft_bin_fp64(xat, a.taps64, a.tw64, N, a.L, a.c, k, sr, si, dr, di);
+                    const int ln = decide_fp64(a, gam64, k, sr, si, dr, di);
+                    __syncwarp();
+                    if (lane == 0) lrow[k] = ln;
                 }
             }
+        }
+        if constexpr (MODE == kModeForward) {
             __syncthreads();
-            for (int i = threadIdx.x; i < lc; i += kBinThreads)
-                trow[l0 + i] = make_float2(__ll2float_rn(acc[2 * i]) * iscale, __ll2float_rn(acc[2 * i + 1]) * iscale);
-            __syncthreads();
+            // a6: exact fixed-point sums.  v_max < 2^ex bounds the kept |Re S|, |Im S| of the frame;
+            // each value is scaled by 2^(39 - ex) and rounded to an int64 (|X| < 2^39); at most
+            // N_f/2 + 1 <= 2^15 + 1 terms per target keep every sum below 2^55, so the integer sums
+            // are exact in any order and the band row is bitwise reproducible.
+            auto S_of = [&](int k) {                                    // S = (Z[k] + conj Z[N-k]) / 2
+                const float2 za = Z[k], zb = Z[(N - k) & (N - 1)];
+                return make_float2(0.5f * (za.x + zb.x), 0.5f * (za.y - zb.y));
+            };
+            float vmax = 0.0f;
+            for (int k = threadIdx.x; k < K; k += kBinThreads) {
+                if (lrow[k] >= 0) {
+                    const float2 S = S_of(k);
+                    vmax = fmaxf(vmax, fmaxf(fabsf(S.x), fabsf(S.y)));
+                }
+            }
+            const float m = block_max(vmax, red);
+            const int ex = max(-87, (int)((__float_as_uint(m) >> 23) & 0xff) - 126);
+            const float scale = __uint_as_float((unsigned)(127 + 39 - ex) << 23);
+            const float iscale = __uint_as_float((unsigned)(127 - 39 + ex) << 23);
+            float2* trow = a.T + fi * a.ldT;
+            for (int l0 = 0; l0 < a.bins; l0 += ch) {
+                const int lc = min(ch, a.bins - l0);
+                for (int i = threadIdx.x; i < 2 * lc; i += kBinThreads) acc[i] = 0;
+                __syncthreads();
+                for (int k = threadIdx.x; k < K; k += kBinThreads) {
+                    const int lr = lrow[k] - l0;
+                    if (lr >= 0 && lr < lc) {                               // -1/-2 give lr < 0 for l0 = 0
+                        const float2 S = S_of(k);
+                        long long xr, xi;
+                        asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xr) : "f"(S.x * scale));
+                        asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xi) : "f"(S.y * scale));
+                        atomicAdd(reinterpret_cast<unsigned long long*>(acc + 2 * lr), (unsigned long long)xr);
+                        atomicAdd(reinterpret_cast<unsigned long long*>(acc + 2 * lr + 1), (unsigned long long)xi);
+                    }
+                }
+                __syncthreads();
+                for (int i = threadIdx.x; i < lc; i += kBinThreads)
+                    trow[l0 + i] = make_float2(__ll2float_rn(acc[2 * i]) * iscale, __ll2float_rn(acc[2 * i + 1]) * iscale);
+                __syncthreads();
+            }
         }
     }
 }

@@ -32,6 +32,9 @@ struct sst_plan {
     // device tables
     float2* d_taps = nullptr;       // [L]  (g, alpha g')
     float2* d_tw = nullptr;         // [N_f]
+    double2* d_taps64 = nullptr;    // [L]  (g, g') fp64 (R23 re-decision)
+    double2* d_tw64 = nullptr;      // [N_f] exp(-2 pi i e/N_f) fp64
+    int32_t* d_mpl = nullptr;       // multi-pass: [mp_fwd_frames][N_f/2 + 1] targets
     float2* d_phz = nullptr;        // [z][64 + 2 N_f/64]
     double* d_renyi = nullptr;      // [kRenyiBlocks][2] partial sums
     unsigned long long* d_amax2 = nullptr;   // ridge emission: max |T| (double bits)
@@ -51,6 +54,7 @@ struct sst_plan {
     int64_t mp_fwd_frames = 0, mp_inv_pairs = 0;
     int32_t n_head = 0, n_tail = 0;
     int fwd_grid = 0, inv_grid = 0;
+    bool redecide = true;           // R23 (SST_NO_REDECIDE=1 turns it off: timing experiments only)
     const float* ext_absmax = nullptr;
     double gamma_abs = 0;
     std::string err;
@@ -58,7 +62,7 @@ struct sst_plan {
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(device);
-        for (void* q : {(void*)d_taps, (void*)d_tw, (void*)d_phz, (void*)d_renyi, (void*)d_amax2, (void*)d_back, (void*)d_inv_head, (void*)d_inv_tail,
+        for (void* q : {(void*)d_taps, (void*)d_tw, (void*)d_taps64, (void*)d_tw64, (void*)d_mpl, (void*)d_phz, (void*)d_renyi, (void*)d_amax2, (void*)d_back, (void*)d_inv_head, (void*)d_inv_tail,
                         (void*)d_inv_per, (void*)d_absmax, (void*)d_seam, (void*)d_twN, (void*)d_mp0, (void*)d_mp1, (void*)d_wf})
             if (q) cudaFree(q);
         cudaSetDevice(prev);
@@ -202,6 +206,11 @@ sst_status validate(const sst_params* p, sst_layout* lay, std::string& msg) {
     return SST_OK;
 }
 
+std::vector<cudaError_t (*)(const float2*)>& w64_uploaders() {
+    static std::vector<cudaError_t (*)(const float2*)> v;   // filled at load time (fft.cuh registrars)
+    return v;
+}
+
 std::mutex g_w64_mu;
 uint64_t g_w64_uploaded = 0;   // bitmask of devices with c_w64 set
 
@@ -213,8 +222,10 @@ sst_status ensure_w64(int device, std::string& msg) {
         const double a = -2.0 * kPi * e / 64.0;
         w[e] = make_float2((float)std::cos(a), (float)std::sin(a));
     }
-    cudaError_t ce = sst::upload_w64(w);
-    if (ce != cudaSuccess) { msg = std::string("upload twiddles: ") + cudaGetErrorString(ce); return SST_E_CUDA; }
+    for (auto fn : w64_uploaders()) {
+        cudaError_t ce = fn(w);
+        if (ce != cudaSuccess) { msg = std::string("upload twiddles: ") + cudaGetErrorString(ce); return SST_E_CUDA; }
+    }
     if (device < 64) g_w64_uploaded |= 1ull << device;
     return SST_OK;
 }
@@ -279,6 +290,16 @@ sst::FwdArgs fwd_args(const sst_plan* pl, const float* x, int64_t x_off, int64_t
     a.zr_scale = (float)(pl->lay.zoom * pl->lay.nfft / (2.0 * kPi * pl->lay.alpha));
     a.r_scale_d = pl->lay.nfft / (2.0 * kPi * pl->lay.alpha);
     a.inv_alpha2 = (float)(1.0 / (2.0 * pl->lay.alpha));
+    // R23: margins of the fp32 decision, 8 x the R21 error model eta = 4 u sqrt(log2 N_f) ||z_m||
+    const double u = std::ldexp(1.0, -24), sl = std::sqrt(std::log2((double)pl->lay.nfft));
+    a.redecide = pl->redecide ? 1 : 0;
+    a.cflag = (float)(8.0 * (pl->lay.zoom * pl->lay.nfft / (2.0 * kPi * pl->lay.alpha)) * 4.0 * u * sl);
+    a.kflag = (float)(8.0 * 2.0 * u * sl);
+    a.gamma_d = pl->gamma_abs;
+    a.gamma_rel_d = pl->p.gamma;
+    a.taps64 = pl->d_taps64;
+    a.tw64 = pl->d_tw64;
+    a.lscratch = pl->d_mpl;
     a.lay = sst::fwd_layout(pl->lay.nfft / 64, pl->lay.win_len, pl->lay.hop);
     return a;
 }
@@ -351,6 +372,10 @@ cudaError_t mp_inverse_accumulate(const sst_plan* pl, const float2* T, int64_t l
 }
 
 }  // namespace
+
+namespace sst {
+void register_w64_uploader(cudaError_t (*fn)(const float2*)) { w64_uploaders().push_back(fn); }
+}  // namespace sst
 
 extern "C" {
 
@@ -474,7 +499,15 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
         for (int32_t j = i; j < L; j += H) d += pl->g[j] * pl->g[j];
         per[i] = (float)(1.0 / (pl->cst * d));
     }
+    std::vector<double2> taps64(L), tw64(Nf);
+    for (int32_t j = 0; j < L; ++j) taps64[j] = make_double2(pl->g[j], pl->gd[j]);
+    for (int32_t e = 0; e < Nf; ++e) {
+        const double a = -2.0 * kPi * (double)e / Nf;
+        tw64[e] = make_double2(std::cos(a), std::sin(a));
+    }
+    if (const char* nr = std::getenv("SST_NO_REDECIDE")) pl->redecide = !(nr[0] == '1');
     if ((s = upload(pl, &pl->d_taps, taps)) != SST_OK || (s = upload(pl, &pl->d_tw, tw)) != SST_OK ||
+        (s = upload(pl, &pl->d_taps64, taps64)) != SST_OK || (s = upload(pl, &pl->d_tw64, tw64)) != SST_OK ||
         (s = upload(pl, &pl->d_phz, phz)) != SST_OK || (s = upload(pl, &pl->d_inv_head, head)) != SST_OK ||
         (s = upload(pl, &pl->d_inv_tail, tail)) != SST_OK || (s = upload(pl, &pl->d_inv_per, per)) != SST_OK) {
         msg = pl->err;
@@ -499,7 +532,8 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
         const size_t elems = (size_t)std::max<int64_t>(pl->mp_fwd_frames, pl->mp_inv_pairs * z) * Nf;
         if (cudaMalloc((void**)&pl->d_mp0, elems * sizeof(float2)) != cudaSuccess ||
             cudaMalloc((void**)&pl->d_mp1, elems * sizeof(float2)) != cudaSuccess ||
-            cudaMalloc((void**)&pl->d_wf, sizeof(float) * (size_t)(2 * pl->mp_inv_pairs) * L) != cudaSuccess) {
+            cudaMalloc((void**)&pl->d_wf, sizeof(float) * (size_t)(2 * pl->mp_inv_pairs) * L) != cudaSuccess ||
+            cudaMalloc((void**)&pl->d_mpl, sizeof(int32_t) * (size_t)pl->mp_fwd_frames * (Nf / 2 + 1)) != cudaSuccess) {
             cudaGetLastError();
             delete pl;
             return fail(nullptr, SST_E_OUT_OF_MEMORY, "cudaMalloc multi-pass scratch");
@@ -557,6 +591,7 @@ static sst_status run_forward_mode(sst_plan* plan, int mode, const float* x, int
         } else {
             sst::FwdArgs m = a;
             m.absmax_out = plan->d_absmax;
+            m.redecide = 0;
             sst_status s = cuda_status(plan, cudaMemsetAsync(plan->d_absmax, 0, sizeof(float), st), "memset");
             if (s != SST_OK) return s;
             s = cuda_status(plan, launch_fwd_any(plan, m, sst::kModeAbsmax, st), "absmax launch");
@@ -597,6 +632,7 @@ sst_status sst_stft(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len
     a.S = reinterpret_cast<float2*>(S);
     a.Sd = reinterpret_cast<float2*>(Sd);
     a.gamma2x4 = -1.0f;   // report every bin
+    a.redecide = 0;
     a.src_lo = 0;
     a.src_hi = plan->lay.nfft / 2 + 1;
     return cuda_status(plan, launch_fwd_any(plan, a, sst::kModeStft, (cudaStream_t)stream),
@@ -632,6 +668,7 @@ sst_status sst_absmax(sst_plan* plan, const float* x, int64_t x_off, int64_t x_l
     sst::FwdArgs a = fwd_args(plan, x, x_off, x_len, fb, fe);
     a.absmax_out = out;
     a.gamma2x4 = -1.0f;
+    a.redecide = 0;
     return cuda_status(plan, launch_fwd_any(plan, a, sst::kModeAbsmax, st), "absmax launch");
 }
 

@@ -71,6 +71,15 @@ struct FwdArgs {
     float zr_scale;          // z N_f / (2 pi alpha)
     double r_scale_d;        // same, fp64 (near-boundary re-decision)
     float inv_alpha2;        // 1 / (2 alpha)
+    // R23 fp64 re-decision of bins the fp32 FFT cannot decide (decide.cuh)
+    int redecide;            // 1: on (forward / targets); 0: off (stft / absmax, or SST_NO_REDECIDE)
+    float cflag;             // 8 zr_scale 4 u sqrt(log2 N_f): margin of the fine position per unit ||z_m||
+    float kflag;             // 8 * 2 u sqrt(log2 N_f): margin of |S| per unit ||z_m||
+    double gamma_d;          // absolute gamma (fp64)
+    double gamma_rel_d;      // relative mode: gamma = gamma_rel_d * (*absmax_dev)
+    const double2* taps64;   // [L] (g, g') fp64
+    const double2* tw64;     // [nfft] exp(-2 pi i e / N_f) fp64
+    int32_t* lscratch;       // multi-pass: [frames][N_f/2 + 1] targets of the chunk
     FwdLayout lay;
     // outputs
     float2* T; int64_t ldT;
@@ -155,7 +164,5 @@ constexpr int kRenyiBlocks = 1184;
 cudaError_t launch_renyi(const float2* T, int64_t rows, int64_t cols, int64_t ldT, double alpha, double* partial,
                          double* out, cudaStream_t s);
 
-// constant-memory table W_64^e (forward), uploaded once per device by the API
-cudaError_t upload_w64(const float2* w64_host);
 
 }  // namespace sst

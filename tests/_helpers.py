@@ -33,49 +33,49 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-def flip_stats(l_gpu, l_orc, S_orc, fhat_orc, k1, zoom, Sd_orc=None, nfft=None, alpha=None, gamma=None):
-    """Target-index disagreement between the GPU and the oracle (BASELINE north_star), computed
-    from oracle quantities only (the oracle never sees GPU data):
-      frac      flipped / above-threshold coefficients;
-      far_big   largest rounding-boundary distance (coarse bins, oracle's fp64 position) of a flip
-                with |S| >= 1e-2 max (reported);
-      far       the same over flips of *resolvable* coefficients -- those whose reassignment
-                frequency an fp32 STFT fixes to better than 1e-5 fine bins (reading R21):
-                delta_r = N_f/(2 pi) eta/2 (1/(alpha |S|) + |S'|/|S|^2),
-                eta = 4 u sqrt(log2 N_f) ||z_m||_2 the packed-FFT error of one bin of frame m,
-                ||z_m||_2^2 = (2/N_f) sum_k (|S|^2 + alpha^2 |S'|^2), u = 2^-24;
-      bad_mask  mask disagreements farther from the threshold than max(1e-5 gamma, eta/2), the
-                fp32 STFT's resolution of |S| in the same error model (R21)."""
-    above = l_orc != -1
-    flips = (l_gpu != l_orc) & above
-    n_above = int(above.sum())
-    frac = flips.sum() / max(1, n_above)
+def flip_stats(l_gpu, l_orc, S_orc, fhat_orc, k1, zoom, gamma=0.0):
+    """Target disagreement between the GPU and the oracle (BASELINE north_star), computed from
+    oracle quantities only (the oracle never sees GPU data):
+      frac      (target flips + mask disagreements) / above-threshold coefficients (<= 1e-4);
+      far       largest distance (coarse bins) of a target flip's oracle fp64 position
+                z (fhat - k1) + 1/2 from the nearest rounding boundary (Eq. 28) -- the clause
+                "lying within 1e-4 bins of a rounding boundary", applied to every flip;
+      far_big   the same over flips with |S| >= 1e-2 max|S| (reported);
+      bad_mask  mask disagreements (Eq. 13) with ||S| - gamma| > 1e-5 gamma, i.e. not explained
+                by the rounding of the threshold itself (must be 0).
+    Reading R23: the GPU re-takes in fp64 every decision its fp32 FFT could have
+    moved, so the clause is asserted as stated, with no resolvability exemption."""
+    kept_o = l_orc != -1
+    kept_g = l_gpu != -1
+    mdiff = kept_o != kept_g
+    flips = kept_o & kept_g & (l_gpu != l_orc)
+    n_above = int(kept_o.sum())
+    frac = (int(flips.sum()) + int(mdiff.sum())) / max(1, n_above)
     amax = np.abs(S_orc).max()
-    pos = zoom * (fhat_orc - k1) + 0.5
     with np.errstate(invalid="ignore"):
+        pos = zoom * (fhat_orc - k1) + 0.5
         dist = np.abs(pos - np.round(pos)) / zoom
+    dist = np.where(np.isfinite(dist), dist, np.inf)
     big = flips & (np.abs(S_orc) >= 1e-2 * amax)
-    far_big = float(dist[big].max()) if big.any() else 0.0
-    out = {"flips": int(flips.sum()), "above": n_above, "frac": float(frac), "far_big": far_big}
-    if Sd_orc is not None:
-        aS = np.abs(S_orc)
-        zn2 = 2.0 / nfft * np.sum(aS ** 2 + alpha ** 2 * np.abs(Sd_orc) ** 2, axis=1, keepdims=True)
-        eta = 4.0 * 2.0 ** -24 * np.sqrt(np.log2(nfft)) * np.sqrt(zn2)
-        with np.errstate(divide="ignore", invalid="ignore"):
-            dr = nfft / (2 * np.pi) * eta / 2 * (1.0 / (alpha * aS) + np.abs(Sd_orc) / aS ** 2)
-        res = flips & (zoom * dr < 1e-5)
-        out["far"] = float(dist[res].max()) if res.any() else 0.0
-        out["unresolvable_flips"] = int((flips & ~res).sum())
-        mdiff = (l_gpu == -1) != (l_orc == -1)
-        g = max(gamma or 0.0, 1e-30)
-        # a mask disagreement is legitimate when |S| lies within what an fp32 STFT resolves of the
-        # threshold: eta/2 (the same per-bin error model, R21) or 1e-5 gamma, whichever is larger
-        out["bad_mask"] = int((mdiff & (np.abs(aS - g) > np.maximum(1e-5 * g, eta / 2))).sum())
-    return out
+    g = max(float(gamma or 0.0), 1e-300)
+    bad_mask = mdiff & (np.abs(np.abs(S_orc) - g) > 1e-5 * g)
+    return {"flips": int(flips.sum()), "mask_diff": int(mdiff.sum()), "above": n_above, "frac": float(frac),
+            "far": float(dist[flips].max()) if flips.any() else 0.0,
+            "far_big": float(dist[big].max()) if big.any() else 0.0,
+            "bad_mask": int(bad_mask.sum())}
+
+
+def assert_flips(st, ctx=None):
+    """The north star's disagreement clause, unconditionally: <= 1e-4 of above-threshold
+    coefficients disagree, every target flip lies within 1e-4 coarse bins of a rounding boundary,
+    and no mask disagreement is farther from gamma than its own rounding (1e-5 gamma)."""
+    assert st["frac"] <= 1e-4, (ctx, st)
+    assert st["far"] <= 1e-4, (ctx, st)
+    assert st["bad_mask"] == 0, (ctx, st)
 
 
 def signal(cfg_name, start=0, stop=None):
     return generate(cfg_name, start, stop)
 
 
-__all__ = ["oracle_window", "config_gamma", "make_plan", "rel", "flip_stats", "signal", "get_config"]
+__all__ = ["oracle_window", "config_gamma", "make_plan", "rel", "flip_stats", "assert_flips", "signal", "get_config"]

@@ -16,7 +16,7 @@ pytestmark = [pytest.mark.gpu,
 
 import oracle as O  # noqa: E402
 from gen.signals import s52_milling  # noqa: E402
-from tests._helpers import flip_stats, rel  # noqa: E402
+from tests._helpers import assert_flips, flip_stats, rel  # noqa: E402
 
 DEV = torch.device("cuda:0")
 
@@ -92,12 +92,11 @@ def test_mp_forward_parity_and_flips(P, spec):
         To, S, Sd, lo = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, gamma,
                                       frames=fr, debug=True)
         _, _, fhat = O.if_estimate(S, Sd, nfft, gamma)
-        st = flip_stats(lg, lo, S, fhat, plan.layout["k1"], z, Sd, nfft, plan.layout["alpha"], gamma)
-        assert st["frac"] <= 1e-4, (fb, st)
-        assert st["far"] <= 1e-4 and st["bad_mask"] == 0, (fb, st)
+        st = flip_stats(lg, lo, S, fhat, plan.layout["k1"], z, gamma)
+        assert_flips(st, fb)
         e = rel(Tall[fb:fe], To)
         print(name, "forward", fb, e, st)
-        assert e <= 1e-3 or st["frac"] <= 1e-5, (fb, e, st)
+        assert e <= 1e-3, (fb, e, st)
 
 
 @pytest.mark.parametrize("spec", [BIG[0], BIG[2]], ids=[BIG[0][0], BIG[2][0]])
@@ -187,29 +186,21 @@ def test_mp_relative_gamma_and_absmax(P):
     gamma = 1e-3 * ref
     To, S, Sd, lo = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, gamma, debug=True)
     _, _, fhat = O.if_estimate(S, Sd, nfft, gamma)
-    st = flip_stats(lg, lo, S, fhat, plan.layout["k1"], z, Sd, nfft, plan.layout["alpha"], gamma)
-    assert st["frac"] <= 1e-4 and st["far"] <= 1e-4, st
-    # mask disagreements must sit within what separates the two sides from the threshold: the fp32
-    # STFT's error in |S| (the R21 error model, eta/2 per bin of frame m) plus the fp32 rounding of
-    # the GPU's max|S| (<= 1e-5 relative)
-    aS = np.abs(S)
-    zn2 = 2.0 / nfft * np.sum(aS ** 2 + plan.layout["alpha"] ** 2 * np.abs(Sd) ** 2, axis=1, keepdims=True)
-    eta = 4.0 * 2.0 ** -24 * np.sqrt(np.log2(nfft)) * np.sqrt(zn2)
-    mdiff = (lg == -1) != (lo == -1)
-    assert mdiff.sum() <= 1e-4 * mdiff.size
-    assert not (mdiff & (np.abs(aS - gamma) > eta / 2 + 2e-5 * gamma)).any()
+    st = flip_stats(lg, lo, S, fhat, plan.layout["k1"], z, gamma)
+    assert_flips(st)
     e = rel(T, To)
-    assert e <= 1e-3 or st["frac"] <= 1e-5, (e, st)
+    assert e <= 1e-3, (e, st)
 
 
 # edge shapes of the multi-pass path: a full-length window (L = N_f, even, c = N_f/2) on a record of
 # exactly N_f samples; a short window (L = N_f/8: mostly zero gather) with a non-power-of-two z and a
-# band not starting at DC; two frames; a single frame with the window centre at tap 0.  (A 101-tap
-# window zero-padded 160x gives 1.4e-4 flips at z = 7 -- r is ill-conditioned there, the regime the
-# extreme cases of test_gpu_parity.py document -- so it is not used as a parity case.)
+# band not starting at DC; a 101-tap window zero-padded 160x at z = 7 (r ill-conditioned: the fp32
+# decisions there are the ones R23 re-takes in fp64); two frames; a single frame with the window
+# centre at tap 0.
 EDGE = [
     ("nf16k_fullwin", 16384, 16384.0, 16384, 2048.0, 4096, 16384, 0.0, 8192.0, 1),
     ("nf16k_shortwin_z7", 50000, 16384.0, 2001, 250.0, 37, 16384, 2000.0, 2500.0, 7),
+    ("nf16k_101tap_z7", 50000, 16384.0, 101, 12.5, 37, 16384, 2000.0, 2500.0, 7),
     ("nf32k_two_frames", 32768, 32768.0, 32768, 4096.0, 16384, 32768, 1000.0, 5000.0, 2),
     ("nf32k_one_frame_c0", 32768, 32768.0, 32768, 8192.0, 32768, 32768, 1000.0, 5000.0, 2, 0),
 ]
@@ -246,19 +237,13 @@ def test_mp_edge_shapes(P, spec):
     lg = plan.targets(xd).cpu().numpy()
     To, S2, Sd2, lo = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, gamma, debug=True)
     _, _, fhat = O.if_estimate(S2, Sd2, nfft, gamma)
-    st = flip_stats(lg, lo, S2, fhat, plan.layout["k1"], z, Sd2, nfft, plan.layout["alpha"], gamma)
-    assert st["frac"] <= 1e-4 and st["far"] <= 1e-4 and st["bad_mask"] == 0, st
+    st = flip_stats(lg, lo, S2, fhat, plan.layout["k1"], z, gamma)
+    assert_flips(st)
     e = rel(T, To)
-    # when a ridge's true IF crosses a fine-bin boundary, its whole bell of large coefficients sits on
-    # that boundary at once (L << N_f oversamples the bell), so the legitimate boundary flips of one
-    # frame can move most of its energy by one bin: then every large flip must be a boundary flip and
-    # the frames without flips must meet the plane tolerance
-    ff = ((lg != lo) & (lo != -1)).any(axis=1)
-    e_clean = rel(T[~ff], To[~ff])
-    assert e <= 1e-3 or (st["far_big"] <= 1e-4 and e_clean <= 1e-3), (e, e_clean, st)
+    assert e <= 1e-3, (e, st)
     y = plan.inverse(plan.forward(xd)).cpu().numpy()
     yo = O.sst_inverse(To, g, c, hop, nfft, z, plan.layout["k1"], N)
-    print(name, "T", e, "frames without flips", e_clean, "inverse", rel(y, yo), st)
+    print(name, "T", e, "inverse", rel(y, yo), st)
     assert rel(y, yo) <= 1e-4, rel(y, yo)
 
 

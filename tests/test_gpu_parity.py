@@ -1,10 +1,11 @@
 """GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by element.
 
-Tolerances (BASELINE.json north_star): STFT relative Frobenius <= 1e-5; squeezed plane
-relative L2 <= 1e-3 with target disagreement <= 1e-4 of above-threshold coefficients, lying
-within 1e-4 coarse bins of a rounding boundary wherever an fp32 STFT resolves the reassignment
-frequency that finely (reading R21); reconstruction relative L2 <= 1e-4.  The oracle
-only ever receives the same fp32 samples (upcast to fp64) and its own window -- never GPU output.
+Tolerances (BASELINE.json north_star), asserted unconditionally in every test: STFT relative
+Frobenius <= 1e-5; squeezed plane relative L2 <= 1e-3 with target disagreement <= 1e-4 of
+above-threshold coefficients, every flip lying within 1e-4 coarse bins of a rounding boundary
+(tests/_helpers.assert_flips; the GPU re-takes uncertain decisions in fp64, reading R23);
+reconstruction relative L2 <= 1e-4.  The oracle only ever receives the same fp32 samples (upcast to
+fp64) and its own window -- never GPU output.
 """
 
 import numpy as np
@@ -17,7 +18,7 @@ pytestmark = [pytest.mark.gpu,
 
 import oracle as O  # noqa: E402
 from gen import get_config  # noqa: E402
-from tests._helpers import config_gamma, flip_stats, make_plan, rel, signal  # noqa: E402
+from tests._helpers import assert_flips, config_gamma, flip_stats, make_plan, rel, signal  # noqa: E402
 
 DEV = torch.device("cuda:0")
 
@@ -89,15 +90,11 @@ def test_forward_parity_and_flips(P, spec):
     lg = plan.targets(xd).cpu().numpy()
     To, S, Sd, lo = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, gamma, debug=True)
     _, _, fhat = O.if_estimate(S, Sd, nfft, gamma)
-    st = flip_stats(lg, lo, S, fhat, plan.layout["k1"], z, Sd, nfft, plan.layout["alpha"], gamma)
+    st = flip_stats(lg, lo, S, fhat, plan.layout["k1"], z, gamma)
     assert T.shape == To.shape
-    assert st["frac"] <= 1e-4, st
-    assert st["far"] <= 1e-4 and st["bad_mask"] == 0, st
-    # whole-plane tolerance of the north star; these synthetic cases are almost noise-free tones and
-    # chirps whose ridge coefficients can sit on a rounding boundary, so a few legitimate boundary
-    # flips of large coefficients may exceed it -- then the flips must be that rare
+    assert_flips(st)
     e = rel(T, To)
-    assert e <= 1e-3 or st["frac"] <= 1e-5, (e, st)
+    assert e <= 1e-3, (e, st)
 
 
 @pytest.mark.parametrize("spec", SMALL, ids=[f"nf{s[5]}_h{s[4]}_z{s[8]}_N{s[0]}" for s in SMALL])
@@ -230,25 +227,34 @@ def test_c1_full(P):
     To, S, Sd, lo = O.sst_forward(x.astype(np.float64), g, gd, c, cfg.hop, cfg.nfft, cfg.fs, cfg.f1, cfg.f2,
                                   cfg.zoom, gamma, debug=True)
     _, _, fhat = O.if_estimate(S, Sd, cfg.nfft, gamma)
-    st = flip_stats(lg, lo, S, fhat, cfg.k1, cfg.zoom, Sd, cfg.nfft, plan.layout["alpha"], gamma)
+    st = flip_stats(lg, lo, S, fhat, cfg.k1, cfg.zoom, gamma)
     Tg = T.cpu().numpy()
     assert rel(Tg, To) <= 1e-3, st
-    assert st["frac"] <= 1e-4, st
-    assert st["far"] <= 1e-4 and st["bad_mask"] == 0, st
+    assert_flips(st)
     yo = O.sst_inverse(To, g, c, cfg.hop, cfg.nfft, cfg.zoom, cfg.k1, cfg.N)
     assert rel(y.cpu().numpy(), yo) <= 1e-4
 
 
-def _windows(F, n, size, seed):
+def _windows(F, n, size, seed, seams=0):
+    """n frame windows of ``size`` frames: both record edges, the windows centred on the rank
+    boundaries F r / P of a P = ``seams`` sharding, the rest at seeded random positions."""
     rng = np.random.default_rng(seed)
-    starts = sorted(set([0, F - size] + list(rng.integers(0, F - size, size=n - 2))))
-    return [(int(s), int(s) + size) for s in starts]
+    fixed = [0, F - size] + ([F * r // seams - size // 2 for r in range(1, seams)] if seams else [])
+    starts = set(fixed)
+    while len(starts) < n:
+        starts.add(int(rng.integers(0, F - size)))
+    return [(int(s), int(s) + size) for s in sorted(starts)]
+
+
+# windows per config: SURVEY §8(d) asks for 64 windows of 1024 frames on C4-C5 (every P = 8 rank seam
+# included); C2 / C3 get the same treatment at their (whole-record) launch
+WINDOWS = {"C2": (16, 1024), "C3": (64, 1024), "C4": (64, 1024), "C5": (64, 1024)}
 
 
 @pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
 def test_config_sampled_frames(P, name):
     """Full-size configs in the bench's launch configuration, compared on sampled frame windows
-    (both record edges included) that the oracle computes one by one."""
+    (both record edges and the P = 8 rank seams included) that the oracle computes one by one."""
     cfg = get_config(name)
     x = signal(name)
     g, gd, c = O.gaussian_window(cfg.L, cfg.sigma)
@@ -256,25 +262,29 @@ def test_config_sampled_frames(P, name):
     plan = make_plan(P, cfg, gamma)
     xd = torch.from_numpy(x).to(DEV)
     F = cfg.frames
+    n, size = WINDOWS[name]
+    wins = _windows(F, n, size, 5, seams=8)
     if name in ("C4", "C5"):
-        wins = _windows(F, 6, 512, 5)     # T of C4 / C5 is 64 / 256 GiB: forward the windows only
-        Tw = {w: plan.forward(xd, *w).cpu().numpy() for w in wins}
+        Tw = None                          # T of C4 / C5 is 64 / 256 GiB: forward the windows only
     else:
         T = plan.forward(xd)
-        wins = _windows(F, 6, 512, 5)
         Tw = {w: T[w[0]:w[1]].cpu().numpy() for w in wins}
         del T
     x64 = x.astype(np.float64)
+    worst = 0.0
     for w in wins:
+        Tg = plan.forward(xd, *w).cpu().numpy() if Tw is None else Tw[w]
         fr = np.arange(*w)
         To, S, Sd, lo = O.sst_forward(x64, g, gd, c, cfg.hop, cfg.nfft, cfg.fs, cfg.f1, cfg.f2, cfg.zoom,
                                       gamma, frames=fr, debug=True)
-        assert rel(Tw[w], To) <= 1e-3, (name, w)
+        e = rel(Tg, To)
+        worst = max(worst, e)
+        assert e <= 1e-3, (name, w, e)
         lg = plan.targets(xd, *w).cpu().numpy()
         _, _, fhat = O.if_estimate(S, Sd, cfg.nfft, gamma)
-        st = flip_stats(lg, lo, S, fhat, cfg.k1, cfg.zoom, Sd, cfg.nfft, plan.layout["alpha"], gamma)
-        assert st["frac"] <= 1e-4, (name, w, st)
-        assert st["far"] <= 1e-4 and st["bad_mask"] == 0, (name, w, st)
+        st = flip_stats(lg, lo, S, fhat, cfg.k1, cfg.zoom, gamma)
+        assert_flips(st, (name, w))
+    print(name, "windows", len(wins), "worst T rel L2", worst)
 
 
 @pytest.mark.parametrize("name", ["C3"])
@@ -352,15 +362,10 @@ def test_extreme_parameters(P, spec):
     To, So64, Sdo64, lo = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, 1e-5, debug=True)
     lg = plan.targets(xd).cpu().numpy()
     _, _, fhat = O.if_estimate(So64, Sdo64, nfft, 1e-5)
-    st = flip_stats(lg, lo, So64, fhat, plan.layout["k1"], z, Sdo64, nfft, plan.layout["alpha"], 1e-5)
+    st = flip_stats(lg, lo, So64, fhat, plan.layout["k1"], z, 1e-5)
     e = rel(T.cpu().numpy(), To)
-    # flips where fp32 resolves r must sit on a boundary (R21); the flip rate grows with z (the fp32
-    # error of r is magnified z times on the fine grid) and a 9-tap window makes r ill-conditioned,
-    # so these deliberately extreme cases allow z/8 x the north-star rate, and a plane error above
-    # 1e-3 only from that handful of flips
-    assert st["far"] <= 1e-4 and st["bad_mask"] == 0, st
-    assert st["frac"] <= 1e-4 * max(1.0, z / 8), (e, st)
-    assert e <= 1e-3 or st["frac"] <= 2e-5 * max(1.0, z / 8), (e, st)
+    assert_flips(st)
+    assert e <= 1e-3, (e, st)
     y = plan.inverse(T).cpu().numpy()
     yo = O.sst_inverse(To, g, c, hop, nfft, z, plan.layout["k1"], N)
     assert rel(y, yo) <= 1e-4
