@@ -125,10 +125,29 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------- reference arm
-def _oracle_window_record(cfg, nfr):
-    """A local record for timing the oracle on ``nfr`` consecutive frames from the middle of the
-    workload: local sample j = global sample f0*H + j, so local frame m = global frame f0 + m."""
-    f0 = cfg.frames // 3
+def host_info():
+    """Cores this process may use (sched_getaffinity) and the CPU model (/proc/cpuinfo)."""
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return cores, model
+
+
+def _oracle_window_record(cfg, nfr, f0=None):
+    """A local record for timing the oracle on ``nfr`` consecutive frames of the workload starting at
+    global frame f0 (default: a third into the record): local sample j = global sample f0*H + j, so
+    local frame m = global frame f0 + m."""
+    f0 = cfg.frames // 3 if f0 is None else f0
     lo = f0 * cfg.hop
     hi = min(cfg.N, lo + nfr * cfg.hop + cfg.L)
     return generate(cfg, lo, hi).astype(np.float64)
@@ -143,51 +162,138 @@ def _oracle_step(O, cfg, xl, g, gd, c, gamma, nfr):
     return nfr * cfg.hop
 
 
-def run_reference(args, cfg):
-    """The fp64 numpy oracle, as it stands, on a bounded sample of the workload per step."""
+def _oracle_setup(name, nfr, f0=None):
     import oracle as O
+    cfg = get_config(name)
     g, gd, c = O.gaussian_window(cfg.L, cfg.sigma)
-    nfr = args.ref_frames
-    xl = _oracle_window_record(cfg, nfr)
-    gamma = 1e-6 * float(np.sum(g)) * float(np.abs(xl).max())
-    for _ in range(args.warmup):
-        _oracle_step(O, cfg, xl, g, gd, c, gamma, nfr)
+    xl = _oracle_window_record(cfg, nfr, f0)
+    gamma = 1e-6 * float(np.sum(g)) * float(np.abs(xl).max())     # reading R6 (bound from x)
+    return O, cfg, xl, g, gd, c, gamma
+
+
+def _oracle_worker(name, nfr, seconds, wid, barrier, out):
+    """One process of the all-core oracle timing (BLAS / FFT threads = 1): its own chunk of frames,
+    one untimed step, then steps for ``seconds`` after all workers have reached the barrier."""
+    O, cfg, xl, g, gd, c, gamma = _oracle_setup(name, nfr, cfg_f0(name, wid))
+    _oracle_step(O, cfg, xl, g, gd, c, gamma, nfr)
+    barrier.wait()
     t0 = time.perf_counter()
-    samples = 0
-    for _ in range(args.steps):
-        samples += _oracle_step(O, cfg, xl, g, gd, c, gamma, nfr)
-    dt = time.perf_counter() - t0
+    done = 0
+    while time.perf_counter() - t0 < seconds:
+        done += _oracle_step(O, cfg, xl, g, gd, c, gamma, nfr)
+    out.put((wid, done, time.perf_counter() - t0))
+
+
+def cfg_f0(name, wid):
+    cfg = get_config(name)
+    return (cfg.frames // 3 + wid * 4096) % max(1, cfg.frames - 8192)
+
+
+def _single_thread_env():
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS", "NUMEXPR_NUM_THREADS"):
+        os.environ[v] = "1"
+
+
+def oracle_all_core(name, nfr, seconds, procs):
+    """The oracle as it stands on every host core: one spawned process per core over its own
+    frame chunk (SURVEY §8(c) 'Parallelism for timing'; the arithmetic is unchanged).  Returns
+    (input Msamples/s aggregated over the processes, processes)."""
+    import multiprocessing as mp
+    _single_thread_env()
+    ctx = mp.get_context("spawn")
+    barrier = ctx.Barrier(procs)
+    out = ctx.Queue()
+    ps = [ctx.Process(target=_oracle_worker, args=(name, nfr, seconds, w, barrier, out)) for w in range(procs)]
+    for p in ps:
+        p.start()
+    res = [out.get() for _ in ps]
+    for p in ps:
+        p.join()
+    samples = sum(r[1] for r in res)
+    dt = max(r[2] for r in res)
+    return samples / dt / 1e6, procs
+
+
+def oracle_gamma_prepass(name, nfr, seconds):
+    """The relative-gamma pre-pass of the oracle (max |S| over the frames, Eq. 13 / R6):
+    one STFT per frame, timed on its own, single process; input Msamples/s."""
+    O, cfg, xl, g, gd, c, gamma = _oracle_setup(name, nfr)
+    done, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        float(np.abs(O.stft(xl, g, c, cfg.hop, cfg.nfft, frames=np.arange(nfr))).max())
+        done += nfr * cfg.hop
+    return done / (time.perf_counter() - t0) / 1e6
+
+
+def run_reference(args, cfg):
+    """The fp64 numpy oracle, as it stands, on the box's host cores: each step is one bounded sample
+    of the workload per core (``--ref-frames`` consecutive frames, forward + inverse of the interior),
+    all cores in parallel (one spawned process each); the step time is the wall time of the slowest."""
+    import multiprocessing as mp
+    cores, model = host_info()
+    procs = max(1, min(cores, args.ref_procs or cores))
+    _single_thread_env()
+    ctx = mp.get_context("spawn")
+    nfr = args.ref_frames
+    with ctx.Pool(procs) as pool:
+        def step():
+            return sum(pool.starmap(_ref_step_worker, [(cfg.name, nfr, w) for w in range(procs)]))
+        pool.starmap(_ref_step_worker, [(cfg.name, 8, w) for w in range(procs)])   # import + cache warm-up
+        for _ in range(args.warmup):
+            step()
+        t0 = time.perf_counter()
+        samples = 0
+        for _ in range(args.steps):
+            samples += step()
+        dt = time.perf_counter() - t0
     value = samples / dt / 1e6
-    sample_desc = (f"{nfr} consecutive frames of {cfg.name} per step (forward of all {nfr} frames + inverse of "
-                   f"the interior half), single-process numpy fp64")
+    sample_desc = (f"per step {procs} processes x {nfr} consecutive frames of {cfg.name} (forward of all frames + "
+                   f"inverse of the interior half), numpy fp64, one process per core, BLAS/FFT threads 1")
     line = {
         "impl": "reference", "metric": "SST fwd+inverse input Msamples/s", "value": value, "unit": "Msamples/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD_DESC[cfg.name], "sample_frames": nfr},
-        "cpu_baseline": {"value": value, "unit": "Msamples/s", "cores": 1, "kind": "oracle", "sample": sample_desc},
+        "config": {"workload": WORKLOAD_DESC[cfg.name], "sample_frames_per_process": nfr},
+        "cpu_baseline": {"value": value, "unit": "Msamples/s", "cores": procs, "cpu_model": model,
+                         "kind": "oracle", "sample": sample_desc},
         "e2e": {"value": value, "unit": "Msamples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+_REF_CACHE = {}
+
+
+def _ref_step_worker(name, nfr, wid):
+    key = (name, nfr, wid)
+    if key not in _REF_CACHE:
+        _REF_CACHE[key] = _oracle_setup(name, nfr, cfg_f0(name, wid))
+    O, cfg, xl, g, gd, c, gamma = _REF_CACHE[key]
+    return _oracle_step(O, cfg, xl, g, gd, c, gamma, nfr)
+
+
 def cpu_baseline(cfg, seconds_target=12.0):
-    """Oracle timed on a bounded sample (rank 0, N=1 only): repeated 128-frame chunks for about
-    ``seconds_target`` seconds; Msamples/s = frames * H_t / time."""
-    import oracle as O
-    g, gd, c = O.gaussian_window(cfg.L, cfg.sigma)
+    """Oracle timed on bounded samples of the workload (rank 0, N=1 only): single process and all
+    cores (one process per core), each for about ``seconds_target`` s of 128-frame chunks, plus the
+    relative-gamma pre-pass on its own; Msamples/s = frames * H_t / time."""
+    O, cfg_, xl, g, gd, c, gamma = _oracle_setup(cfg.name, 128)
     nfr = 128
-    xl = _oracle_window_record(cfg, nfr)
-    gamma = 1e-6 * float(np.sum(g)) * float(np.abs(xl).max())
     done = 0
     t0 = time.perf_counter()
     while time.perf_counter() - t0 < seconds_target:
         done += _oracle_step(O, cfg, xl, g, gd, c, gamma, nfr)
     dt = time.perf_counter() - t0
-    return {"value": done / dt / 1e6, "unit": "Msamples/s", "cores": 1, "kind": "oracle",
-            "sample": f"{done // cfg.hop} frames of {cfg.name} in chunks of {nfr} consecutive frames (forward + "
-                      f"inverse of each chunk's interior half), single-process numpy fp64, {dt:.1f} s"}
+    single = done / dt / 1e6
+    cores, model = host_info()
+    allc, procs = oracle_all_core(cfg.name, nfr, seconds_target, cores)
+    pre = oracle_gamma_prepass(cfg.name, nfr, min(5.0, seconds_target))
+    return {"value": allc, "unit": "Msamples/s", "cores": procs, "cpu_model": model, "kind": "oracle",
+            "single_core_value": single, "gamma_prepass_single_core": pre,
+            "sample": f"{cfg.name}: chunks of {nfr} consecutive frames (forward + inverse of each chunk's interior "
+                      f"half), numpy fp64; value = {procs} processes (one per core, BLAS/FFT threads 1) for "
+                      f"{seconds_target:.0f} s; single_core_value = one process for {dt:.1f} s ({done // cfg.hop} "
+                      f"frames); gamma_prepass_single_core = the relative-gamma max|S| pre-pass alone, one process"}
 
 
 # ------------------------------------------------------------------------------------- our arm
@@ -435,7 +541,8 @@ def main():
     ap.add_argument("--e2e-chunks", type=int, default=8)
     ap.add_argument("--e2e-no-graph", action="store_true", help="launch the e2e round trip chunk by chunk")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--ref-frames", type=int, default=2048)
+    ap.add_argument("--ref-frames", type=int, default=512)
+    ap.add_argument("--ref-procs", type=int, default=0, help="reference arm processes (default: every core)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
