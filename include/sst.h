@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SST_ABI_VERSION 1
+#define SST_ABI_VERSION 2
 
 typedef enum {
     SST_OK = 0,
@@ -94,7 +94,19 @@ typedef struct {
     double alpha;         /* g' packing scale (R18)                                            */
     double hf;            /* H_f = N / N_f                                             */
     double hf_bound;      /* Eq. 38 bound 3N/(4 pi sigma fs) (sigma in s), 0 if sigma unknown  */
+    double sigma_f_hz;    /* frequency diffusion sigma_f = 1/(2 pi sigma) (Eq. 35), 0 if
+                             sigma unknown                                                     */
+    double df_eq37_hz;    /* Eq. 37 limit 1.5 sigma_f on df; same condition as Eq. 38  */
+    double df_eq46_hz;    /* Eq. 46 limit sqrt(2) sigma_f on df                        */
+    double hf_bound46;    /* Eq. 46 as an H_f bound: N sqrt(2) sigma_f / fs            */
+    uint32_t warnings;    /* SST_WARN_* bits: which of the bounds df exceeds (non-fatal)       */
 } sst_layout;
+
+/* sst_layout.warnings (also reported as text by sst_last_error after sst_plan_create) */
+enum {
+    SST_WARN_EQ37 = 1u,   /* df >= 1.5 sigma_f (Eq. 37 / Eq. 38): reassignment stops concentrating */
+    SST_WARN_EQ46 = 2u    /* df >= sqrt(2) sigma_f (Eq. 46): outside the effective-SST interval    */
+};
 
 typedef struct sst_plan sst_plan;
 
@@ -107,7 +119,9 @@ typedef struct sst_plan sst_plan;
 sst_status sst_gaussian_window(int32_t L, double sigma_samples, int32_t center, double* g, double* gd);
 
 /* Validate parameters without a GPU (the checks of sst_plan_create, R9, R20).
- * Returns SST_OK, SST_E_INVALID_ARGUMENT, SST_E_COVERAGE or SST_E_UNSUPPORTED.             */
+ * Returns SST_OK, SST_E_INVALID_ARGUMENT, SST_E_COVERAGE or SST_E_UNSUPPORTED (also when a
+ * window / hop needs more than 227 KB of shared memory for the forward, the inverse, or the
+ * z = 1 inverse that sst_istft runs).                                                       */
 sst_status sst_params_validate(const sst_params* p);
 
 /* Layout a valid parameter set would have (host only, no plan).                            */
@@ -115,7 +129,9 @@ sst_status sst_params_layout(const sst_params* p, sst_layout* out);
 
 const char* sst_status_str(sst_status s);
 /* Message for the last failing call on `plan`; plan == NULL -> this thread's last failure.
- * Also carries non-fatal warnings (H_f above the Eq. 38 bound) after plan creation. */
+ * Also carries non-fatal warnings after plan creation: df at or above the Eq. 37 limit
+ * 1.5 sigma_f (H_f above the Eq. 38 bound) and / or the Eq. 46 limit
+ * sqrt(2) sigma_f -- see sst_layout.warnings.                                     */
 const char* sst_last_error(const sst_plan* plan);
 int32_t sst_abi_version(void);
 

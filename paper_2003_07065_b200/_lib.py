@@ -10,8 +10,12 @@ from __future__ import annotations
 import ctypes
 import os
 
+ABI_VERSION = 2                  # SST_ABI_VERSION of include/sst.h this binding mirrors
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("SST_LIB_PATH") or os.path.join(_HERE, "libsst.so")   # override: dev A/B builds only
+# SST_LIB=bounds loads the -DSST_BOUNDS debug build (device-side bounds asserts); SST_LIB_PATH
+# overrides the path (dev A/B builds only)
+_VARIANT = {"": "libsst.so", "release": "libsst.so", "bounds": "libsst_bounds.so"}[os.environ.get("SST_LIB", "")]
+LIB_PATH = os.environ.get("SST_LIB_PATH") or os.path.join(_HERE, _VARIANT)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -19,6 +23,8 @@ if not os.path.exists(LIB_PATH):
         "There is no fallback implementation.")
 
 lib = ctypes.CDLL(LIB_PATH)
+if lib.sst_abi_version() != ABI_VERSION:
+    raise ImportError(f"{LIB_PATH} has ABI version {lib.sst_abi_version()}, this binding needs {ABI_VERSION}: rebuild it")
 
 # ---------------------------------------------------------------- constants (sst.h)
 SST_OK = 0
@@ -33,6 +39,9 @@ SST_GAMMA_RELATIVE = 1
 SST_SOURCE_TRUNCATE = 2
 SST_DETERMINISTIC = 4
 SST_DISCRETE_CONSTANT = 8
+
+SST_WARN_EQ37 = 1
+SST_WARN_EQ46 = 2
 
 _i32, _i64, _u32, _dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_double
 _vp = ctypes.c_void_p
@@ -49,7 +58,9 @@ class sst_layout(ctypes.Structure):
     _fields_ = [("n", _i64), ("frames", _i64), ("bins", _i32), ("k1", _i32), ("k2", _i32),
                 ("nfft", _i32), ("zoom", _i32), ("hop", _i32), ("center", _i32), ("win_len", _i32),
                 ("src_bins", _i32), ("fs", _dbl), ("f0_hz", _dbl), ("df_hz", _dbl), ("dfz_hz", _dbl),
-                ("gamma_abs", _dbl), ("alpha", _dbl), ("hf", _dbl), ("hf_bound", _dbl)]
+                ("gamma_abs", _dbl), ("alpha", _dbl), ("hf", _dbl), ("hf_bound", _dbl),
+                ("sigma_f_hz", _dbl), ("df_eq37_hz", _dbl), ("df_eq46_hz", _dbl), ("hf_bound46", _dbl),
+                ("warnings", _u32)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

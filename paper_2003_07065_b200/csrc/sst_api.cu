@@ -155,7 +155,8 @@ sst_status validate(const sst_params* p, sst_layout* lay, std::string& msg) {
         constexpr int kMaxSmem = 227 * 1024;
         const int n2 = p->nfft / 64;
         if (p->hop <= L && p->nfft <= sst::kMaxFusedNfft && (sst::fwd_layout(n2, L, p->hop).total > kMaxSmem ||
-                            sst::inv_layout(n2, L, p->hop, p->zoom).total > kMaxSmem)) {
+                            sst::inv_layout(n2, L, p->hop, p->zoom).total > kMaxSmem ||
+                            sst::inv_layout(n2, L, p->hop, 1).total > kMaxSmem)) {   // z = 1: sst_istft
             msg = "window / hop too large for this build's shared-memory tiles (227 KB per CTA)";
             return SST_E_UNSUPPORTED;
         }
@@ -201,6 +202,14 @@ sst_status validate(const sst_params* p, sst_layout* lay, std::string& msg) {
         lay->alpha = p->sigma > 0 ? p->sigma * std::sqrt(2.0) : (sgd2 > 0 ? std::sqrt(sg2 / sgd2) : 1.0);
         lay->hf = (double)N / p->nfft;
         lay->hf_bound = p->sigma > 0 ? 3.0 * (double)N / (4.0 * kPi * p->sigma) : 0.0;   // Eq. 38, sigma_s = sigma/fs
+        // Eq. 35: sigma_f = 1/(2 pi sigma_s) Hz with sigma_s = sigma / fs; Eq. 37 / Eq. 46 limits on df
+        lay->sigma_f_hz = p->sigma > 0 ? p->fs / (2.0 * kPi * p->sigma) : 0.0;
+        lay->df_eq37_hz = 1.5 * lay->sigma_f_hz;
+        lay->df_eq46_hz = std::sqrt(2.0) * lay->sigma_f_hz;
+        lay->hf_bound46 = lay->df_eq46_hz * (double)N / p->fs;
+        lay->warnings = 0;
+        if (p->sigma > 0 && df >= lay->df_eq37_hz) lay->warnings |= SST_WARN_EQ37;
+        if (p->sigma > 0 && df >= lay->df_eq46_hz) lay->warnings |= SST_WARN_EQ46;
     }
     msg.clear();
     return SST_OK;
@@ -549,11 +558,22 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
         if (pl->fwd_grid <= 0 || pl->inv_grid <= 0) { delete pl; return fail(nullptr, SST_E_CUDA, "occupancy query failed"); }
     }
     pl->err.clear();
-    if (pl->lay.hf_bound > 0 && pl->lay.hf > pl->lay.hf_bound) {
-        char buf[256];
-        std::snprintf(buf, sizeof buf, "warning: H_f = %.3g exceeds the Eq. 38 bound %.3g (P:L357); SST degenerates to STFT",
-                      pl->lay.hf, pl->lay.hf_bound);
-        pl->err = buf;
+    if (pl->lay.warnings) {
+        char buf[512];
+        std::string w = "warning:";
+        if (pl->lay.warnings & SST_WARN_EQ37) {
+            std::snprintf(buf, sizeof buf,
+                          " df = %.4g Hz >= 1.5 sigma_f = %.4g Hz (Eq. 37, P:L353), i.e. H_f = %.4g >= %.4g (Eq. 38, P:L357):"
+                          " reassignment no longer concentrates, SST degenerates to the STFT;",
+                          pl->lay.df_hz, pl->lay.df_eq37_hz, pl->lay.hf, pl->lay.hf_bound);
+            w += buf;
+        }
+        if (pl->lay.warnings & SST_WARN_EQ46) {
+            std::snprintf(buf, sizeof buf, " df = %.4g Hz >= sqrt(2) sigma_f = %.4g Hz, H_f = %.4g >= %.4g (Eq. 46, P:L413)",
+                          pl->lay.df_hz, pl->lay.df_eq46_hz, pl->lay.hf, pl->lay.hf_bound46);
+            w += buf;
+        }
+        pl->err = w;
     }
     *out = pl;
     return SST_OK;

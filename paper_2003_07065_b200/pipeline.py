@@ -22,6 +22,12 @@ class RoundTrip:
     """Reusable device buffers + streams for repeated round trips of one plan."""
 
     def __init__(self, plan, chunks: int = 8):
+        from ._lib import SST_GAMMA_RELATIVE
+        if (plan.flags & SST_GAMMA_RELATIVE) and plan._absmax_ref is None:
+            # each chunk's forward would otherwise take max|S| over its own frames only, so the
+            # chunks would use different thresholds (Eq. 13): require the record's max up front
+            raise ValueError("RoundTrip with SST_GAMMA_RELATIVE needs the record's max|S|: call "
+                             "plan.set_absmax(plan.absmax(x_device)) (or an all-reduced max) first")
         self.plan = plan
         lay = plan.layout
         self.N, self.H, self.c, self.L, self.F = lay["n"], lay["hop"], lay["center"], lay["win_len"], lay["frames"]

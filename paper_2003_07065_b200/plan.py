@@ -65,6 +65,16 @@ def _ptr(t: torch.Tensor, device: torch.device, dtype, name: str) -> int:
     return t.data_ptr()
 
 
+def _rows(T: torch.Tensor, rows: int, bins: int, name: str):
+    """T must be a 2-D [>= rows, ldT >= B] plane (the C ABI cannot see tensor extents)."""
+    if not isinstance(T, torch.Tensor) or T.dim() != 2:
+        raise ValueError(f"{name} must be a 2-D [rows, ldT] tensor")
+    if rows < 0 or T.shape[0] < rows:
+        raise ValueError(f"{name} has {T.shape[0]} rows, need {rows}")
+    if T.shape[1] < bins:
+        raise ValueError(f"{name} has ldT = {T.shape[1]} < B = {bins}")
+
+
 def _stream(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
@@ -157,8 +167,11 @@ class Plan:
         """sst_inverse: x_hat[N] float32 from the whole-record T (Eq. 25-26)."""
         if T.dim() != 2 or T.shape[0] != self.frames:
             raise ValueError("T must be [F, ldT] with all frames")
+        _rows(T, self.frames, self.bins, "T")
         if out is None:
             out = torch.empty(self.n, dtype=torch.float32, device=self.device)
+        if out.numel() < self.n:
+            raise ValueError("out must hold N samples")
         L.check(L.sst_inverse(self._h, _ptr(T, self.device, torch.complex64, "T"), T.shape[1],
                               _ptr(out, self.device, torch.float32, "y"), _stream(self.device)), self._h)
         return out
@@ -166,6 +179,7 @@ class Plan:
     def inverse_accumulate(self, T: torch.Tensor, frame_begin: int, frame_end: int, y: torch.Tensor,
                            y_off: int = 0) -> torch.Tensor:
         """sst_inverse_accumulate: y += unnormalised OLA of frames [frame_begin, frame_end)."""
+        _rows(T, int(frame_end) - int(frame_begin), self.bins, "T")
         L.check(L.sst_inverse_accumulate(self._h, _ptr(T, self.device, torch.complex64, "T"), T.shape[1],
                                          int(frame_begin), int(frame_end),
                                          _ptr(y, self.device, torch.float32, "y"), int(y_off), y.numel(),
@@ -191,8 +205,7 @@ class Plan:
 
     def renyi(self, T: torch.Tensor, alpha: float = 3.0) -> torch.Tensor:
         """sst_renyi: device float64 [3] = (sum |T|^2, sum |T|^(2 alpha), H_alpha) (Eq. 32)."""
-        if T.dim() != 2:
-            raise ValueError("T must be [rows, ldT]")
+        _rows(T, T.shape[0] if T.dim() == 2 else -1, self.bins, "T")
         out = torch.empty(3, dtype=torch.float64, device=self.device)
         L.check(L.sst_renyi(self._h, _ptr(T, self.device, torch.complex64, "T"), T.shape[0], T.shape[1],
                             float(alpha), out.data_ptr(), _stream(self.device)), self._h)
@@ -201,6 +214,7 @@ class Plan:
     # ------------------------------------------------------------------ mode retrieval (f1, R22)
     def ridge_emission(self, T: torch.Tensor):
         """sst_ridge_emission: (E float64 [rows, B], floor float64 scalar) on the device."""
+        _rows(T, T.shape[0] if T.dim() == 2 else -1, self.bins, "T")
         E = torch.empty((T.shape[0], self.bins), dtype=torch.float64, device=self.device)
         fl = torch.empty((), dtype=torch.float64, device=self.device)
         L.check(L.sst_ridge_emission(self._h, _ptr(T, self.device, torch.complex64, "T"), T.shape[1], T.shape[0],
@@ -209,6 +223,8 @@ class Plan:
 
     def ridge(self, E: torch.Tensor, floor: torch.Tensor, lam: float = 0.01, count: int = 1, suppress: int = 3):
         """sst_ridge: int32 [count, rows] ridge paths (E is modified: suppressed zones)."""
+        if E.dim() != 2 or E.shape[1] != self.bins:
+            raise ValueError(f"E must be [rows, B={self.bins}]")
         paths = torch.empty((count, E.shape[0]), dtype=torch.int32, device=self.device)
         L.check(L.sst_ridge(self._h, _ptr(E, self.device, torch.float64, "E"), E.shape[0], float(lam), int(count),
                             int(suppress), _ptr(floor, self.device, torch.float64, "floor"), paths.data_ptr(),
@@ -221,6 +237,9 @@ class Plan:
 
     def zone_mask(self, T: torch.Tensor, path: torch.Tensor, half: int, keep_inside: bool = True) -> torch.Tensor:
         """sst_zone_mask, in place on T."""
+        _rows(T, T.shape[0] if T.dim() == 2 else -1, self.bins, "T")
+        if path.numel() < T.shape[0]:
+            raise ValueError("path must have one bin per row of T")
         L.check(L.sst_zone_mask(self._h, _ptr(T, self.device, torch.complex64, "T"), T.shape[1], T.shape[0],
                                 _ptr(path, self.device, torch.int32, "path"), int(half), int(bool(keep_inside)),
                                 _stream(self.device)), self._h)
@@ -233,6 +252,9 @@ class Plan:
 
     def mode_full(self, T: torch.Tensor, path: torch.Tensor, half: int) -> torch.Tensor:
         """sst_mode_full: Eq. 15 (H_t = 1), float32 [rows]."""
+        _rows(T, T.shape[0] if T.dim() == 2 else -1, self.bins, "T")
+        if path.numel() < T.shape[0]:
+            raise ValueError("path must have one bin per row of T")
         x = torch.empty(T.shape[0], dtype=torch.float32, device=self.device)
         L.check(L.sst_mode_full(self._h, _ptr(T, self.device, torch.complex64, "T"), T.shape[1], T.shape[0],
                                 _ptr(path, self.device, torch.int32, "path"), int(half), x.data_ptr(),

@@ -33,7 +33,7 @@ def test_exports_every_declared_symbol(P):
     for n in names:
         assert hasattr(_lib.lib, n), n
         assert n in _lib.SIGNATURES, n
-    assert _lib.lib.sst_abi_version() == 1
+    assert _lib.lib.sst_abi_version() == _lib.ABI_VERSION == 2
 
 
 def test_status_strings(P):
@@ -117,6 +117,38 @@ def test_layout_values(P):
     # Eq. 38 bound with sigma in seconds = sigma_samples / fs (golden: P:L359 'H_f < 64')
     lay = P.layout(n=8192, fs=1024.0, win_len=187, sigma=0.03 * 1024, hop=20, nfft=1024, f1=0.0, f2=512.0)
     assert int(np.ceil(lay["hf_bound"])) == 64
+
+
+def test_eq37_eq46_warnings(P):
+    """Eq. 35/37/46 limits in the layout (host only) and the warning bits, pinned to the paper's
+    printed values for its simulation (sigma = 0.03 s, N = 8192, fs = 1024): sigma_f = 5.31 Hz
+    (P:L335), H_f < 64 (Eq. 38, P:L359) and H_f < 60 (Eq. 46, P:L415)."""
+    import json
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "paper_values.json")))
+    base = dict(n=8192, fs=1024.0, win_len=187, sigma=0.03 * 1024, hop=20, f1=0.0, f2=512.0)
+    lay = P.layout(nfft=1024, **base)                         # H_f = 8: inside both intervals
+    assert lay["sigma_f_hz"] == pytest.approx(5.305, abs=5e-3)
+    assert int(np.ceil(lay["hf_bound"])) == gold["hf_bound_eq38"]["value"] == 64
+    assert int(np.round(lay["hf_bound46"])) == gold["hf_bound_eq46"]["value"] == 60
+    assert lay["df_eq37_hz"] == pytest.approx(1.5 * lay["sigma_f_hz"])
+    assert lay["df_eq46_hz"] == pytest.approx(np.sqrt(2.0) * lay["sigma_f_hz"])
+    assert lay["warnings"] == 0
+    # H_f = 64 = N / N_f with N_f = 128: df = 8 Hz >= 1.5 sigma_f = 7.96 Hz and >= sqrt 2 sigma_f
+    lay = P.layout(nfft=256, **dict(base, win_len=187))        # H_f = 32: still fine
+    assert lay["warnings"] == 0
+    lay = P.layout(nfft=128, **dict(base, win_len=127, hop=20))
+    assert lay["warnings"] == P.SST_WARN_EQ37 | P.SST_WARN_EQ46
+    # between the two limits: df in [sqrt 2 sigma_f, 1.5 sigma_f) -> only the Eq. 46 bit
+    sig = 1024.0 / (2 * np.pi * 8.0 / 1.45)                      # sigma_f = 8 / 1.45 Hz with df = 8 Hz
+    lay = P.layout(n=8192, fs=1024.0, win_len=127, sigma=sig, hop=20, nfft=128, f1=0.0, f2=512.0)
+    assert lay["warnings"] == P.SST_WARN_EQ46
+
+
+def test_istft_shared_memory_checked_by_validate(P):
+    """A window / hop whose z = 1 inverse (run by sst_istft) needs more shared memory than the plan's
+    z: rejected by validation (SST_E_UNSUPPORTED), not at launch."""
+    assert P.validate(n=1 << 20, fs=1000.0, win_len=4096, sigma=512.0, hop=2048, nfft=4096, f1=0.0, f2=500.0,
+                      zoom=2) == P.SST_E_UNSUPPORTED
 
 
 def test_plan_create_without_gpu_fails_cleanly(P):

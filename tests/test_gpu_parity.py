@@ -480,3 +480,32 @@ def test_pipelined_host_roundtrip(P, chunks):
         torch.cuda.synchronize()
         assert torch.equal(T, T_ref)
         assert torch.equal(yh, y_run)
+
+
+def test_pipelined_roundtrip_relative_gamma(P):
+    """RoundTrip under SST_GAMMA_RELATIVE: refused until the record's max|S| is supplied (chunks would
+    otherwise threshold against their own maxima); with plan.set_absmax(plan.absmax(x)) it equals the
+    single-call forward + inverse (T bitwise, x_hat to re-association)."""
+    from paper_2003_07065_b200.pipeline import RoundTrip
+    spec = SMALL[4]
+    N, fs, L, sigma, hop, nfft, f1, f2, z = spec
+    x, g, gd, c = _case(spec)
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=1e-3, flags=P.SST_GAMMA_RELATIVE, device=0)
+    xd = torch.from_numpy(x).to(DEV)
+    with pytest.raises(ValueError):
+        RoundTrip(plan, chunks=4)
+    amax = plan.absmax(xd)
+    plan.set_absmax(amax)
+    T_ref = plan.forward(xd)
+    y_ref = plan.inverse(T_ref).cpu().numpy()
+    xh = torch.from_numpy(x).pin_memory()
+    yh = torch.zeros(N, dtype=torch.float32).pin_memory()
+    T = torch.empty_like(T_ref)
+    RoundTrip(plan, chunks=4).run(xh, yh, T)
+    torch.cuda.synchronize()
+    assert torch.equal(T, T_ref)
+    assert rel(yh.numpy(), y_ref) <= 1e-6
+    # and the threshold really is the record's: the oracle at 1e-3 * its own max|S|
+    So = O.stft(x.astype(np.float64), g, c, hop, nfft)
+    To = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, 1e-3 * float(np.abs(So).max()))
+    assert rel(T.cpu().numpy(), To) <= 1e-3
