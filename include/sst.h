@@ -182,6 +182,14 @@ sst_status sst_inverse_accumulate(sst_plan* plan, const float* T, int64_t ldT,
                                   float* y, int64_t y_off, int64_t y_len, void* stream);
 /* Step 2: y[n - y_off] /= C d[n] for global n in [y_off, y_off + y_len) (C = sqrt 2 or C_d). */
 sst_status sst_inverse_finalize(sst_plan* plan, float* y, int64_t y_off, int64_t y_len, void* stream);
+/* Step 2 on a rank of a time-sharded inverse: the received seam -- the previous
+ * rank's partial Eq. 26 sums over global samples [seam_off, seam_off + seam_len), device float --
+ * is added and the result normalised in one pass:
+ *   y[n - y_off] = (y[n - y_off] + seam[n - seam_off]) / (C d[n])   (seam term only inside its span).
+ * The seam span must lie inside the y span (SST_E_INVALID_ARGUMENT otherwise); seam_len = 0 is
+ * sst_inverse_finalize.  The transport (NCCL / gloo) only moves the bytes; this is the arithmetic. */
+sst_status sst_inverse_finalize_seam(sst_plan* plan, float* y, int64_t y_off, int64_t y_len, const float* seam,
+                                     int64_t seam_off, int64_t seam_len, void* stream);
 
 /* ---------------------------------------------------------------- plain STFT synthesis ----- */
 

@@ -86,6 +86,7 @@ SIGNATURES = {
     "sst_inverse": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "sst_inverse_accumulate": (_i32, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp]),
     "sst_inverse_finalize": (_i32, [_vp, _vp, _i64, _i64, _vp]),
+    "sst_inverse_finalize_seam": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp]),
     "sst_istft": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "sst_renyi": (_i32, [_vp, _vp, _i64, _i64, _dbl, _vp, _vp]),
     "sst_ridge_emission": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp]),

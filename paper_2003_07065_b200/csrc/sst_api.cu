@@ -55,6 +55,7 @@ struct sst_plan {
     int32_t n_head = 0, n_tail = 0;
     int fwd_grid = 0, inv_grid = 0;
     bool redecide = true;           // R23 (SST_NO_REDECIDE=1 turns it off: timing experiments only)
+    double r23_m = 8.0;             // R23 margin factor over the R21 error model (SST_R23_M: experiments)
     const float* ext_absmax = nullptr;
     double gamma_abs = 0;
     std::string err;
@@ -302,8 +303,8 @@ sst::FwdArgs fwd_args(const sst_plan* pl, const float* x, int64_t x_off, int64_t
     // R23: margins of the fp32 decision, 8 x the R21 error model eta = 4 u sqrt(log2 N_f) ||z_m||
     const double u = std::ldexp(1.0, -24), sl = std::sqrt(std::log2((double)pl->lay.nfft));
     a.redecide = pl->redecide ? 1 : 0;
-    a.cflag = (float)(8.0 * (pl->lay.zoom * pl->lay.nfft / (2.0 * kPi * pl->lay.alpha)) * 4.0 * u * sl);
-    a.kflag = (float)(8.0 * 2.0 * u * sl);
+    a.cflag = (float)(pl->r23_m * (pl->lay.zoom * pl->lay.nfft / (2.0 * kPi * pl->lay.alpha)) * 4.0 * u * sl);
+    a.kflag = (float)(pl->r23_m * 2.0 * u * sl);
     a.gamma_d = pl->gamma_abs;
     a.gamma_rel_d = pl->p.gamma;
     a.taps64 = pl->d_taps64;
@@ -515,6 +516,7 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
         tw64[e] = make_double2(std::cos(a), std::sin(a));
     }
     if (const char* nr = std::getenv("SST_NO_REDECIDE")) pl->redecide = !(nr[0] == '1');
+    if (const char* mm = std::getenv("SST_R23_M")) { const double v = std::atof(mm); if (v > 0) pl->r23_m = v; }
     if ((s = upload(pl, &pl->d_taps, taps)) != SST_OK || (s = upload(pl, &pl->d_tw, tw)) != SST_OK ||
         (s = upload(pl, &pl->d_taps64, taps64)) != SST_OK || (s = upload(pl, &pl->d_tw64, tw64)) != SST_OK ||
         (s = upload(pl, &pl->d_phz, phz)) != SST_OK || (s = upload(pl, &pl->d_inv_head, head)) != SST_OK ||
@@ -887,14 +889,21 @@ sst_status sst_mode_full(sst_plan* plan, const float* T, int64_t ldT, int64_t ro
 }
 
 sst_status sst_inverse_finalize(sst_plan* plan, float* y, int64_t y_off, int64_t y_len, void* stream) {
+    return sst_inverse_finalize_seam(plan, y, y_off, y_len, nullptr, 0, 0, stream);
+}
+
+sst_status sst_inverse_finalize_seam(sst_plan* plan, float* y, int64_t y_off, int64_t y_len, const float* seam,
+                                     int64_t seam_off, int64_t seam_len, void* stream) {
     if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
     if (!y || y_len < 0) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL y or negative length");
     if (y_off < 0 || y_off + y_len > plan->lay.n) return fail(plan, SST_E_INVALID_ARGUMENT, "y span outside [0, N)");
+    if (seam_len < 0 || (seam_len > 0 && (!seam || seam_off < y_off || seam_off + seam_len > y_off + y_len)))
+        return fail(plan, SST_E_INVALID_ARGUMENT, "seam span must lie inside the y span");
     DeviceGuard guard(plan->device);
     return cuda_status(plan,
                        sst::launch_finalize(y, y_off, y_len, plan->lay.n, plan->lay.hop, plan->lay.center, plan->d_inv_head,
                                             plan->n_head, plan->d_inv_tail, plan->n_tail, plan->d_inv_per, 1.0f,
-                                            (cudaStream_t)stream),
+                                            (cudaStream_t)stream, seam_len > 0 ? seam : nullptr, seam_off, seam_len),
                        "finalize launch");
 }
 

@@ -144,7 +144,8 @@ cudaError_t launch_inverse(const InvArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_inverse_seams(const InvArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_finalize(float* y, int64_t y_off, int64_t y_len, int64_t n, int32_t hop, int32_t c,
                             const float* inv_head, int32_t n_head, const float* inv_tail, int32_t n_tail,
-                            const float* inv_per, float out_scale, cudaStream_t s);
+                            const float* inv_per, float out_scale, cudaStream_t s, const float* seam = nullptr,
+                            int64_t seam_off = 0, int64_t seam_len = 0);
 int inverse_max_grid(int nfft, int hop, int L, int zoom, int device);
 
 // Renyi sums over a complex64 plane: partial[2*blockIdx] = {sum |T|^2, sum |T|^(2 alpha)},

@@ -48,7 +48,10 @@ __global__ void seam_kernel(const InvArgs a, int ctas) {
     }
 }
 
-__global__ void finalize_kernel(float* y, int64_t y_off, int64_t y_len, InvArgs a) {
+// y = (y + seam) / (C d[n]) on [y_off, y_off + y_len): the received rank seam (partial OLA sums of the
+// neighbouring rank's frames, Eq. 26) is added in the same pass that normalises (seam == nullptr: none)
+__global__ void finalize_kernel(float* y, int64_t y_off, int64_t y_len, InvArgs a, const float* seam,
+                                int64_t seam_off, int64_t seam_len) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     // r = (s + c) mod hop, advanced incrementally (one 64-bit modulo per thread)
@@ -56,7 +59,11 @@ __global__ void finalize_kernel(float* y, int64_t y_off, int64_t y_len, InvArgs 
     const int step = (int)(stride % a.hop);
     for (; i < y_len; i += stride) {
         const int64_t s = y_off + i;
-        if (s >= 0 && s < a.n) y[i] *= inv_norm_r(s, r, a) * a.out_scale;
+        if (s >= 0 && s < a.n) {
+            float v = y[i];
+            if (seam && s >= seam_off && s < seam_off + seam_len) v += seam[s - seam_off];
+            y[i] = v * inv_norm_r(s, r, a) * a.out_scale;
+        }
         r += step;
         r -= (r >= a.hop) ? a.hop : 0;
     }
@@ -139,7 +146,8 @@ cudaError_t launch_renyi(const float2* T, int64_t rows, int64_t cols, int64_t ld
 
 cudaError_t launch_finalize(float* y, int64_t y_off, int64_t y_len, int64_t n, int32_t hop, int32_t c,
                             const float* inv_head, int32_t n_head, const float* inv_tail, int32_t n_tail,
-                            const float* inv_per, float out_scale, cudaStream_t s) {
+                            const float* inv_per, float out_scale, cudaStream_t s, const float* seam,
+                            int64_t seam_off, int64_t seam_len) {
     InvArgs a{};
     a.out_scale = out_scale;
     a.n = n; a.hop = hop; a.c = c;
@@ -148,7 +156,7 @@ cudaError_t launch_finalize(float* y, int64_t y_off, int64_t y_len, int64_t n, i
     const int64_t want = (y_len + threads - 1) / threads;
     const int blocks = (int)(want < 2368 ? want : 2368);
     if (blocks <= 0) return cudaSuccess;
-    finalize_kernel<<<blocks, threads, 0, s>>>(y, y_off, y_len, a);
+    finalize_kernel<<<blocks, threads, 0, s>>>(y, y_off, y_len, a, seam, seam_off, seam_len);
     return cudaGetLastError();
 }
 

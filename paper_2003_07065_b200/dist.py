@@ -70,27 +70,87 @@ def shard(n: int, hop: int, win_len: int, center: int, world: int, rank: int) ->
     return Shard(rank, world, fb, fe, span_lo, span_hi, own_lo, own_hi, seam_in, seam_out, F)
 
 
-def exchange_seams(y_span: torch.Tensor, sh: Shard, hop: int, center: int, group=None) -> torch.Tensor:
-    """Add rank-1's partial OLA sums into this rank's left seam and send this rank's right-seam
-    partials to rank+1 (ncclSend/ncclRecv via batch_isend_irecv).  ``y_span`` holds the
-    unnormalised partial y over [span_lo, span_hi).  Returns ``y_span`` (modified in place)."""
+def _staged(t: torch.Tensor, group) -> bool:
+    """gloo moves host tensors only: device buffers are staged through the host."""
+    return t.is_cuda and dist.get_backend(group) != "nccl"
+
+
+def exchange_seams(y_span: torch.Tensor, sh: Shard, hop: int, center: int, group=None):
+    """Send this rank's right-seam partial sums to rank+1 and receive rank-1's partial sums of this
+    rank's left seam (ncclSend / ncclRecv via batch_isend_irecv; through the host under gloo).
+    Only moves bytes: the addition (Eq. 26) happens in the library, fused into the finalize pass
+    (``Plan.inverse_finalize_seam``).  ``y_span`` holds the unnormalised partial y over
+    [span_lo, span_hi).  Returns the received seam (global samples [own_lo, own_lo + seam_in)) or
+    None."""
     if sh.world == 1:
-        return y_span
+        return None
+    stage = _staged(y_span, group)
     ops = []
     recv = None
     if sh.seam_out > 0:
         lo = max(0, sh.frame_end * hop - center) - sh.span_lo
-        ops.append(dist.P2POp(dist.isend, y_span[lo:lo + sh.seam_out].contiguous(), sh.rank + 1, group))
+        out = y_span[lo:lo + sh.seam_out].contiguous()
+        ops.append(dist.P2POp(dist.isend, out.cpu() if stage else out, sh.rank + 1, group))
     if sh.seam_in > 0:
-        recv = torch.empty(sh.seam_in, dtype=y_span.dtype, device=y_span.device)
+        recv = torch.empty(sh.seam_in, dtype=y_span.dtype, device="cpu" if stage else y_span.device)
         ops.append(dist.P2POp(dist.irecv, recv, sh.rank - 1, group))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
-    if recv is not None:
-        lo = sh.own_lo - sh.span_lo
-        y_span[lo:lo + sh.seam_in] += recv
-    return y_span
+    if recv is not None and stage:
+        recv = recv.to(y_span.device, non_blocking=False)
+    return recv
+
+
+def finalize_owned(plan, y_span: torch.Tensor, sh: Shard, recv) -> torch.Tensor:
+    """Normalise the samples this rank owns, adding the received left seam in the same pass
+    (sst_inverse_finalize_seam).  Returns the owned slice (a view of ``y_span``)."""
+    own = own_slice(y_span, sh)
+    plan.inverse_finalize_seam(own, sh.own_lo, recv, sh.own_lo)
+    return own
+
+
+class ShardedRun:
+    """One rank's share of the hot path over a time-sharded record: sst_forward of
+    its frames (no collective), and with ``inverse`` the accumulate of its frames' Eq. 26 partial
+    sums over its sample span, the seam exchange with its neighbours, and the owned-range finalise.
+    ``chunk_frames`` bounds the T buffer (records whose band plane does not fit, e.g. C5's 256 GiB
+    on one GPU): the frames are then processed chunk by chunk, forward then accumulate, reusing it.
+    This is the multi-rank step ``bench.py --gpus N`` times."""
+
+    def __init__(self, plan, sh: Shard, x_span: torch.Tensor, inverse: bool = True, chunk_frames: int = 0,
+                 group=None):
+        self.plan, self.sh, self.x, self.inverse, self.group = plan, sh, x_span, inverse, group
+        lay = plan.layout
+        self.hop, self.c = lay["hop"], lay["center"]
+        n = sh.frames
+        self.chunk = n if chunk_frames <= 0 else min(n, chunk_frames)
+        self.T = torch.empty((self.chunk, plan.bins), dtype=torch.complex64, device=plan.device)
+        self.y = torch.empty(sh.span_hi - sh.span_lo, dtype=torch.float32, device=plan.device) if inverse else None
+        self.own = None
+
+    def step(self):
+        sh, plan = self.sh, self.plan
+        if self.inverse:
+            self.y.zero_()
+        for fb in range(sh.frame_begin, sh.frame_end, self.chunk):
+            fe = min(sh.frame_end, fb + self.chunk)
+            T = self.T[:fe - fb]
+            plan.forward(self.x, fb, fe, x_off=sh.span_lo, out=T)
+            if self.inverse:
+                plan.inverse_accumulate(T, fb, fe, self.y, y_off=sh.span_lo)
+        if self.inverse:
+            recv = exchange_seams(self.y, sh, self.hop, self.c, self.group)
+            self.own = finalize_owned(plan, self.y, sh, recv)
+        return self.own
+
+    @property
+    def launches_per_step(self) -> int:
+        chunks = -(-self.sh.frames // self.chunk)
+        if not self.inverse:
+            return chunks
+        # forward + accumulate (+ seam kernel) per chunk, zero fill, finalize
+        return chunks * 3 + 2
 
 
 def own_slice(y_span: torch.Tensor, sh: Shard) -> torch.Tensor:
@@ -100,9 +160,13 @@ def own_slice(y_span: torch.Tensor, sh: Shard) -> torch.Tensor:
 
 def gather_owned(y_own: torch.Tensor, sh: Shard, n: int, dst: int = 0, group=None):
     """Collect every rank's owned samples into one [N] tensor on ``dst`` (verification only;
-    excluded from throughput).  Returns the tensor on dst, None elsewhere."""
+    excluded from throughput; staged through the host under gloo).  Returns the tensor on dst,
+    None elsewhere."""
     if sh.world == 1:
         return y_own
+    if _staged(y_own, group):
+        out = gather_owned(y_own.cpu(), sh, n, dst, group)
+        return None if out is None else out.to(y_own.device)
     sizes = [torch.zeros(1, dtype=torch.int64, device=y_own.device) for _ in range(sh.world)]
     dist.all_gather(sizes, torch.tensor([y_own.numel()], dtype=torch.int64, device=y_own.device), group=group)
     mx = int(max(int(s.item()) for s in sizes))
@@ -144,8 +208,11 @@ def max_over_ranks(value: float, device, group=None) -> float:
     """all_reduce(MAX) of one float (timings, max|S|)."""
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     if dist.is_available() and dist.is_initialized():
+        if _staged(t, group):
+            t = t.cpu()
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
 
 
-__all__ = ["Shard", "shard", "exchange_seams", "own_slice", "gather_owned", "max_over_ranks", "frames_of"]
+__all__ = ["Shard", "shard", "exchange_seams", "finalize_owned", "ShardedRun", "own_slice", "gather_owned",
+           "gather_band", "max_over_ranks", "frames_of"]

@@ -192,6 +192,17 @@ class Plan:
                                        _stream(self.device)), self._h)
         return y
 
+    def inverse_finalize_seam(self, y: torch.Tensor, y_off: int, seam: torch.Tensor | None,
+                              seam_off: int = 0) -> torch.Tensor:
+        """sst_inverse_finalize_seam: y = (y + seam) / (C d[n]) in one pass (seam over global samples
+        [seam_off, seam_off + seam.numel()), inside y's span); seam None -> plain finalize."""
+        if seam is None or seam.numel() == 0:
+            return self.inverse_finalize(y, y_off)
+        L.check(L.sst_inverse_finalize_seam(self._h, _ptr(y, self.device, torch.float32, "y"), int(y_off), y.numel(),
+                                            _ptr(seam, self.device, torch.float32, "seam"), int(seam_off), seam.numel(),
+                                            _stream(self.device)), self._h)
+        return y
+
     # ------------------------------------------------------------------ plain STFT synthesis / analysis
     def istft(self, S: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """sst_istft: Eq. 10-11 synthesis of the one-sided STFT S[F, >= N_f/2+1] (from stft())."""
