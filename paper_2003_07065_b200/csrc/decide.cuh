@@ -54,12 +54,13 @@ __device__ __forceinline__ int bin_target(const FwdArgs& a, float gam4, float cm
     const float fl = floorf(t);
     const int l = base + (int)fl;                                            // Eq. 28 (R10, R17)
     const int lin = ((unsigned)l < (unsigned)a.bins && fin) ? l : -2;
-    // R23 margin of the fine position: z delta r = cm (1/|2S| + (|U|+|V|)/|2S|^2) (R21 error model)
+    // R23 margin of the fine position: z delta r = cm (1/|2S| + (|U|+|V|)/|2S|^2) (R21 error model);
+    // only targets in [-1, B] can cross into / inside the band (margins of coefficients the north
+    // star's location clause covers, |S| >= 1e-2 max|S|, stay far below half a bin)
     const float rs = rsqrtf(mag4);
     const float mg = cm * fmaf(fabsf(UV.x) + fabsf(UV.y), rsq, rs);
     const float fr = t - fl;
-    const float pf = (float)base + t;                                        // fine position + 1/2
-    const bool near_l = fminf(fr, 1.0f - fr) < mg && pf > -mg && pf < (float)a.bins + mg;
+    const bool near_l = fabsf(fr - 0.5f) > 0.5f - mg && (unsigned)(l + 1) <= (unsigned)a.bins + 1u;
     unsure = src && ((keep && near_l) || fabsf(mag4 - gam4) < km);
     return keep ? lin : -1;
 }
@@ -77,27 +78,38 @@ __device__ __forceinline__ void fwd_margins(const FwdArgs& a, float gam4, float 
 
 // fp64 S, S' of bin k of one frame by the direct Eq. 8 sum
 //   S[m,k] = sum_{j=0}^{L-1} x[m H - c + j] g[j] e^{-i 2 pi k (j - c)/N_f}   (and g' for S'),
-// warp-cooperative: all 32 lanes call it with the same k and frame; lane-strided taps, fixed
-// xor-tree reduction (deterministic).  xat(j) returns the frame's sample j as float (zero outside
-// the record).  taps64[j] = (g[j], g'[j]); tw64[e] = exp(-2 pi i e / N_f), both fp64.
+// warp-cooperative: all 32 lanes call it with the same k and frame.  Lane l takes taps
+// j = l + 32 t; with W = e^{-2 pi i/N_f}, W^{k (j - c)} = W^{k (l - c)} W^{32 k t}, so the per-tap
+// twiddle W^{32 k t} is the same for every lane (one broadcast load) and the lane factor
+// W^{k (l - c)} multiplies the lane's partial sums once; fixed xor-tree reduction (deterministic).
+// xat(j) returns the frame's sample j as float (zero outside the record).  taps64[j] = (g[j], g'[j]);
+// tw64[e] = W^e, both fp64.
 template <class XF>
 __device__ __forceinline__ void stft_bin_fp64(XF xat, const double2* __restrict__ taps64,
                                               const double2* __restrict__ tw64, int nfft, int L, int c, int k,
                                               double& sr, double& si, double& dr, double& di) {
     const int lane = threadIdx.x & 31;
     const unsigned msk = (unsigned)nfft - 1u;
-    sr = si = dr = di = 0.0;
+    const unsigned step = (32u * (unsigned)k) & msk;
+    double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+    unsigned e = 0;
 #pragma unroll 4
     for (int j = lane; j < L; j += 32) {
         const double xv = (double)xat(j);
         const double2 w = __ldg(taps64 + j);
-        const double2 e = __ldg(tw64 + (((unsigned)k * (unsigned)(j - c)) & msk));
+        const double2 t = __ldg(tw64 + e);                                   // W^{32 k t}: warp-uniform
         const double p = xv * w.x, q = xv * w.y;
-        sr = fma(p, e.x, sr);
-        si = fma(p, e.y, si);
-        dr = fma(q, e.x, dr);
-        di = fma(q, e.y, di);
+        ar = fma(p, t.x, ar);
+        ai = fma(p, t.y, ai);
+        br = fma(q, t.x, br);
+        bi = fma(q, t.y, bi);
+        e = (e + step) & msk;
     }
+    const double2 f = __ldg(tw64 + (((unsigned)k * (unsigned)(lane - c)) & msk));   // W^{k (l - c)}
+    sr = ar * f.x - ai * f.y;
+    si = ar * f.y + ai * f.x;
+    dr = br * f.x - bi * f.y;
+    di = br * f.y + bi * f.x;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         sr += __shfl_xor_sync(0xffffffffu, sr, o);

@@ -185,7 +185,7 @@ def test_sharded_run_step(world, chunk):
     world ranks equals the single-process inverse; chunking reuses one T buffer."""
     case = CASES[1]
     N, L, hop, nfft, z, g, c, T, k1 = _problem(case)
-    ref = O.sst_inverse(T, g, c, hop, nfft, z, k1, N)
+    ref = O.sst_inverse(T.astype(np.complex64).astype(np.complex128), g, c, hop, nfft, z, k1, N)   # T travels as complex64
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
