@@ -55,7 +55,7 @@ struct sst_plan {
     int32_t n_head = 0, n_tail = 0;
     int fwd_grid = 0, inv_grid = 0;
     bool redecide = true;           // R23 (SST_NO_REDECIDE=1 turns it off: timing experiments only)
-    double r23_m = 8.0;             // R23 margin factor over the R21 error model (SST_R23_M: experiments)
+    double r23_m = 6.0;             // R23 margin factor over the R21 error model (SST_R23_M: experiments)
     const float* ext_absmax = nullptr;
     double gamma_abs = 0;
     std::string err;
