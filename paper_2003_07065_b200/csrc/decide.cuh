@@ -119,6 +119,53 @@ __device__ __forceinline__ void stft_bin_fp64(XF xat, const double2* __restrict_
     }
 }
 
+// The same sum with all TPB threads of a CTA (tap j = thread + TPB t; the per-tap twiddle
+// W^{TPB k t} is uniform, the thread factor W^{k (thread - c)} applied once), reduced over the warps
+// in a fixed order through `red` (TPB/32 double4).  Every thread must call it; v = (Re S, Im S,
+// Re S', Im S') on thread 0 (deterministic).  Ends with a __syncthreads (red reusable).
+template <int TPB, class XF>
+__device__ __forceinline__ void stft_bin_fp64_cta(XF xat, const double2* __restrict__ taps64,
+                                                  const double2* __restrict__ tw64, int nfft, int L, int c, int k,
+                                                  double (&v)[4], double4* red) {
+    const unsigned msk = (unsigned)nfft - 1u;
+    const unsigned step = ((unsigned)TPB * (unsigned)k) & msk;
+    double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+    unsigned e = 0;
+#pragma unroll 4
+    for (int j = threadIdx.x; j < L; j += TPB) {
+        const double xv = (double)xat(j);
+        const double2 w = __ldg(taps64 + j);
+        const double2 t = __ldg(tw64 + e);                                   // W^{TPB k t}: CTA-uniform
+        const double p = xv * w.x, q = xv * w.y;
+        ar = fma(p, t.x, ar);
+        ai = fma(p, t.y, ai);
+        br = fma(q, t.x, br);
+        bi = fma(q, t.y, bi);
+        e = (e + step) & msk;
+    }
+    const double2 f = __ldg(tw64 + (((unsigned)k * (unsigned)((int)threadIdx.x - c)) & msk));
+    double s0 = ar * f.x - ai * f.y, s1 = ar * f.y + ai * f.x;
+    double s2 = br * f.x - bi * f.y, s3 = br * f.y + bi * f.x;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_double4(s0, s1, s2, s3);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        v[0] = v[1] = v[2] = v[3] = 0.0;
+#pragma unroll
+        for (int w = 0; w < TPB / 32; ++w) {
+            const double4 r = red[w];
+            v[0] += r.x; v[1] += r.y; v[2] += r.z; v[3] += r.w;
+        }
+    }
+    __syncthreads();
+}
+
 // The oracle's decision (Eq. 13, 36, 28; R8, R10) in fp64 on the fp64 S, S'.
 __device__ __forceinline__ int decide_fp64(const FwdArgs& a, double gamma, int k, double sr, double si, double dr,
                                            double di) {

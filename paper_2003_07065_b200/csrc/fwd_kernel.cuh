@@ -66,6 +66,10 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
     constexpr bool KEEPL = (MODE == kModeForward || MODE == kModeTargets);   // targets kept in registers
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ float wnrm[TPB / 32];               // per-warp ||z_m||^2 partials (groups of > 1 warp)
+    __shared__ int4 rq[KEEPL ? kRedecideQ : 1];    // R23 queue: (k, frame group, register slot, owner thread)
+    __shared__ int rq_res[KEEPL ? kRedecideQ : 1]; // R23 fp64 decisions
+    __shared__ double4 rq_red[TPB / 32];           // R23 per-warp partial sums
+    __shared__ int rq_n;
     float2* smem = reinterpret_cast<float2*>(smem_raw);
     float2* taps_s = reinterpret_cast<float2*>(smem_raw + a.lay.taps_off);
     float* xbuf = reinterpret_cast<float*>(smem_raw + a.lay.xb_off);
@@ -338,28 +342,42 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                     return i < 16 ? j + 64 * (16 * h + i) : ((j == 0) ? 32 : 64 - j) + 64 * (16 * h + i - 16);
                 }
             };
-            if (__any_sync(0xffffffffu, uns != 0ull)) {
-                // one warp-uniform loop over the warp's flagged (lane, slot) pairs with a single copy of
-                // the fp64 sum (an unrolled copy per slot measured ~30x slower: cold instruction cache)
-                const double gam64 = launch_gamma64(a);
-                const int lane = threadIdx.x & 31;
-                const int wbase = threadIdx.x & ~31;
-                unsigned long long my = uns;
+            // CTA-cooperative: the tile's flagged bins are queued in shared memory and every thread of
+            // the CTA takes a share of each item's taps, so no warp holds the CTA's tile barrier for a
+            // warp-serial sum (rare: a few per hundred frames on C2-C5)
+            unsigned long long my = uns;
 #pragma unroll 1
-                while (true) {
-                    const unsigned ball = __ballot_sync(0xffffffffu, my != 0ull);
-                    if (!ball) break;
-                    const int src = __ffs(ball) - 1;
-                    const int i = __ffsll((long long)__shfl_sync(0xffffffffu, my, src)) - 1;
-                    if (lane == src) my &= my - 1;
-                    const int k = __shfl_sync(0xffffffffu, bin_k(i), src);
-                    const float* xs = xb + pad + ((wbase + src) / N2) * a.hop;
-                    double sr, si, dr, di;
-                    stft_bin_fp64([&](int j) { return xs[j]; }, a.taps64, a.tw64, N, a.L, a.c, k, sr, si, dr, di);
-                    const int ln = decide_fp64(a, gam64, k, sr, si, dr, di);
+            while (__syncthreads_or(my != 0ull)) {
+                if (threadIdx.x == 0) rq_n = 0;
+                __syncthreads();
+                while (my) {
+                    const int i = __ffsll((long long)my) - 1;
+                    const int q = atomicAdd(&rq_n, 1);
+                    if (q >= kRedecideQ) break;                        // queue full: next round
+                    my &= my - 1;
+                    rq[q] = make_int4(bin_k(i), group, i, threadIdx.x);   // (k, frame group, slot, owner)
+                }
+                __syncthreads();
+                const int nq = min(rq_n, kRedecideQ);
+                const double gam64 = launch_gamma64(a);
+#pragma unroll 1
+                for (int q = 0; q < nq; ++q) {
+                    const int4 it = rq[q];
+                    const float* xs = xb + pad + it.y * a.hop;
+                    double v[4];
+                    stft_bin_fp64_cta<TPB>([&](int j) { return xs[j]; }, a.taps64, a.tw64, N, a.L, a.c, it.x, v,
+                                           rq_red);
+                    if (threadIdx.x == 0) rq_res[q] = decide_fp64(a, gam64, it.x, v[0], v[1], v[2], v[3]);
+                }
+                __syncthreads();
+#pragma unroll 1
+                for (int q = 0; q < nq; ++q) {
+                    const int4 it = rq[q];
+                    if (it.w != (int)threadIdx.x) continue;
+                    const int ln = rq_res[q];
 #pragma unroll
                     for (int ii = 0; ii < NB; ++ii)
-                        if (lane == src && ii == i) bl[ii] = ln;
+                        if (ii == it.z) bl[ii] = ln;
                 }
             }
             if constexpr (MODE == kModeTargets) {

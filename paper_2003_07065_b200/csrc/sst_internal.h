@@ -54,6 +54,8 @@ __host__ __device__ inline InvLayout inv_layout(int n2, int L, int H, int zoom) 
     return v;
 }
 
+constexpr int kRedecideQ = 64;     // R23 queue slots per CTA round (forward kernel)
+
 struct FwdArgs {
     const float* x;          // points at global sample x_off
     int64_t x_off, x_len;
