@@ -119,31 +119,33 @@ __device__ __forceinline__ void stft_bin_fp64(XF xat, const double2* __restrict_
     }
 }
 
-// The same sum with all TPB threads of a CTA (tap j = thread + TPB t; the per-tap twiddle
-// W^{TPB k t} is uniform, the thread factor W^{k (thread - c)} applied once), reduced over the warps
-// in a fixed order through `red` (TPB/32 double4).  Every thread must call it; v = (Re S, Im S,
-// Re S', Im S') on thread 0 (deterministic).  Ends with a __syncthreads (red reusable).
+// The same sum with all TPB threads of a CTA (tap j = thread + TPB t; W^{k (j - c)} =
+// W^{k (thread - c)} W^{TPB k t}: the thread factor is one table load, the CTA-uniform per-tap factor
+// is generated by the recurrence w <- w W^{TPB k} -- at most L/TPB <= 64 steps of fp64 complex
+// products, ~1e-14 relative), reduced over the warps in a fixed order through `red` (TPB/32 double4).
+// taps64 may point to shared or global memory.  Every thread must call it; v = (Re S, Im S, Re S',
+// Im S') on thread 0 (deterministic).  Ends with a __syncthreads (red reusable).
 template <int TPB, class XF>
-__device__ __forceinline__ void stft_bin_fp64_cta(XF xat, const double2* __restrict__ taps64,
-                                                  const double2* __restrict__ tw64, int nfft, int L, int c, int k,
-                                                  double (&v)[4], double4* red) {
+__device__ __forceinline__ void stft_bin_fp64_cta(XF xat, const double2* taps64, const double2* __restrict__ tw64,
+                                                  int nfft, int L, int c, int k, double (&v)[4], double4* red) {
     const unsigned msk = (unsigned)nfft - 1u;
-    const unsigned step = ((unsigned)TPB * (unsigned)k) & msk;
+    const double2 st = __ldg(tw64 + (((unsigned)TPB * (unsigned)k) & msk));
+    const double2 f = __ldg(tw64 + (((unsigned)k * (unsigned)((int)threadIdx.x - c)) & msk));
     double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
-    unsigned e = 0;
+    double wr = 1.0, wi = 0.0;
 #pragma unroll 4
     for (int j = threadIdx.x; j < L; j += TPB) {
         const double xv = (double)xat(j);
-        const double2 w = __ldg(taps64 + j);
-        const double2 t = __ldg(tw64 + e);                                   // W^{TPB k t}: CTA-uniform
+        const double2 w = taps64[j];
         const double p = xv * w.x, q = xv * w.y;
-        ar = fma(p, t.x, ar);
-        ai = fma(p, t.y, ai);
-        br = fma(q, t.x, br);
-        bi = fma(q, t.y, bi);
-        e = (e + step) & msk;
+        ar = fma(p, wr, ar);
+        ai = fma(p, wi, ai);
+        br = fma(q, wr, br);
+        bi = fma(q, wi, bi);
+        const double nr = fma(wr, st.x, -wi * st.y);
+        wi = fma(wr, st.y, wi * st.x);
+        wr = nr;
     }
-    const double2 f = __ldg(tw64 + (((unsigned)k * (unsigned)((int)threadIdx.x - c)) & msk));
     double s0 = ar * f.x - ai * f.y, s1 = ar * f.y + ai * f.x;
     double s2 = br * f.x - bi * f.y, s3 = br * f.y + bi * f.x;
 #pragma unroll

@@ -94,6 +94,15 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
     float vmax = 0.0f;
 
     for (int i = threadIdx.x; i < a.L; i += TPB) taps_s[i] = __ldg(a.taps + i);
+    // fp64 taps of the R23 re-decision: shared memory when the layout has room, else global (L2)
+    const double2* taps64 = a.taps64;
+    if constexpr (KEEPL) {
+        if (a.lay.t64_off >= 0) {
+            double2* t64s = reinterpret_cast<double2*>(smem_raw + a.lay.t64_off);
+            for (int i = threadIdx.x; i < a.L; i += TPB) t64s[i] = __ldg(a.taps64 + i);
+            taps64 = t64s;
+        }
+    }
     if (threadIdx.x == 0) {
         mbar_init(&mbar[0], 1);
         mbar_init(&mbar[1], 1);
@@ -365,7 +374,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                     const int4 it = rq[q];
                     const float* xs = xb + pad + it.y * a.hop;
                     double v[4];
-                    stft_bin_fp64_cta<TPB>([&](int j) { return xs[j]; }, a.taps64, a.tw64, N, a.L, a.c, it.x, v,
+                    stft_bin_fp64_cta<TPB>([&](int j) { return xs[j]; }, taps64, a.tw64, N, a.L, a.c, it.x, v,
                                            rq_red);
                     if (threadIdx.x == 0) rq_res[q] = decide_fp64(a, gam64, it.x, v[0], v[1], v[2], v[3]);
                 }

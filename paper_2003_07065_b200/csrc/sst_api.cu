@@ -155,8 +155,7 @@ sst_status validate(const sst_params* p, sst_layout* lay, std::string& msg) {
         // shared-memory footprint of the forward / inverse CTAs (227 KB per CTA on sm_100)
         constexpr int kMaxSmem = 227 * 1024;
         const int n2 = p->nfft / 64;
-        constexpr int kFwdStatic = 2048;   // the forward's static shared memory (R23 queue, reductions)
-        if (p->hop <= L && p->nfft <= sst::kMaxFusedNfft && (sst::fwd_layout(n2, L, p->hop).total > kMaxSmem - kFwdStatic ||
+        if (p->hop <= L && p->nfft <= sst::kMaxFusedNfft && (sst::fwd_layout(n2, L, p->hop).total > kMaxSmem - sst::kFwdStaticSmem ||
                             sst::inv_layout(n2, L, p->hop, p->zoom).total > kMaxSmem ||
                             sst::inv_layout(n2, L, p->hop, 1).total > kMaxSmem)) {   // z = 1: sst_istft
             msg = "window / hop too large for this build's shared-memory tiles (227 KB per CTA)";
