@@ -119,22 +119,24 @@ __device__ __forceinline__ void stft_bin_fp64(XF xat, const double2* __restrict_
     }
 }
 
-// The same sum with all TPB threads of a CTA (tap j = thread + TPB t; W^{k (j - c)} =
-// W^{k (thread - c)} W^{TPB k t}: the thread factor is one table load, the CTA-uniform per-tap factor
-// is generated by the recurrence w <- w W^{TPB k} -- at most L/TPB <= 64 steps of fp64 complex
-// products, ~1e-14 relative), reduced over the warps in a fixed order through `red` (TPB/32 double4).
-// taps64 may point to shared or global memory.  Every thread must call it; v = (Re S, Im S, Re S',
-// Im S') on thread 0 (deterministic).  Ends with a __syncthreads (red reusable).
-template <int TPB, class XF>
-__device__ __forceinline__ void stft_bin_fp64_cta(XF xat, const double2* taps64, const double2* __restrict__ tw64,
-                                                  int nfft, int L, int c, int k, double (&v)[4], double4* red) {
+// One part of the same sum: virtual warp `part` of `parts` (a fixed decomposition of the taps, so
+// the fp64 result does not depend on how many real warps share the work): lane l takes taps
+// j = 32 part + l + 32 parts t, so W^{k (j - c)} = W^{k (32 part + l - c)} W^{32 parts k t}: one
+// table load per thread and a uniform per-tap factor generated by the recurrence w <- w W^{32 parts k}
+// (<= L / (32 parts) steps of fp64 complex products, ~1e-14 relative).  taps64 may be in shared or
+// global memory.  Returns the part's sums (Re S, Im S, Re S', Im S') on every lane (fixed xor tree).
+template <class XF>
+__device__ __forceinline__ double4 stft_bin_fp64_part(XF xat, const double2* taps64, const double2* __restrict__ tw64,
+                                                      int nfft, int L, int c, int k, int part, int parts) {
+    const int lane = threadIdx.x & 31;
     const unsigned msk = (unsigned)nfft - 1u;
-    const double2 st = __ldg(tw64 + (((unsigned)TPB * (unsigned)k) & msk));
-    const double2 f = __ldg(tw64 + (((unsigned)k * (unsigned)((int)threadIdx.x - c)) & msk));
+    const int j0 = 32 * part + lane, stride = 32 * parts;
+    const double2 st = __ldg(tw64 + (((unsigned)stride * (unsigned)k) & msk));
+    const double2 f = __ldg(tw64 + (((unsigned)k * (unsigned)(j0 - c)) & msk));
     double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
     double wr = 1.0, wi = 0.0;
 #pragma unroll 4
-    for (int j = threadIdx.x; j < L; j += TPB) {
+    for (int j = j0; j < L; j += stride) {
         const double xv = (double)xat(j);
         const double2 w = taps64[j];
         const double p = xv * w.x, q = xv * w.y;
@@ -155,17 +157,7 @@ __device__ __forceinline__ void stft_bin_fp64_cta(XF xat, const double2* taps64,
         s2 += __shfl_xor_sync(0xffffffffu, s2, o);
         s3 += __shfl_xor_sync(0xffffffffu, s3, o);
     }
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_double4(s0, s1, s2, s3);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        v[0] = v[1] = v[2] = v[3] = 0.0;
-#pragma unroll
-        for (int w = 0; w < TPB / 32; ++w) {
-            const double4 r = red[w];
-            v[0] += r.x; v[1] += r.y; v[2] += r.z; v[3] += r.w;
-        }
-    }
-    __syncthreads();
+    return make_double4(s0, s1, s2, s3);
 }
 
 // The oracle's decision (Eq. 13, 36, 28; R8, R10) in fp64 on the fp64 S, S'.
@@ -173,7 +165,7 @@ __device__ __forceinline__ int decide_fp64(const FwdArgs& a, double gamma, int k
                                            double di) {
     if (!(k >= a.src_lo && k < a.src_hi)) return -1;
     const double mag = sr * sr + si * si;
-    if (!(sqrt(mag) > gamma)) return -1;                                     // |S| > gamma (Eq. 13)
+    if (!(mag > gamma * gamma)) return -1;                                   // |S| > gamma (Eq. 13)
     const double im = di * sr - dr * si;                                     // Im(S' conj S)
     const double r = -im / mag * ((double)a.nfft / 6.283185307179586476925);   // Eq. 36
     const double fh = fabs((double)k + r);                                   // Eq. 13 (R8)

@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
     __shared__ float wnrm[TPB / 32];               // per-warp ||z_m||^2 partials (groups of > 1 warp)
     __shared__ int4 rq[KEEPL ? kRedecideQ : 1];    // R23 queue: (k, frame group, register slot, owner thread)
     __shared__ int rq_res[KEEPL ? kRedecideQ : 1]; // R23 fp64 decisions
-    __shared__ double4 rq_red[TPB / 32];           // R23 per-warp partial sums
+    __shared__ double4 rq_red[KEEPL ? (TPB / 32) * (TPB / 32) : 1];   // R23 partial sums [item][part]
     __shared__ int rq_n;
     float2* smem = reinterpret_cast<float2*>(smem_raw);
     float2* taps_s = reinterpret_cast<float2*>(smem_raw + a.lay.taps_off);
@@ -369,16 +369,41 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                 __syncthreads();
                 const int nq = min(rq_n, kRedecideQ);
                 const double gam64 = launch_gamma64(a);
+                // the queue in passes of `per` items, `parts` warps per item (all warps busy, two barriers
+                // per pass): many items -> one warp each; one item -> every warp of the CTA.  Each item's
+                // taps are always split into W fixed virtual parts summed in a fixed order, whatever
+                // `parts` is: bitwise reproducible
+                constexpr int W = TPB / 32;
+                int parts = W;
+                while (parts > 1 && parts * nq > W) parts >>= 1;
+                const int per = W / parts;
+                const int warp = threadIdx.x >> 5;
 #pragma unroll 1
-                for (int q = 0; q < nq; ++q) {
-                    const int4 it = rq[q];
-                    const float* xs = xb + pad + it.y * a.hop;
-                    double v[4];
-                    stft_bin_fp64_cta<TPB>([&](int j) { return xs[j]; }, taps64, a.tw64, N, a.L, a.c, it.x, v,
-                                           rq_red);
-                    if (threadIdx.x == 0) rq_res[q] = decide_fp64(a, gam64, it.x, v[0], v[1], v[2], v[3]);
+                for (int q0 = 0; q0 < nq; q0 += per) {
+                    const int q = q0 + warp / parts;
+                    if (q < nq) {
+                        const int4 it = rq[q];
+                        const float* xs = xb + pad + it.y * a.hop;
+#pragma unroll 1
+                        for (int vp = warp % parts; vp < W; vp += parts) {
+                            const double4 r = stft_bin_fp64_part([&](int j) { return xs[j]; }, taps64, a.tw64, N,
+                                                                 a.L, a.c, it.x, vp, W);
+                            if ((threadIdx.x & 31) == 0) rq_red[(warp / parts) * W + vp] = r;
+                        }
+                    }
+                    __syncthreads();
+                    if (threadIdx.x < per && q0 + (int)threadIdx.x < nq) {
+                        const int qq = q0 + threadIdx.x;
+                        double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+#pragma unroll
+                        for (int w = 0; w < W; ++w) {
+                            const double4 r = rq_red[threadIdx.x * W + w];
+                            v0 += r.x; v1 += r.y; v2 += r.z; v3 += r.w;
+                        }
+                        rq_res[qq] = decide_fp64(a, gam64, rq[qq].x, v0, v1, v2, v3);
+                    }
+                    __syncthreads();
                 }
-                __syncthreads();
 #pragma unroll 1
                 for (int q = 0; q < nq; ++q) {
                     const int4 it = rq[q];

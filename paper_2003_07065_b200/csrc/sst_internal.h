@@ -23,7 +23,7 @@ __host__ __device__ constexpr int round_up(int v, int m) { return (v + m - 1) / 
 
 // forward dynamic shared memory: [G exchange buffers][taps L float2][2 input tiles][2 mbarriers]
 // [fp64 taps L double2, when they fit without costing a resident CTA (R23 re-decision)]
-constexpr int kFwdStaticSmem = 2048;   // the forward's static shared memory (R23 queue, reductions), bound
+constexpr int kFwdStaticSmem = 4096;   // the forward's static shared memory (R23 queue, reductions), bound
 struct FwdLayout {
     int taps_off, xb_off, mbar_off, xcap, t64_off, total;
 };
@@ -35,9 +35,11 @@ __host__ __device__ inline FwdLayout fwd_layout(int n2, int L, int H) {
     f.xcap = round_up((G - 1) * H + L + 8, 4);          // floats per input tile buffer
     f.mbar_off = f.xb_off + 2 * f.xcap * 4;
     f.total = f.mbar_off + 16;
+    // (only while the SM's shared-memory carveout stays at or below 196 KB: a larger one shrinks L1,
+    // which the twiddle loads use -- measured 8 % slower on C3)
     const int ctas = tpb_of(n2, true) == 256 ? 1 : 2;   // resident CTAs per SM (launch bounds)
     const int with = round_up(f.total, 16) + L * 16;
-    if ((with + kFwdStaticSmem + 1024) * ctas <= 228 * 1024) {
+    if ((with + kFwdStaticSmem + 1024) * ctas <= 196 * 1024) {
         f.t64_off = round_up(f.total, 16);
         f.total = with;
     } else {
