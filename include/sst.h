@@ -151,6 +151,10 @@ sst_status sst_plan_set_gamma(sst_plan* plan, double gamma_abs);
 /* RELATIVE mode: take max|S| from this device float (e.g. all-reduced over ranks) instead of
  * computing it per call; NULL restores per-call computation.  Not owned by the plan.        */
 sst_status sst_plan_set_absmax(sst_plan* plan, const float* absmax_device);
+/* R23 counters since plan creation (sst_forward / sst_targets): out[0] = source bins whose fp32
+ * decision was re-taken in fp64 (direct Eq. 8 sum), out[1] = of those, bins whose target changed.
+ * HOST uint64_t[2].  Synchronous (waits for the device).                                    */
+sst_status sst_plan_counters(sst_plan* plan, uint64_t* out);
 void sst_plan_destroy(sst_plan* plan);
 
 /* ---------------------------------------------------------------- forward ------------------ */

@@ -82,6 +82,7 @@ SIGNATURES = {
     "sst_plan_set_gamma": (_i32, [_vp, _dbl]),
     "sst_plan_set_absmax": (_i32, [_vp, _vp]),
     "sst_plan_destroy": (None, [_vp]),
+    "sst_plan_counters": (_i32, [_vp, ctypes.POINTER(ctypes.c_uint64)]),
     "sst_forward": (_i32, [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp]),
     "sst_inverse": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "sst_inverse_accumulate": (_i32, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp]),

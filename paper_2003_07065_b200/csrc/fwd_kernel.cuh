@@ -369,6 +369,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                 __syncthreads();
                 const int nq = min(rq_n, kRedecideQ);
                 const double gam64 = launch_gamma64(a);
+                if (threadIdx.x == 0) atomicAdd(a.r23_count, (unsigned long long)nq);
                 // the queue in passes of `per` items, `parts` warps per item (all warps busy, two barriers
                 // per pass): many items -> one warp each; one item -> every warp of the CTA.  Each item's
                 // taps are always split into W fixed virtual parts summed in a fixed order, whatever
@@ -411,7 +412,10 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                     const int ln = rq_res[q];
 #pragma unroll
                     for (int ii = 0; ii < NB; ++ii)
-                        if (ii == it.z) bl[ii] = ln;
+                        if (ii == it.z) {
+                            if (bl[ii] != ln) atomicAdd(a.r23_count + 1, 1ull);
+                            bl[ii] = ln;
+                        }
                 }
             }
             if constexpr (MODE == kModeTargets) {

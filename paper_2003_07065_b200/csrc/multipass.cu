@@ -291,7 +291,10 @@ __global__ void __launch_bounds__(kBinThreads) mp_bins_kernel(const FwdArgs a, c
                     stft_bin_fp64(xat, a.taps64, a.tw64, N, a.L, a.c, k, sr, si, dr, di);
                     const int ln = decide_fp64(a, gam64, k, sr, si, dr, di);
                     __syncwarp();
-                    if (lane == 0) lrow[k] = ln;
+                    if (lane == 0) {
+                        lrow[k] = ln;
+                        atomicAdd(a.r23_count, 1ull);
+                    }
                 }
             }
         }

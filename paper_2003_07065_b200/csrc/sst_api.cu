@@ -35,6 +35,7 @@ struct sst_plan {
     double2* d_taps64 = nullptr;    // [L]  (g, g') fp64 (R23 re-decision)
     double2* d_tw64 = nullptr;      // [N_f] exp(-2 pi i e/N_f) fp64
     int32_t* d_mpl = nullptr;       // multi-pass: [mp_fwd_frames][N_f/2 + 1] targets
+    unsigned long long* d_r23 = nullptr;   // [2] R23 counters (sst_plan_counters)
     float2* d_phz = nullptr;        // [z][64 + 2 N_f/64]
     double* d_renyi = nullptr;      // [kRenyiBlocks][2] partial sums
     unsigned long long* d_amax2 = nullptr;   // ridge emission: max |T| (double bits)
@@ -63,7 +64,7 @@ struct sst_plan {
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(device);
-        for (void* q : {(void*)d_taps, (void*)d_tw, (void*)d_taps64, (void*)d_tw64, (void*)d_mpl, (void*)d_phz, (void*)d_renyi, (void*)d_amax2, (void*)d_back, (void*)d_inv_head, (void*)d_inv_tail,
+        for (void* q : {(void*)d_taps, (void*)d_tw, (void*)d_taps64, (void*)d_tw64, (void*)d_mpl, (void*)d_r23, (void*)d_phz, (void*)d_renyi, (void*)d_amax2, (void*)d_back, (void*)d_inv_head, (void*)d_inv_tail,
                         (void*)d_inv_per, (void*)d_absmax, (void*)d_seam, (void*)d_twN, (void*)d_mp0, (void*)d_mp1, (void*)d_wf})
             if (q) cudaFree(q);
         cudaSetDevice(prev);
@@ -310,6 +311,7 @@ sst::FwdArgs fwd_args(const sst_plan* pl, const float* x, int64_t x_off, int64_t
     a.taps64 = pl->d_taps64;
     a.tw64 = pl->d_tw64;
     a.lscratch = pl->d_mpl;
+    a.r23_count = pl->d_r23;
     a.lay = sst::fwd_layout(pl->lay.nfft / 64, pl->lay.win_len, pl->lay.hop);
     return a;
 }
@@ -527,6 +529,9 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
     }
     cudaError_t ce = cudaMalloc((void**)&pl->d_absmax, sizeof(float));
     if (ce != cudaSuccess) { delete pl; cudaGetLastError(); return fail(nullptr, SST_E_OUT_OF_MEMORY, "cudaMalloc absmax"); }
+    ce = cudaMalloc((void**)&pl->d_r23, 2 * sizeof(unsigned long long));
+    if (ce == cudaSuccess) ce = cudaMemset(pl->d_r23, 0, 2 * sizeof(unsigned long long));
+    if (ce != cudaSuccess) { delete pl; cudaGetLastError(); return fail(nullptr, SST_E_OUT_OF_MEMORY, "cudaMalloc counters"); }
     if (Nf > sst::kMaxFusedNfft) {
         // multi-pass path: W_N table and scratch for a bounded chunk of frames (kMpScratch per buffer)
         pl->mp = true;
@@ -600,6 +605,16 @@ sst_status sst_plan_set_absmax(sst_plan* plan, const float* absmax_device) {
     if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
     plan->ext_absmax = absmax_device;
     return SST_OK;
+}
+
+sst_status sst_plan_counters(sst_plan* plan, uint64_t* out) {
+    if (!plan || !out) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL plan or out");
+    DeviceGuard guard(plan->device);
+    unsigned long long h[2] = {0, 0};
+    sst_status s = cuda_status(plan, cudaMemcpy(h, plan->d_r23, sizeof h, cudaMemcpyDeviceToHost), "counters");
+    out[0] = h[0];
+    out[1] = h[1];
+    return s;
 }
 
 void sst_plan_destroy(sst_plan* plan) { delete plan; }

@@ -94,6 +94,7 @@ struct FwdArgs {
     const double2* taps64;   // [L] (g, g') fp64
     const double2* tw64;     // [nfft] exp(-2 pi i e / N_f) fp64
     int32_t* lscratch;       // multi-pass: [frames][N_f/2 + 1] targets of the chunk
+    unsigned long long* r23_count;   // [2]: bins re-decided, of which the fp64 target differed
     FwdLayout lay;
     // outputs
     float2* T; int64_t ldT;

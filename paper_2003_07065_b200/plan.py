@@ -149,6 +149,12 @@ class Plan:
         self._absmax_ref = t
         L.check(L.sst_plan_set_absmax(self._h, ptr), self._h)
 
+    def counters(self) -> dict:
+        """sst_plan_counters: R23 fp64 re-decisions so far (synchronous)."""
+        out = (ctypes.c_uint64 * 2)()
+        L.check(L.sst_plan_counters(self._h, out), self._h)
+        return {"redecided": int(out[0]), "changed": int(out[1])}
+
     # ------------------------------------------------------------------ forward
     def forward(self, x: torch.Tensor, frame_begin: int = 0, frame_end: int | None = None,
                 x_off: int = 0, out: torch.Tensor | None = None) -> torch.Tensor:

@@ -38,5 +38,8 @@ for _ in range(iters):
     torch.cuda.synchronize()
     tf += a.elapsed_time(b)
     ti += b.elapsed_time(c)
+cnt = plan.counters()
+calls = iters + 2
 print(f"{os.environ.get('SST_LIB_PATH', 'libsst.so')} {name} N={cfg.N}: fwd {tf/iters:.3f} ms  inv {ti/iters:.3f} ms  "
-      f"-> {cfg.N / ((tf + ti) / iters * 1e-3) / 1e6:.1f} MS/s")
+      f"-> {cfg.N / ((tf + ti) / iters * 1e-3) / 1e6:.1f} MS/s; R23 re-decided {cnt['redecided'] / calls / plan.frames:.4f}"
+      f"/frame, changed {cnt['changed'] / calls / plan.frames:.2e}/frame")
