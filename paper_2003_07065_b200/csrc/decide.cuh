@@ -123,10 +123,10 @@ __device__ __forceinline__ void stft_bin_fp64(XF xat, const double2* __restrict_
 // the fp64 result does not depend on how many real warps share the work): lane l takes taps
 // j = 32 part + l + 32 parts t, so W^{k (j - c)} = W^{k (32 part + l - c)} W^{32 parts k t}: one
 // table load per thread and a uniform per-tap factor generated by the recurrence w <- w W^{32 parts k}
-// (<= L / (32 parts) steps of fp64 complex products, ~1e-14 relative).  taps64 may be in shared or
-// global memory.  Returns the part's sums (Re S, Im S, Re S', Im S') on every lane (fixed xor tree).
-template <class XF>
-__device__ __forceinline__ double4 stft_bin_fp64_part(XF xat, const double2* taps64, const double2* __restrict__ tw64,
+// (<= L / (32 parts) steps of fp64 complex products, ~1e-14 relative).  tap64(j) returns (g[j], g'[j])
+// in fp64.  Returns the part's sums (Re S, Im S, Re S', Im S') on every lane (fixed xor tree).
+template <class XF, class TF>
+__device__ __forceinline__ double4 stft_bin_fp64_part(XF xat, TF tap64, const double2* __restrict__ tw64,
                                                       int nfft, int L, int c, int k, int part, int parts) {
     const int lane = threadIdx.x & 31;
     const unsigned msk = (unsigned)nfft - 1u;
@@ -138,7 +138,7 @@ __device__ __forceinline__ double4 stft_bin_fp64_part(XF xat, const double2* tap
 #pragma unroll 4
     for (int j = j0; j < L; j += stride) {
         const double xv = (double)xat(j);
-        const double2 w = taps64[j];
+        const double2 w = tap64(j);
         const double p = xv * w.x, q = xv * w.y;
         ar = fma(p, wr, ar);
         ai = fma(p, wi, ai);

@@ -94,15 +94,22 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
     float vmax = 0.0f;
 
     for (int i = threadIdx.x; i < a.L; i += TPB) taps_s[i] = __ldg(a.taps + i);
-    // fp64 taps of the R23 re-decision: shared memory when the layout has room, else global (L2)
-    const double2* taps64 = a.taps64;
+    // fp64 taps of the R23 re-decision: the resident fp32 taps plus fp32 corrections in shared memory
+    // when the layout has room (exact to fp64 rounding), else the fp64 table in global memory
+    float2* tapc_s = nullptr;
     if constexpr (KEEPL) {
         if (a.lay.t64_off >= 0) {
-            double2* t64s = reinterpret_cast<double2*>(smem_raw + a.lay.t64_off);
-            for (int i = threadIdx.x; i < a.L; i += TPB) t64s[i] = __ldg(a.taps64 + i);
-            taps64 = t64s;
+            tapc_s = reinterpret_cast<float2*>(smem_raw + a.lay.t64_off);
+            for (int i = threadIdx.x; i < a.L; i += TPB) tapc_s[i] = __ldg(a.tapc + i);
         }
     }
+    auto tap64 = [&](int j) -> double2 {
+        if (tapc_s) {
+            const float2 t = taps_s[j], e = tapc_s[j];
+            return make_double2((double)t.x + (double)e.x, fma((double)t.y, a.inv_alpha_d, (double)e.y));
+        }
+        return __ldg(a.taps64 + j);
+    };
     if (threadIdx.x == 0) {
         mbar_init(&mbar[0], 1);
         mbar_init(&mbar[1], 1);
@@ -387,7 +394,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                         const float* xs = xb + pad + it.y * a.hop;
 #pragma unroll 1
                         for (int vp = warp % parts; vp < W; vp += parts) {
-                            const double4 r = stft_bin_fp64_part([&](int j) { return xs[j]; }, taps64, a.tw64, N,
+                            const double4 r = stft_bin_fp64_part([&](int j) { return xs[j]; }, tap64, a.tw64, N,
                                                                  a.L, a.c, it.x, vp, W);
                             if ((threadIdx.x & 31) == 0) rq_red[(warp / parts) * W + vp] = r;
                         }
@@ -505,7 +512,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                             t = make_float2(limbs_to_float(a0[i], a0[CH + i], iscale),
                                             limbs_to_float(a0[2 * CH + i], a0[3 * CH + i], iscale));
                         }
-                        trow[l0 + i] = t;
+                        __stcs(trow + l0 + i, t);           // streaming: T is written once, read by the inverse later
                     }
                 group_sync<N2>(group);
             }
