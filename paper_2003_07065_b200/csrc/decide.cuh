@@ -56,12 +56,17 @@ __device__ __forceinline__ int bin_target(const FwdArgs& a, float gam4, float cm
     const int lin = ((unsigned)l < (unsigned)a.bins && fin) ? l : -2;
     // R23 margin of the fine position: z delta r = cm (1/|2S| + (|U|+|V|)/|2S|^2) (R21 error model);
     // only targets in [-1, B] can cross into / inside the band (margins of coefficients the north
-    // star's location clause covers, |S| >= 1e-2 max|S|, stay far below half a bin)
-    const float rs = rsqrtf(mag4);
-    const float mg = cm * fmaf(fabsf(UV.x) + fabsf(UV.y), rsq, rs);
-    const float fr = t - fl;
-    const bool near_l = fabsf(fr - 0.5f) > 0.5f - mg && (unsigned)(l + 1) <= (unsigned)a.bins + 1u;
-    unsure = src && ((keep && near_l) || fabsf(mag4 - gam4) < km);
+    // star's location clause covers, |S| >= 1e-2 max|S|, stay far below half a bin).  Evaluated only
+    // when some lane of the warp has such a target (warp-uniform skip: most source bins of a narrow
+    // band's plane land far outside it).
+    const bool cand = src && (unsigned)(l + 1) <= (unsigned)a.bins + 1u && fin;
+    unsure = false;
+    if (__any_sync(__activemask(), cand)) {
+        const float rs = rsqrtf(mag4);
+        const float mg = cm * fmaf(fabsf(UV.x) + fabsf(UV.y), rsq, rs);
+        const float fr = t - fl;
+        unsure = cand && ((keep && fabsf(fr - 0.5f) > 0.5f - mg) || fabsf(mag4 - gam4) < km);
+    }
     return keep ? lin : -1;
 }
 

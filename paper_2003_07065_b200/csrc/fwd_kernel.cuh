@@ -32,12 +32,11 @@ struct TileIn {
     bool bulk;
 };
 
-template <int G>
-__device__ __forceinline__ TileIn tile_in(const FwdArgs& a, int64_t t, bool x_aligned) {
+// frames [f, f + g) (global indices) of one tile
+__device__ __forceinline__ TileIn tile_in(const FwdArgs& a, int64_t f, int g, bool x_aligned) {
     TileIn ti;
-    const int64_t f = a.frame_begin + t * G;
     ti.s_lo = f * a.hop - a.c;
-    const int64_t s_hi = (f + G - 1) * a.hop - a.c + a.L;
+    const int64_t s_hi = (f + g - 1) * a.hop - a.c + a.L;
     const int64_t v_lo = a.x_off > 0 ? a.x_off : 0;
     const int64_t v_hi = min(a.n, a.x_off + a.x_len);
     const int64_t d0 = ti.s_lo - a.x_off;
@@ -85,7 +84,11 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
     }
 
     const int64_t nfr = a.frame_end - a.frame_begin;
-    const int64_t ntiles = (nfr + G - 1) / G;
+    // list mode (R23 repair): tile t is the single frame flist[t] (group 0), inline re-decision
+    const bool lmode = a.flist != nullptr;
+    const int64_t ntiles = lmode ? (int64_t)*a.flist_n : (nfr + G - 1) / G;
+    auto tile_first = [&](int64_t t) -> int64_t { return lmode ? (int64_t)__ldg(a.flist + t) : t * G; };
+    const int tile_g = lmode ? 1 : G;
     const int64_t tiles_per_cta = (ntiles + gridDim.x - 1) / gridDim.x;
     const int64_t t_begin = (int64_t)blockIdx.x * tiles_per_cta;
     const int64_t t_end = min(ntiles, t_begin + tiles_per_cta);
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
     }
     __syncthreads();
     if (threadIdx.x == 0 && t_begin < t_end) {
-        const TileIn ti = tile_in<G>(a, t_begin, x_aligned);
+        const TileIn ti = tile_in(a, a.frame_begin + tile_first(t_begin), tile_g, x_aligned);
         if (ti.bulk) {
             mbar_arrive_tx(&mbar[0], ti.bytes);
             bulk_g2s(xbuf, a.x + ti.a_lo, ti.bytes, &mbar[0]);
@@ -130,14 +133,15 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
         float* xb = xbuf + bsel * a.lay.xcap;
         // prefetch tile + 1 into the other buffer (freed by the barrier that ended tile - 1)
         if (threadIdx.x == 0 && tile + 1 < t_end) {
-            const TileIn tn = tile_in<G>(a, tile + 1, x_aligned);
+            const TileIn tn = tile_in(a, a.frame_begin + tile_first(tile + 1), tile_g, x_aligned);
             if (tn.bulk) {
                 fence_proxy_async();
                 mbar_arrive_tx(&mbar[bsel ^ 1], tn.bytes);
                 bulk_g2s(xbuf + (bsel ^ 1) * a.lay.xcap, a.x + tn.a_lo, tn.bytes, &mbar[bsel ^ 1]);
             }
         }
-        const TileIn ti = tile_in<G>(a, tile, x_aligned);
+        const int64_t f_first = tile_first(tile);    // first frame of the tile within the launch
+        const TileIn ti = tile_in(a, a.frame_begin + f_first, tile_g, x_aligned);
         int pad = ti.pad;
         if (ti.bulk) {
             mbar_wait(&mbar[bsel], (phase >> bsel) & 1);
@@ -145,7 +149,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
         } else {
             const int64_t v_lo = a.x_off > 0 ? a.x_off : 0;
             const int64_t v_hi = min(a.n, a.x_off + a.x_len);
-            const int span = (G - 1) * a.hop + a.L;
+            const int span = (tile_g - 1) * a.hop + a.L;
             for (int i = threadIdx.x; i < span; i += TPB) {
                 const int64_t s = ti.s_lo + i;
                 xb[i] = (s >= v_lo && s < v_hi) ? __ldg(a.x + (s - a.x_off)) : 0.0f;
@@ -154,7 +158,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
             __syncthreads();
         }
 
-        const int64_t fi = tile * G + group;       // frame index within the launch
+        const int64_t fi = lmode ? (group == 0 ? f_first : nfr) : f_first + group;   // frame within the launch
         const bool valid = fi < nfr;
         const float* xw = xb + pad + group * a.hop; // x[m H - c + j], j = 0..L-1 (j = tau + c)
 
@@ -362,6 +366,18 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
             // the CTA takes a share of each item's taps, so no warp holds the CTA's tile barrier for a
             // warp-serial sum (rare: a few per hundred frames on C2-C5)
             unsigned long long my = uns;
+            if (a.gq && my) {
+                // deferred (the common path): squeeze at the fp32 target now, queue for redecide_kernel
+#pragma unroll
+                for (int ii = 0; ii < NB; ++ii)
+                    if ((my >> ii) & 1ull) {
+                        const unsigned q = atomicAdd(a.gq_n, 1u);
+                        if (q < a.gq_cap) {
+                            a.gq[q] = make_int4((int)fi, bin_k(ii), bl[ii], 0);
+                            my &= ~(1ull << ii);
+                        }
+                    }
+            }
 #pragma unroll 1
             while (__syncthreads_or(my != 0ull)) {
                 if (threadIdx.x == 0) rq_n = 0;
@@ -376,7 +392,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                 __syncthreads();
                 const int nq = min(rq_n, kRedecideQ);
                 const double gam64 = launch_gamma64(a);
-                if (threadIdx.x == 0) atomicAdd(a.r23_count, (unsigned long long)nq);
+                if (threadIdx.x == 0 && !lmode) atomicAdd(a.r23_count, (unsigned long long)nq);
                 // the queue in passes of `per` items, `parts` warps per item (all warps busy, two barriers
                 // per pass): many items -> one warp each; one item -> every warp of the CTA.  Each item's
                 // taps are always split into W fixed virtual parts summed in a fixed order, whatever
@@ -420,7 +436,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
 #pragma unroll
                     for (int ii = 0; ii < NB; ++ii)
                         if (ii == it.z) {
-                            if (bl[ii] != ln) atomicAdd(a.r23_count + 1, 1ull);
+                            if (bl[ii] != ln && !lmode) atomicAdd(a.r23_count + 1, 1ull);
                             bl[ii] = ln;
                         }
                 }

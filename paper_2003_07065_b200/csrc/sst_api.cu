@@ -37,6 +37,11 @@ struct sst_plan {
     float2* d_tapc = nullptr;       // [L] fp32 corrections of the fp32 taps to fp64
     int32_t* d_mpl = nullptr;       // multi-pass: [mp_fwd_frames][N_f/2 + 1] targets
     unsigned long long* d_r23 = nullptr;   // [2] R23 counters (sst_plan_counters)
+    int4* d_gq = nullptr;           // R23 deferral queue [gq_cap]
+    unsigned int* d_gctr = nullptr; // [2] queue entries, dirty frames
+    unsigned int* d_dirty_bits = nullptr;   // [(F + 31) / 32]
+    int* d_dirty_list = nullptr;    // [gq_cap]
+    unsigned int gq_cap = 0;
     float2* d_phz = nullptr;        // [z][64 + 2 N_f/64]
     double* d_renyi = nullptr;      // [kRenyiBlocks][2] partial sums
     unsigned long long* d_amax2 = nullptr;   // ridge emission: max |T| (double bits)
@@ -65,7 +70,8 @@ struct sst_plan {
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(device);
-        for (void* q : {(void*)d_taps, (void*)d_tw, (void*)d_taps64, (void*)d_tw64, (void*)d_tapc, (void*)d_mpl, (void*)d_r23, (void*)d_phz, (void*)d_renyi, (void*)d_amax2, (void*)d_back, (void*)d_inv_head, (void*)d_inv_tail,
+        for (void* q : {(void*)d_taps, (void*)d_tw, (void*)d_taps64, (void*)d_tw64, (void*)d_tapc, (void*)d_mpl, (void*)d_r23, (void*)d_gq, (void*)d_gctr,
+                        (void*)d_dirty_bits, (void*)d_dirty_list, (void*)d_phz, (void*)d_renyi, (void*)d_amax2, (void*)d_back, (void*)d_inv_head, (void*)d_inv_tail,
                         (void*)d_inv_per, (void*)d_absmax, (void*)d_seam, (void*)d_twN, (void*)d_mp0, (void*)d_mp1, (void*)d_wf})
             if (q) cudaFree(q);
         cudaSetDevice(prev);
@@ -566,6 +572,18 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
         }
     } else {
         pl->fwd_grid = sst::forward_max_grid(Nf, L, H, device);
+        // R23 deferral: a queue of up to 2^20 flagged bins per launch (measured rates: 0.01-1.3 per frame
+        // on C2-C5, ~20 on C1); beyond it the forward re-decides inline
+        pl->gq_cap = 1u << 20;
+        const size_t words = (size_t)((pl->lay.frames + 31) / 32);
+        if (cudaMalloc((void**)&pl->d_gq, sizeof(int4) * pl->gq_cap) != cudaSuccess ||
+            cudaMalloc((void**)&pl->d_gctr, 2 * sizeof(unsigned int)) != cudaSuccess ||
+            cudaMalloc((void**)&pl->d_dirty_bits, sizeof(unsigned int) * words) != cudaSuccess ||
+            cudaMalloc((void**)&pl->d_dirty_list, sizeof(int) * pl->gq_cap) != cudaSuccess) {
+            cudaGetLastError();
+            delete pl;
+            return fail(nullptr, SST_E_OUT_OF_MEMORY, "cudaMalloc R23 queue");
+        }
         pl->inv_grid = sst::inverse_max_grid(Nf, H, L, z, device);
         const int32_t seam_len = std::max(0, L - H);
         if (seam_len > 0) {
@@ -647,7 +665,30 @@ static sst_status run_forward_mode(sst_plan* plan, int mode, const float* x, int
         }
     }
     (void)x; (void)x_off; (void)x_len;
-    return cuda_status(plan, launch_fwd_any(plan, a, mode, st), "forward launch");
+    const int64_t nfr = a.frame_end - a.frame_begin;
+    const bool defer = !plan->mp && a.redecide && plan->d_gq && nfr < (1ll << 31) &&
+                       (mode == sst::kModeForward || mode == sst::kModeTargets);
+    if (!defer) return cuda_status(plan, launch_fwd_any(plan, a, mode, st), "forward launch");
+    // R23 deferred: forward (fp32 decisions, flagged bins queued) -> fp64 re-decisions -> repair of the
+    // rows whose decision changed (forward) / fp64 targets written (targets)
+    sst_status s = cuda_status(plan, cudaMemsetAsync(plan->d_gctr, 0, 2 * sizeof(unsigned int), st), "memset");
+    if (s != SST_OK) return s;
+    if (mode == sst::kModeForward)
+        s = cuda_status(plan, cudaMemsetAsync(plan->d_dirty_bits, 0, sizeof(unsigned int) * (size_t)((nfr + 31) / 32), st),
+                        "memset");
+    if (s != SST_OK) return s;
+    a.gq = plan->d_gq;
+    a.gq_n = plan->d_gctr;
+    a.gq_cap = plan->gq_cap;
+    s = cuda_status(plan, launch_fwd_any(plan, a, mode, st), "forward launch");
+    if (s != SST_OK) return s;
+    s = cuda_status(plan, sst::launch_redecide(a, mode, plan->d_dirty_bits, plan->d_dirty_list, st), "redecide launch");
+    if (s != SST_OK || mode != sst::kModeForward) return s;
+    sst::FwdArgs r = a;
+    r.gq = nullptr;
+    r.flist = plan->d_dirty_list;
+    r.flist_n = plan->d_gctr + 1;
+    return cuda_status(plan, sst::launch_forward(r, mode, plan->fwd_grid, st), "repair launch");
 }
 
 sst_status sst_forward(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len, int64_t frame_begin,

@@ -98,6 +98,14 @@ struct FwdArgs {
     const double2* tw64;     // [nfft] exp(-2 pi i e / N_f) fp64
     int32_t* lscratch;       // multi-pass: [frames][N_f/2 + 1] targets of the chunk
     unsigned long long* r23_count;   // [2]: bins re-decided, of which the fp64 target differed
+    // R23 deferral: flagged bins are squeezed at their fp32 target and queued (frame within the
+    // launch, k, fp32 target); redecide_kernel re-takes them in fp64 and lists the frames whose target
+    // changed; a list-mode launch (flist) recomputes those rows with inline re-decision
+    int4* gq;                        // queue (nullptr: inline re-decision only)
+    unsigned int* gq_n;              // [0] queue entries, [1] dirty frames
+    unsigned int gq_cap;
+    const int* flist;                // list mode: frames (within the launch) to process, one per tile
+    const unsigned int* flist_n;     // list mode: device count
     FwdLayout lay;
     // outputs
     float2* T; int64_t ldT;
@@ -156,6 +164,9 @@ cudaError_t launch_mp_inverse_accumulate(const MpInvArgs& a, cudaStream_t s);
 
 // launchers (return cudaGetLastError())
 cudaError_t launch_forward(const FwdArgs& a, int mode, int grid, cudaStream_t s);
+// R23 deferred re-decisions of the queue a.gq (forward: dirty frames -> dirty_bits / dirty_list /
+// a.gq_n[1]; targets: the fp64 targets written to a.lout)
+cudaError_t launch_redecide(const FwdArgs& a, int mode, unsigned int* dirty_bits, int* dirty_list, cudaStream_t s);
 int forward_max_grid(int nfft, int L, int H, int device);
 
 cudaError_t launch_inverse(const InvArgs& a, int grid, cudaStream_t s);

@@ -69,6 +69,53 @@ __global__ void finalize_kernel(float* y, int64_t y_off, int64_t y_len, InvArgs 
     }
 }
 
+// ------------------------------------------------------------------------------- R23 ---------
+// Deferred fp64 re-decisions (reading R23): one warp per queued bin (frame within the launch, k, fp32
+// target), the direct Eq. 8 sum over the frame's samples in global memory, the oracle's decision in
+// fp64.  Targets mode: the fp64 target is written to a.lout.  Forward mode: a frame whose target
+// changed is listed once (dirty_bits / dirty_list / a.gq_n[1]) for the list-mode repair launch.
+__global__ void __launch_bounds__(256) redecide_kernel(const FwdArgs a, int mode, unsigned int* dirty_bits,
+                                                      int* dirty_list) {
+    const unsigned n = min(*a.gq_n, a.gq_cap);
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const double gam64 = launch_gamma64(a);
+    const int64_t v_lo = a.x_off > 0 ? a.x_off : 0;
+    const int64_t v_hi = min(a.n, a.x_off + a.x_len);
+    const int64_t K = a.nfft / 2 + 1;
+    for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < n; e += nw) {
+        const int4 it = a.gq[e];
+        const int64_t s0 = (a.frame_begin + it.x) * a.hop - a.c;
+        auto xat = [&](int j) -> float {
+            const int64_t sj = s0 + j;
+            return (sj >= v_lo && sj < v_hi) ? __ldg(a.x + (sj - a.x_off)) : 0.0f;
+        };
+        double sr, si, dr, di;
+        stft_bin_fp64(xat, a.taps64, a.tw64, a.nfft, a.L, a.c, it.y, sr, si, dr, di);
+        const int ln = decide_fp64(a, gam64, it.y, sr, si, dr, di);
+        if (lane == 0) {
+            atomicAdd(a.r23_count, 1ull);
+            if (ln != it.z) {
+                atomicAdd(a.r23_count + 1, 1ull);
+                if (mode == kModeTargets) {
+                    a.lout[(int64_t)it.x * K + it.y] = ln;
+                } else {
+                    const unsigned bit = 1u << (it.x & 31);
+                    if (!(atomicOr(dirty_bits + (it.x >> 5), bit) & bit)) dirty_list[atomicAdd(a.gq_n + 1, 1u)] = it.x;
+                }
+            }
+        }
+    }
+}
+
+cudaError_t launch_redecide(const FwdArgs& a, int mode, unsigned int* dirty_bits, int* dirty_list, cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    redecide_kernel<<<sms * 4, 256, 0, s>>>(a, mode, dirty_bits, dirty_list);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------------- Renyi -------
 __global__ void __launch_bounds__(256) renyi_partial_kernel(const float2* T, int64_t rows, int64_t cols,
                                                             int64_t ldT, double alpha, double* partial) {
