@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
     __shared__ int rq_res[KEEPL ? kRedecideQ : 1]; // R23 fp64 decisions
     __shared__ double4 rq_red[KEEPL ? (TPB / 32) * (TPB / 32) : 1];   // R23 partial sums [item][part]
     __shared__ int rq_n;
+    __shared__ unsigned cq_n;                      // R23 deferral: entries this CTA queued
     float2* smem = reinterpret_cast<float2*>(smem_raw);
     float2* taps_s = reinterpret_cast<float2*>(smem_raw + a.lay.taps_off);
     float* xbuf = reinterpret_cast<float*>(smem_raw + a.lay.xb_off);
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
         return __ldg(a.taps64 + j);
     };
     if (threadIdx.x == 0) {
+        cq_n = 0;
         mbar_init(&mbar[0], 1);
         mbar_init(&mbar[1], 1);
         fence_mbar_init();
@@ -367,13 +369,16 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
             // warp-serial sum (rare: a few per hundred frames on C2-C5)
             unsigned long long my = uns;
             if (a.gq && my) {
-                // deferred (the common path): squeeze at the fp32 target now, queue for redecide_kernel
+                // deferred (the common path): squeeze at the fp32 target now, queue for redecide_kernel in
+                // this CTA's region of the queue (shared-memory index: no global atomic on the tile path)
+                const unsigned reg = a.gq_cap / gridDim.x;
+                int4* cq = a.gq + (size_t)blockIdx.x * reg;
 #pragma unroll
                 for (int ii = 0; ii < NB; ++ii)
                     if ((my >> ii) & 1ull) {
-                        const unsigned q = atomicAdd(a.gq_n, 1u);
-                        if (q < a.gq_cap) {
-                            a.gq[q] = make_int4((int)fi, bin_k(ii), bl[ii], 0);
+                        const unsigned q = atomicAdd(&cq_n, 1u);
+                        if (q < reg) {
+                            cq[q] = make_int4((int)fi, bin_k(ii), bl[ii], 0);
                             my &= ~(1ull << ii);
                         }
                     }
@@ -536,6 +541,12 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
         __syncthreads();   // tile input buffer and group buffers free for the next tile
     }
 
+    if constexpr (KEEPL) {
+        if (a.gq) {
+            __syncthreads();
+            if (threadIdx.x == 0) a.gq_counts[blockIdx.x] = min(cq_n, a.gq_cap / gridDim.x);
+        }
+    }
     if constexpr (MODE == kModeAbsmax) {
         // block max of 4|S|^2 -> |S|
 #pragma unroll

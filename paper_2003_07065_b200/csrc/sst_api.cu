@@ -18,6 +18,7 @@
 namespace {
 
 thread_local std::string g_thread_err;
+constexpr int64_t kR23Chunk = 1 << 20;   // frames per deferred R23 launch sequence
 
 constexpr double kPi = 3.14159265358979323846264338327950288;
 
@@ -37,8 +38,8 @@ struct sst_plan {
     float2* d_tapc = nullptr;       // [L] fp32 corrections of the fp32 taps to fp64
     int32_t* d_mpl = nullptr;       // multi-pass: [mp_fwd_frames][N_f/2 + 1] targets
     unsigned long long* d_r23 = nullptr;   // [2] R23 counters (sst_plan_counters)
-    int4* d_gq = nullptr;           // R23 deferral queue [gq_cap]
-    unsigned int* d_gctr = nullptr; // [2] queue entries, dirty frames
+    int4* d_gq = nullptr;           // R23 deferral queue [gq_cap], one region per CTA
+    unsigned int* d_gctr = nullptr; // [1 + fwd_grid]: dirty frames, then each CTA's queued entries
     unsigned int* d_dirty_bits = nullptr;   // [(F + 31) / 32]
     int* d_dirty_list = nullptr;    // [gq_cap]
     unsigned int gq_cap = 0;
@@ -572,12 +573,13 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
         }
     } else {
         pl->fwd_grid = sst::forward_max_grid(Nf, L, H, device);
-        // R23 deferral: a queue of up to 2^20 flagged bins per launch (measured rates: 0.01-1.3 per frame
-        // on C2-C5, ~20 on C1); beyond it the forward re-decides inline
-        pl->gq_cap = 1u << 20;
-        const size_t words = (size_t)((pl->lay.frames + 31) / 32);
+        // R23 deferral: a queue of up to 2^22 flagged bins per chunk of 2^20 frames (measured rates:
+        // 0.01-1.3 per frame on C2-C5, ~20 on C1), split into one region per CTA; a CTA whose region is
+        // full re-decides inline
+        pl->gq_cap = 1u << 22;
+        const size_t words = (size_t)((std::min<int64_t>(pl->lay.frames, kR23Chunk) + 31) / 32);
         if (cudaMalloc((void**)&pl->d_gq, sizeof(int4) * pl->gq_cap) != cudaSuccess ||
-            cudaMalloc((void**)&pl->d_gctr, 2 * sizeof(unsigned int)) != cudaSuccess ||
+            cudaMalloc((void**)&pl->d_gctr, (1 + (size_t)std::max(1, pl->fwd_grid)) * sizeof(unsigned int)) != cudaSuccess ||
             cudaMalloc((void**)&pl->d_dirty_bits, sizeof(unsigned int) * words) != cudaSuccess ||
             cudaMalloc((void**)&pl->d_dirty_list, sizeof(int) * pl->gq_cap) != cudaSuccess) {
             cudaGetLastError();
@@ -666,29 +668,43 @@ static sst_status run_forward_mode(sst_plan* plan, int mode, const float* x, int
     }
     (void)x; (void)x_off; (void)x_len;
     const int64_t nfr = a.frame_end - a.frame_begin;
-    const bool defer = !plan->mp && a.redecide && plan->d_gq && nfr < (1ll << 31) &&
+    const bool defer = !plan->mp && a.redecide && plan->d_gq &&
                        (mode == sst::kModeForward || mode == sst::kModeTargets);
     if (!defer) return cuda_status(plan, launch_fwd_any(plan, a, mode, st), "forward launch");
-    // R23 deferred: forward (fp32 decisions, flagged bins queued) -> fp64 re-decisions -> repair of the
-    // rows whose decision changed (forward) / fp64 targets written (targets)
-    sst_status s = cuda_status(plan, cudaMemsetAsync(plan->d_gctr, 0, 2 * sizeof(unsigned int), st), "memset");
-    if (s != SST_OK) return s;
-    if (mode == sst::kModeForward)
-        s = cuda_status(plan, cudaMemsetAsync(plan->d_dirty_bits, 0, sizeof(unsigned int) * (size_t)((nfr + 31) / 32), st),
-                        "memset");
-    if (s != SST_OK) return s;
-    a.gq = plan->d_gq;
-    a.gq_n = plan->d_gctr;
-    a.gq_cap = plan->gq_cap;
-    s = cuda_status(plan, launch_fwd_any(plan, a, mode, st), "forward launch");
-    if (s != SST_OK) return s;
-    s = cuda_status(plan, sst::launch_redecide(a, mode, plan->d_dirty_bits, plan->d_dirty_list, st), "redecide launch");
-    if (s != SST_OK || mode != sst::kModeForward) return s;
-    sst::FwdArgs r = a;
-    r.gq = nullptr;
-    r.flist = plan->d_dirty_list;
-    r.flist_n = plan->d_gctr + 1;
-    return cuda_status(plan, sst::launch_forward(r, mode, plan->fwd_grid, st), "repair launch");
+    // R23 deferred, per chunk of frames: forward (fp32 decisions, flagged bins queued) -> fp64
+    // re-decisions -> repair of the rows whose decision changed (forward) / fp64 targets (targets)
+    const int64_t K = plan->lay.nfft / 2 + 1;
+    for (int64_t c0 = a.frame_begin; c0 < a.frame_end; c0 += kR23Chunk) {
+        sst::FwdArgs b = a;
+        b.frame_begin = c0;
+        b.frame_end = std::min<int64_t>(a.frame_end, c0 + kR23Chunk);
+        const int64_t off = c0 - a.frame_begin, n = b.frame_end - b.frame_begin;
+        if (b.T) b.T += off * a.ldT;
+        if (b.lout) b.lout += off * K;
+        const int grid = fwd_grid_for(plan, n);
+        sst_status s = cuda_status(plan, cudaMemsetAsync(plan->d_gctr, 0, sizeof(unsigned int), st), "memset");
+        if (s == SST_OK && mode == sst::kModeForward)
+            s = cuda_status(plan, cudaMemsetAsync(plan->d_dirty_bits, 0, sizeof(unsigned int) * (size_t)((n + 31) / 32), st),
+                            "memset");
+        if (s != SST_OK) return s;
+        b.gq = plan->d_gq;
+        b.gq_n = plan->d_gctr;
+        b.gq_counts = plan->d_gctr + 1;
+        b.gq_cap = plan->gq_cap;
+        b.gq_ctas = grid;
+        s = cuda_status(plan, sst::launch_forward(b, mode, grid, st), "forward launch");
+        if (s != SST_OK) return s;
+        s = cuda_status(plan, sst::launch_redecide(b, mode, plan->d_dirty_bits, plan->d_dirty_list, st), "redecide launch");
+        if (s != SST_OK) return s;
+        if (mode != sst::kModeForward) continue;
+        sst::FwdArgs r = b;
+        r.gq = nullptr;
+        r.flist = plan->d_dirty_list;
+        r.flist_n = plan->d_gctr;
+        s = cuda_status(plan, sst::launch_forward(r, mode, plan->fwd_grid, st), "repair launch");
+        if (s != SST_OK) return s;
+    }
+    return SST_OK;
 }
 
 sst_status sst_forward(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len, int64_t frame_begin,

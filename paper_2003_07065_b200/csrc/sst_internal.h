@@ -101,9 +101,12 @@ struct FwdArgs {
     // R23 deferral: flagged bins are squeezed at their fp32 target and queued (frame within the
     // launch, k, fp32 target); redecide_kernel re-takes them in fp64 and lists the frames whose target
     // changed; a list-mode launch (flist) recomputes those rows with inline re-decision
-    int4* gq;                        // queue (nullptr: inline re-decision only)
-    unsigned int* gq_n;              // [0] queue entries, [1] dirty frames
+    int4* gq;                        // queue (nullptr: inline re-decision only): CTA b owns entries
+                                     // [b * (gq_cap / grid), ...), counted in gq_counts[b]
+    unsigned int* gq_counts;         // [grid] entries each CTA queued
+    unsigned int* gq_n;              // [1]: dirty frames (redecide_kernel)
     unsigned int gq_cap;
+    int gq_ctas;                     // grid of the launch that filled the queue (redecide_kernel)
     const int* flist;                // list mode: frames (within the launch) to process, one per tile
     const unsigned int* flist_n;     // list mode: device count
     FwdLayout lay;

@@ -76,15 +76,20 @@ __global__ void finalize_kernel(float* y, int64_t y_off, int64_t y_len, InvArgs 
 // changed is listed once (dirty_bits / dirty_list / a.gq_n[1]) for the list-mode repair launch.
 __global__ void __launch_bounds__(256) redecide_kernel(const FwdArgs a, int mode, unsigned int* dirty_bits,
                                                       int* dirty_list) {
-    const unsigned n = min(*a.gq_n, a.gq_cap);
+    const unsigned reg = a.gq_cap / a.gq_ctas;
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const double gam64 = launch_gamma64(a);
     const int64_t v_lo = a.x_off > 0 ? a.x_off : 0;
     const int64_t v_hi = min(a.n, a.x_off + a.x_len);
     const int64_t K = a.nfft / 2 + 1;
-    for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < n; e += nw) {
-        const int4 it = a.gq[e];
+    // items (CTA region b, entry i) in a grid-stride walk over the concatenated regions
+    int64_t base = 0;
+    for (int b = 0; b < a.gq_ctas; ++b) {
+      const unsigned cnt = __ldg(a.gq_counts + b);
+      for (int64_t e = ((w0 - base) % nw + nw) % nw; e < cnt; e += nw) {
+        const int4 it = a.gq[(size_t)b * reg + e];
         const int64_t s0 = (a.frame_begin + it.x) * a.hop - a.c;
         auto xat = [&](int j) -> float {
             const int64_t sj = s0 + j;
@@ -101,10 +106,12 @@ __global__ void __launch_bounds__(256) redecide_kernel(const FwdArgs a, int mode
                     a.lout[(int64_t)it.x * K + it.y] = ln;
                 } else {
                     const unsigned bit = 1u << (it.x & 31);
-                    if (!(atomicOr(dirty_bits + (it.x >> 5), bit) & bit)) dirty_list[atomicAdd(a.gq_n + 1, 1u)] = it.x;
+                    if (!(atomicOr(dirty_bits + (it.x >> 5), bit) & bit)) dirty_list[atomicAdd(a.gq_n, 1u)] = it.x;
                 }
             }
         }
+      }
+      base += cnt;
     }
 }
 
