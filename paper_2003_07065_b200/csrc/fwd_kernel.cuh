@@ -65,10 +65,6 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
     constexpr bool KEEPL = (MODE == kModeForward || MODE == kModeTargets);   // targets kept in registers
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ float wnrm[TPB / 32];               // per-warp ||z_m||^2 partials (groups of > 1 warp)
-    __shared__ int4 rq[KEEPL ? kRedecideQ : 1];    // R23 queue: (k, frame group, register slot, owner thread)
-    __shared__ int rq_res[KEEPL ? kRedecideQ : 1]; // R23 fp64 decisions
-    __shared__ double4 rq_red[KEEPL ? (TPB / 32) * (TPB / 32) : 1];   // R23 partial sums [item][part]
-    __shared__ int rq_n;
     __shared__ unsigned cq_n;                      // R23 deferral: entries this CTA queued
     float2* smem = reinterpret_cast<float2*>(smem_raw);
     float2* taps_s = reinterpret_cast<float2*>(smem_raw + a.lay.taps_off);
@@ -98,22 +94,6 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
     float vmax = 0.0f;
 
     for (int i = threadIdx.x; i < a.L; i += TPB) taps_s[i] = __ldg(a.taps + i);
-    // fp64 taps of the R23 re-decision: the resident fp32 taps plus fp32 corrections in shared memory
-    // when the layout has room (exact to fp64 rounding), else the fp64 table in global memory
-    float2* tapc_s = nullptr;
-    if constexpr (KEEPL) {
-        if (a.lay.t64_off >= 0) {
-            tapc_s = reinterpret_cast<float2*>(smem_raw + a.lay.t64_off);
-            for (int i = threadIdx.x; i < a.L; i += TPB) tapc_s[i] = __ldg(a.tapc + i);
-        }
-    }
-    auto tap64 = [&](int j) -> double2 {
-        if (tapc_s) {
-            const float2 t = taps_s[j], e = tapc_s[j];
-            return make_double2((double)t.x + (double)e.x, fma((double)t.y, a.inv_alpha_d, (double)e.y));
-        }
-        return __ldg(a.taps64 + j);
-    };
     if (threadIdx.x == 0) {
         cq_n = 0;
         mbar_init(&mbar[0], 1);
@@ -364,83 +344,47 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                     return i < 16 ? j + 64 * (16 * h + i) : ((j == 0) ? 32 : 64 - j) + 64 * (16 * h + i - 16);
                 }
             };
-            // CTA-cooperative: the tile's flagged bins are queued in shared memory and every thread of
-            // the CTA takes a share of each item's taps, so no warp holds the CTA's tile barrier for a
-            // warp-serial sum (rare: a few per hundred frames on C2-C5)
+            // Deferred (the common path): the flagged bins stay squeezed at their fp32 targets and are
+            // queued in this CTA's region of the queue (shared-memory index) for redecide_kernel; no CTA
+            // barrier here, so warps keep their own pace through the tile.  Inline fallback (region full,
+            // or the list-mode repair launch): one warp-uniform loop per warp with a single copy of the
+            // warp-cooperative fp64 sum.
             unsigned long long my = uns;
             if (a.gq && my) {
-                // deferred (the common path): squeeze at the fp32 target now, queue for redecide_kernel in
-                // this CTA's region of the queue (shared-memory index: no global atomic on the tile path)
                 const unsigned reg = a.gq_cap / gridDim.x;
                 int4* cq = a.gq + (size_t)blockIdx.x * reg;
-#pragma unroll
-                for (int ii = 0; ii < NB; ++ii)
-                    if ((my >> ii) & 1ull) {
-                        const unsigned q = atomicAdd(&cq_n, 1u);
-                        if (q < reg) {
-                            cq[q] = make_int4((int)fi, bin_k(ii), bl[ii], 0);
-                            my &= ~(1ull << ii);
-                        }
-                    }
-            }
 #pragma unroll 1
-            while (__syncthreads_or(my != 0ull)) {
-                if (threadIdx.x == 0) rq_n = 0;
-                __syncthreads();
                 while (my) {
                     const int i = __ffsll((long long)my) - 1;
-                    const int q = atomicAdd(&rq_n, 1);
-                    if (q >= kRedecideQ) break;                        // queue full: next round
-                    my &= my - 1;
-                    rq[q] = make_int4(bin_k(i), group, i, threadIdx.x);   // (k, frame group, slot, owner)
-                }
-                __syncthreads();
-                const int nq = min(rq_n, kRedecideQ);
-                const double gam64 = launch_gamma64(a);
-                if (threadIdx.x == 0 && !lmode) atomicAdd(a.r23_count, (unsigned long long)nq);
-                // the queue in passes of `per` items, `parts` warps per item (all warps busy, two barriers
-                // per pass): many items -> one warp each; one item -> every warp of the CTA.  Each item's
-                // taps are always split into W fixed virtual parts summed in a fixed order, whatever
-                // `parts` is: bitwise reproducible
-                constexpr int W = TPB / 32;
-                int parts = W;
-                while (parts > 1 && parts * nq > W) parts >>= 1;
-                const int per = W / parts;
-                const int warp = threadIdx.x >> 5;
-#pragma unroll 1
-                for (int q0 = 0; q0 < nq; q0 += per) {
-                    const int q = q0 + warp / parts;
-                    if (q < nq) {
-                        const int4 it = rq[q];
-                        const float* xs = xb + pad + it.y * a.hop;
-#pragma unroll 1
-                        for (int vp = warp % parts; vp < W; vp += parts) {
-                            const double4 r = stft_bin_fp64_part([&](int j) { return xs[j]; }, tap64, a.tw64, N,
-                                                                 a.L, a.c, it.x, vp, W);
-                            if ((threadIdx.x & 31) == 0) rq_red[(warp / parts) * W + vp] = r;
-                        }
-                    }
-                    __syncthreads();
-                    if (threadIdx.x < per && q0 + (int)threadIdx.x < nq) {
-                        const int qq = q0 + threadIdx.x;
-                        double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+                    int li = 0;
 #pragma unroll
-                        for (int w = 0; w < W; ++w) {
-                            const double4 r = rq_red[threadIdx.x * W + w];
-                            v0 += r.x; v1 += r.y; v2 += r.z; v3 += r.w;
-                        }
-                        rq_res[qq] = decide_fp64(a, gam64, rq[qq].x, v0, v1, v2, v3);
-                    }
-                    __syncthreads();
+                    for (int ii = 0; ii < NB; ++ii) li = (ii == i) ? bl[ii] : li;
+                    const unsigned q = atomicAdd(&cq_n, 1u);
+                    if (q >= reg) break;                               // region full: inline below
+                    cq[q] = make_int4((int)fi, bin_k(i), li, 0);
+                    my &= my - 1;
                 }
+            }
+            if (__any_sync(0xffffffffu, my != 0ull)) {
+                const double gam64 = launch_gamma64(a);
+                const int lane = threadIdx.x & 31;
+                const int wbase = threadIdx.x & ~31;
 #pragma unroll 1
-                for (int q = 0; q < nq; ++q) {
-                    const int4 it = rq[q];
-                    if (it.w != (int)threadIdx.x) continue;
-                    const int ln = rq_res[q];
+                while (true) {
+                    const unsigned ball = __ballot_sync(0xffffffffu, my != 0ull);
+                    if (!ball) break;
+                    const int src = __ffs(ball) - 1;
+                    const int i = __ffsll((long long)__shfl_sync(0xffffffffu, my, src)) - 1;
+                    if (lane == src) my &= my - 1;
+                    const int k = __shfl_sync(0xffffffffu, bin_k(i), src);
+                    const float* xs = xb + pad + ((wbase + src) / N2) * a.hop;
+                    double sr, si, dr, di;
+                    stft_bin_fp64([&](int j) { return xs[j]; }, a.taps64, a.tw64, N, a.L, a.c, k, sr, si, dr, di);
+                    const int ln = decide_fp64(a, gam64, k, sr, si, dr, di);
+                    if (lane == 0 && !lmode) atomicAdd(a.r23_count, 1ull);
 #pragma unroll
                     for (int ii = 0; ii < NB; ++ii)
-                        if (ii == it.z) {
+                        if (lane == src && ii == i) {
                             if (bl[ii] != ln && !lmode) atomicAdd(a.r23_count + 1, 1ull);
                             bl[ii] = ln;
                         }

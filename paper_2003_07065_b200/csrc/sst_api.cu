@@ -35,7 +35,6 @@ struct sst_plan {
     float2* d_tw = nullptr;         // [N_f]
     double2* d_taps64 = nullptr;    // [L]  (g, g') fp64 (R23 re-decision)
     double2* d_tw64 = nullptr;      // [N_f] exp(-2 pi i e/N_f) fp64
-    float2* d_tapc = nullptr;       // [L] fp32 corrections of the fp32 taps to fp64
     int32_t* d_mpl = nullptr;       // multi-pass: [mp_fwd_frames][N_f/2 + 1] targets
     unsigned long long* d_r23 = nullptr;   // [2] R23 counters (sst_plan_counters)
     int4* d_gq = nullptr;           // R23 deferral queue [gq_cap], one region per CTA
@@ -71,7 +70,7 @@ struct sst_plan {
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(device);
-        for (void* q : {(void*)d_taps, (void*)d_tw, (void*)d_taps64, (void*)d_tw64, (void*)d_tapc, (void*)d_mpl, (void*)d_r23, (void*)d_gq, (void*)d_gctr,
+        for (void* q : {(void*)d_taps, (void*)d_tw, (void*)d_taps64, (void*)d_tw64, (void*)d_mpl, (void*)d_r23, (void*)d_gq, (void*)d_gctr,
                         (void*)d_dirty_bits, (void*)d_dirty_list, (void*)d_phz, (void*)d_renyi, (void*)d_amax2, (void*)d_back, (void*)d_inv_head, (void*)d_inv_tail,
                         (void*)d_inv_per, (void*)d_absmax, (void*)d_seam, (void*)d_twN, (void*)d_mp0, (void*)d_mp1, (void*)d_wf})
             if (q) cudaFree(q);
@@ -317,8 +316,6 @@ sst::FwdArgs fwd_args(const sst_plan* pl, const float* x, int64_t x_off, int64_t
     a.gamma_d = pl->gamma_abs;
     a.gamma_rel_d = pl->p.gamma;
     a.taps64 = pl->d_taps64;
-    a.tapc = pl->d_tapc;
-    a.inv_alpha_d = 1.0 / pl->lay.alpha;
     a.tw64 = pl->d_tw64;
     a.lscratch = pl->d_mpl;
     a.r23_count = pl->d_r23;
@@ -522,13 +519,7 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
         per[i] = (float)(1.0 / (pl->cst * d));
     }
     std::vector<double2> taps64(L), tw64(Nf);
-    std::vector<float2> tapc(L);
-    for (int32_t j = 0; j < L; ++j) {
-        taps64[j] = make_double2(pl->g[j], pl->gd[j]);
-        // fp64 taps rebuilt on the device as (double)taps + corr: g = t.x + c.x, g' = t.y / alpha + c.y
-        tapc[j] = make_float2((float)(pl->g[j] - (double)taps[j].x),
-                              (float)(pl->gd[j] - (double)taps[j].y * (1.0 / alpha)));
-    }
+    for (int32_t j = 0; j < L; ++j) taps64[j] = make_double2(pl->g[j], pl->gd[j]);
     for (int32_t e = 0; e < Nf; ++e) {
         const double a = -2.0 * kPi * (double)e / Nf;
         tw64[e] = make_double2(std::cos(a), std::sin(a));
@@ -537,7 +528,6 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
     if (const char* mm = std::getenv("SST_R23_M")) { const double v = std::atof(mm); if (v > 0) pl->r23_m = v; }
     if ((s = upload(pl, &pl->d_taps, taps)) != SST_OK || (s = upload(pl, &pl->d_tw, tw)) != SST_OK ||
         (s = upload(pl, &pl->d_taps64, taps64)) != SST_OK || (s = upload(pl, &pl->d_tw64, tw64)) != SST_OK ||
-        (s = upload(pl, &pl->d_tapc, tapc)) != SST_OK ||
         (s = upload(pl, &pl->d_phz, phz)) != SST_OK || (s = upload(pl, &pl->d_inv_head, head)) != SST_OK ||
         (s = upload(pl, &pl->d_inv_tail, tail)) != SST_OK || (s = upload(pl, &pl->d_inv_per, per)) != SST_OK) {
         msg = pl->err;

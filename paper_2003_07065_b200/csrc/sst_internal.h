@@ -22,11 +22,9 @@ __host__ __device__ constexpr int cap_of(int n2) { return 64 * (n2 + 1) + (n2 < 
 __host__ __device__ constexpr int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 // forward dynamic shared memory: [G exchange buffers][taps L float2][2 input tiles][2 mbarriers]
-// [fp64 tap corrections L float2, when they fit (R23 re-decision): the fp64 taps are
-//  g = taps.x + corr.x, g' = taps.y / alpha + corr.y]
-constexpr int kFwdStaticSmem = 4096;   // the forward's static shared memory (R23 queue, reductions), bound
+constexpr int kFwdStaticSmem = 1024;   // the forward's static shared memory (reductions, counters), bound
 struct FwdLayout {
-    int taps_off, xb_off, mbar_off, xcap, t64_off, total;
+    int taps_off, xb_off, mbar_off, xcap, total;
 };
 __host__ __device__ inline FwdLayout fwd_layout(int n2, int L, int H) {
     FwdLayout f{};
@@ -36,16 +34,6 @@ __host__ __device__ inline FwdLayout fwd_layout(int n2, int L, int H) {
     f.xcap = round_up((G - 1) * H + L + 8, 4);          // floats per input tile buffer
     f.mbar_off = f.xb_off + 2 * f.xcap * 4;
     f.total = f.mbar_off + 16;
-    // (only while the SM's shared-memory carveout stays at or below 196 KB: a larger one shrinks L1,
-    // which the twiddle loads use -- measured 8 % slower on C3)
-    const int ctas = tpb_of(n2, true) == 256 ? 1 : 2;   // resident CTAs per SM (launch bounds)
-    const int with = round_up(f.total, 16) + L * 8;
-    if ((with + kFwdStaticSmem + 1024) * ctas <= 196 * 1024) {
-        f.t64_off = round_up(f.total, 16);
-        f.total = with;
-    } else {
-        f.t64_off = -1;
-    }
     return f;
 }
 
@@ -66,8 +54,6 @@ __host__ __device__ inline InvLayout inv_layout(int n2, int L, int H, int zoom) 
     v.total = v.ring_off + r * 4;
     return v;
 }
-
-constexpr int kRedecideQ = 64;     // R23 queue slots per CTA round (forward kernel)
 
 struct FwdArgs {
     const float* x;          // points at global sample x_off
@@ -93,8 +79,6 @@ struct FwdArgs {
     double gamma_d;          // absolute gamma (fp64)
     double gamma_rel_d;      // relative mode: gamma = gamma_rel_d * (*absmax_dev)
     const double2* taps64;   // [L] (g, g') fp64
-    const float2* tapc;      // [L] fp32 corrections: g = (double)taps.x + corr.x, g' = (double)taps.y / alpha + corr.y
-    double inv_alpha_d;      // 1 / alpha
     const double2* tw64;     // [nfft] exp(-2 pi i e / N_f) fp64
     int32_t* lscratch;       // multi-pass: [frames][N_f/2 + 1] targets of the chunk
     unsigned long long* r23_count;   // [2]: bins re-decided, of which the fp64 target differed

@@ -1,6 +1,3 @@
-for M in 6; do
-SST_R23_M=$M timeout 300 python tools/time_cfg.py C3 1 > gpurun_out/plain_k.log 2>&1 && \
-SST_R23_M=$M timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launch_M$M.csv python tools/time_cfg.py C3 1 > gpurun_out/ncu_k.log 2>&1
-done
-SST_NO_REDECIDE=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launch_off.csv python tools/time_cfg.py C3 1 > gpurun_out/ncu_k2.log 2>&1
-echo done
+SST_R23_M=6 timeout 300 python tools/time_cfg.py C3 1 > gpurun_out/plain_k.log 2>&1 && \
+SST_R23_M=6 timeout 900 ncu --set full --import-source on --clock-control none -k regex:fwd_kernel -c 1 -o gpurun_out/prof_fwd_r23 python tools/time_cfg.py C3 1 > gpurun_out/ncu_full.log 2>&1
+echo "ncu exit $?" >> gpurun_out/ncu_full.log
