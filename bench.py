@@ -4,10 +4,14 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C3] [--impl ours|reference]
 
 One step = the whole hot path over one record: sst_forward of every
-frame (band output T in HBM) then the inverse (Eq. 25-26) back to x_hat.  At N=1 the workload
-is BASELINE.json configs[2] (C3, aero-engine run-up, forward + inverse; DESIGN.md §8 says why).
-For N>1 (torchrun, one rank per GPU, NCCL) the record is time-sharded with per-rank work fixed
-(weak scaling: the run-up record is N x longer); ranks exchange the inverse's OLA seams.
+frame (band output T in HBM) then the inverse (Eq. 25-26) back to x_hat.  The workload is
+BASELINE.json configs[2] (C3, aero-engine run-up, forward + inverse; DESIGN.md §8 says why).
+For N>1 (torchrun, one rank per GPU, NCCL) the same record is time-sharded over the ranks (strong
+scaling): each rank forwards its frames, accumulates its inverse partial sums, exchanges the OLA
+seams with its neighbours over NCCL and finalises the samples it owns (dist.ShardedRun).  Legs
+(``--legs``, default C4,C5): the largest configs on their fixed records, sharded the same way --
+C4 forward (T resident), C5 forward + inverse in frame chunks with one reused T buffer (its 256 GiB
+plane never exists whole on one GPU) -- so t_1 / (P t_P) can be read per config.
 
 Prints ONE JSON line on rank 0.  ``--impl reference`` times the fp64 CPU oracle instead
 (the reference arm of this tier), on the box's host cores.
@@ -357,6 +361,82 @@ def measure_extras(P, plan, cfg, x, T, y, stream, ev, reps=5):
     return out
 
 
+def store_peak_gbs(dev, gib=4, reps=5):
+    """Write-only HBM bandwidth on this GPU (C5's forward traffic is ~all writes): a
+    `fill_` of a buffer larger than L2, CUDA events, best of `reps`."""
+    import torch
+    buf = torch.empty(gib << 30, dtype=torch.uint8, device=dev)
+    buf.fill_(1)
+    best = float("inf")
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        buf.fill_(2)
+        b.record()
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b))
+    del buf
+    torch.cuda.empty_cache()
+    return (gib << 30) / (best * 1e-3) / 1e9
+
+
+def measure_leg(P, D, name, world, rank, local, dev, steps, warmup, chunk_frames, hbm_gbs, store_gbs):
+    """A SURVEY §8(d) leg on a fixed record, time-sharded over the ranks (strong scaling): C4 (forward,
+    T resident) or C5 (forward + inverse; frames processed in chunks of ``chunk_frames`` with one
+    reused T buffer -- its 256 GiB plane never exists whole).  Device time, max over ranks; the
+    forward share is timed by forward-only passes."""
+    import torch
+    cfg = get_config(name)
+    c = cfg.L // 2
+    sh = D.shard(cfg.N, cfg.hop, cfg.L, c, world, rank)
+    x_host = generate(cfg, sh.span_lo, sh.span_hi)
+    g, gd = P.gaussian_window(cfg.L, cfg.sigma)
+    gamma = 1e-6 * float(np.sum(g)) * D.max_over_ranks(float(np.abs(x_host).max()), dev)   # reading R6
+    plan = P.Plan(cfg.N, cfg.fs, cfg.L, cfg.sigma, cfg.hop, cfg.nfft, cfg.f1, cfg.f2, cfg.zoom, gamma=gamma,
+                  device=local)
+    x = torch.from_numpy(x_host).to(dev)
+    del x_host
+    run = D.ShardedRun(plan, sh, x, inverse=cfg.inverse, chunk_frames=chunk_frames if cfg.inverse else 0)
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn, k):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(k):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return D.max_over_ranks(a.elapsed_time(b) / k, dev)
+
+    step_ms = timed(run.step, steps)
+    fwd_ms = timed(lambda: run.step(forward_only=True), steps) if cfg.inverse else step_ms
+    fwd_fl, inv_fl, fwd_b, inv_b = algorithmic_counts(cfg)
+    F = cfg.frames
+    out = {"workload": WORKLOAD_DESC[name], "ms_per_step": step_ms, "fwd_ms": fwd_ms,
+           "msamples_per_s": cfg.N / (step_ms * 1e-3) / 1e6, "tf_coeffs_per_s": F * cfg.bins / (step_ms * 1e-3),
+           "fwd_hbm_gbs": F * fwd_b / (fwd_ms * 1e-3) / 1e9 / world,
+           "fwd_hbm_frac": F * fwd_b / (fwd_ms * 1e-3) / 1e9 / world / hbm_gbs,
+           "fwd_fp32_frac": F * fwd_fl / (fwd_ms * 1e-3) / 1e12 / world / (148 * 128 * 2 * 1.965e9 / 1e12),
+           "chunk_frames": run.chunk, "T_chunk_gib": run.chunk * cfg.bins * 8 / 2 ** 30,
+           "launches_per_step": run.launches_per_step, "r23": plan.counters()}
+    if cfg.inverse:
+        inv_ms = step_ms - fwd_ms
+        out.update({"inv_ms": inv_ms, "inv_hbm_gbs": F * inv_b / (inv_ms * 1e-3) / 1e9 / world,
+                    "inv_hbm_frac": F * inv_b / (inv_ms * 1e-3) / 1e9 / world / hbm_gbs,
+                    "inv_fp32_frac": F * inv_fl / (inv_ms * 1e-3) / 1e12 / world / (148 * 128 * 2 * 1.965e9 / 1e12)})
+    if store_gbs:
+        out["fwd_frac_of_store_peak"] = out["fwd_hbm_gbs"] / store_gbs
+    del run, x
+    plan.close()
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, cfg_base):
     import torch
     import torch.distributed as dist
@@ -373,7 +453,7 @@ def run_ours(args, cfg_base):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    cfg = cfg_base.with_(N=cfg_base.N * world) if world > 1 else cfg_base   # weak scaling
+    cfg = cfg_base                                  # strong scaling: one fixed record over the ranks
     g, gd = P.gaussian_window(cfg.L, cfg.sigma)
     c = cfg.L // 2
     sh = D.shard(cfg.N, cfg.hop, cfg.L, c, world, rank)
@@ -383,26 +463,25 @@ def run_ours(args, cfg_base):
     plan = P.Plan(cfg.N, cfg.fs, cfg.L, cfg.sigma, cfg.hop, cfg.nfft, cfg.f1, cfg.f2, cfg.zoom,
                   gamma=gamma, device=local)
     x = torch.from_numpy(x_host).to(dev)
-    T = torch.empty((sh.frames, plan.bins), dtype=torch.complex64, device=dev)
-    span = sh.span_hi - sh.span_lo
-    y = torch.empty(span if world > 1 else cfg.N, dtype=torch.float32, device=dev)
-    do_inv = True
     stream = torch.cuda.current_stream(dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    if world == 1:
+        T = torch.empty((sh.frames, plan.bins), dtype=torch.complex64, device=dev)
+        y = torch.empty(cfg.N, dtype=torch.float32, device=dev)
+        run = None
+    else:
+        run = D.ShardedRun(plan, sh, x, inverse=True)    # forward, accumulate, NCCL seams, finalize
 
     def step(record=None):
         e0, e1, e2 = (ev(), ev(), ev()) if record is not None else (None, None, None)
         if e0: e0.record(stream)
-        plan.forward(x, sh.frame_begin, sh.frame_end, x_off=sh.span_lo, out=T)
-        if e1: e1.record(stream)
-        if do_inv:
-            if world == 1:
-                plan.inverse(T, out=y)
-            else:
-                y.zero_()
-                plan.inverse_accumulate(T, sh.frame_begin, sh.frame_end, y, y_off=sh.span_lo)
-                D.exchange_seams(y, sh, cfg.hop, c)
-                plan.inverse_finalize(D.own_slice(y, sh), y_off=sh.own_lo)
+        if run is None:
+            plan.forward(x, out=T)
+            if e1: e1.record(stream)
+            plan.inverse(T, out=y)
+        else:
+            run.step()
+            if e1: e1.record(stream)
         if e2: e2.record(stream)
         if record is not None:
             record.append((e0, e1, e2))
@@ -425,14 +504,26 @@ def run_ours(args, cfg_base):
             dist.barrier()
         torch.cuda.synchronize()
     ms_local = t_start.elapsed_time(t_end)
-    fwd_ms = sum(a.elapsed_time(b) for a, b, _ in recs) / len(recs)
-    inv_ms = sum(b.elapsed_time(cc) for _, b, cc in recs) / len(recs)
     per_step = sorted(a.elapsed_time(cc) for a, _, cc in recs)      # median and min too
     step_stats = {"median_ms": per_step[len(per_step) // 2], "min_ms": per_step[0], "max_ms": per_step[-1]}
     ms_total = D.max_over_ranks(ms_local, dev)
     ms_step = ms_total / args.steps
-    total_samples = cfg.N
-    value = total_samples / (ms_step * 1e-3) / 1e6
+    if run is None:
+        fwd_ms = sum(a.elapsed_time(b) for a, b, _ in recs) / len(recs)
+        inv_ms = sum(b.elapsed_time(cc) for _, b, cc in recs) / len(recs)
+    else:
+        # forward share of a rank's step from forward-only passes (after the timed region)
+        a, b = ev(), ev()
+        a.record(stream)
+        for _ in range(3):
+            run.step(forward_only=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        fwd_ms = a.elapsed_time(b) / 3
+        inv_ms = max(0.0, ms_local / args.steps - fwd_ms)
+    fwd_ms = D.max_over_ranks(fwd_ms, dev)
+    inv_ms = D.max_over_ranks(inv_ms, dev)
+    value = cfg.N / (ms_step * 1e-3) / 1e6
     coeffs_per_s = cfg.frames * cfg.bins / (ms_step * 1e-3)
 
     # ---- end to end through the public API with host buffers (pinned), per step
@@ -441,7 +532,7 @@ def run_ours(args, cfg_base):
         xh = torch.from_numpy(x_host).pin_memory()
         own = sh.own_hi - sh.own_lo
         yh = torch.empty(own, dtype=torch.float32).pin_memory()
-        rt = None
+        rt = graph = None
         if world == 1:
             # host -> host through the public pipeline helper: chunked H2D / forward / inverse /
             # finalize / D2H on three streams, transfers overlapped with the kernels
@@ -465,24 +556,24 @@ def run_ours(args, cfg_base):
                     rt.run(xh, yh, T)
                 continue
             x.copy_(xh, non_blocking=True)
-            step()
-            yh.copy_(D.own_slice(y, sh), non_blocking=True)
+            own_y = run.step()
+            yh.copy_(own_y, non_blocking=True)
         a1 = ev()
         a1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = D.max_over_ranks(a0.elapsed_time(a1), dev) / args.steps
-        e2e = {"value": total_samples / (e2e_ms * 1e-3) / 1e6, "unit": "Msamples/s",
-               "h2d_bytes_per_step": int(xh.numel() * 4 * world), "d2h_bytes_per_step": int(cfg.N * 4),
-               "ms_per_step": e2e_ms}
+        e2e = {"value": cfg.N / (e2e_ms * 1e-3) / 1e6, "unit": "Msamples/s",
+               "h2d_bytes_per_step": int(D.max_over_ranks(xh.numel() * 4, dev) * world),
+               "d2h_bytes_per_step": int(cfg.N * 4), "ms_per_step": e2e_ms}
 
     hbm_gbs, sm_max_mhz, peak_src = _peaks()
     fwd_fl, inv_fl, fwd_b, inv_b = algorithmic_counts(cfg)
     nfr_rank = sh.frames
     fp32_peak = 148 * 128 * 2 * sm_max_mhz * 1e6 / 1e12   # TFLOP/s
     fwd_tf = fwd_fl * nfr_rank / (fwd_ms * 1e-3) / 1e12
-    inv_tf = inv_fl * nfr_rank / (inv_ms * 1e-3) / 1e12
+    inv_tf = inv_fl * nfr_rank / (inv_ms * 1e-3) / 1e12 if inv_ms > 0 else 0.0
     fwd_gbs = fwd_b * nfr_rank / (fwd_ms * 1e-3) / 1e9
-    inv_gbs = inv_b * nfr_rank / (inv_ms * 1e-3) / 1e9
+    inv_gbs = inv_b * nfr_rank / (inv_ms * 1e-3) / 1e9 if inv_ms > 0 else 0.0
     dom = "forward" if fwd_ms >= inv_ms else "inverse"
     ach = fwd_tf if dom == "forward" else inv_tf
     traffic = _traffic(cfg_base.name, dom, nfr_rank) if world == 1 else None
@@ -495,20 +586,32 @@ def run_ours(args, cfg_base):
                 "alu": {"forward_tflops": fwd_tf, "inverse_tflops": inv_tf,
                         "forward_frac": fwd_tf / fp32_peak, "inverse_frac": inv_tf / fp32_peak},
                 "per_frame": {"fwd_flops": fwd_fl, "inv_flops": inv_fl, "fwd_bytes": fwd_b, "inv_bytes": inv_b}}
+    r23 = plan.counters()
+    launches_per_step = (3 + 2) if run is None else run.launches_per_step
     extras = None
     if world == 1 and not args.no_extras:
         extras = measure_extras(P, plan, cfg, x, T, y, stream, ev)
+    del x
+    if run is None:
+        del T, y
+    else:
+        del run
+    plan.close()
+    torch.cuda.empty_cache()
+    legs = {}
+    store = store_peak_gbs(dev) if args.legs else None
+    for name in [s for s in args.legs.split(",") if s]:
+        legs[name] = measure_leg(P, D, name, world, rank, local, dev, args.leg_steps, 3, args.c5_chunk, hbm_gbs, store)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg_base, args.cpu_seconds)
-    launches_per_step = 1 + (2 if world == 1 else 3)
     if rank == 0:
         line = {
             "metric": "SST fwd+inverse input Msamples/s", "value": value, "unit": "Msamples/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD_DESC[cfg_base.name], "N_per_gpu": cfg_base.N, "N_total": cfg.N,
+            "config": {"workload": WORKLOAD_DESC[cfg_base.name], "N": cfg.N, "N_per_gpu": sh.frames * cfg.hop,
                        "frames": cfg.frames, "bins": cfg.bins, "T_bytes": cfg.frames * cfg.bins * 8,
                        "parallelism": f"time-shard x{world}",
                        "l2": "inputs larger than L2 (T = %.1f GiB written and read per step)" % (
@@ -516,6 +619,9 @@ def run_ours(args, cfg_base):
             "tf_coeffs_per_s": coeffs_per_s,
             "fwd_ms": fwd_ms, "inv_ms": inv_ms, "step_ms_stats": step_stats,
             "roofline": roofline,
+            "r23": r23,
+            "legs": legs or None,
+            "hbm_store_gbs": store,
             "cpu_baseline": cpu,
             "extras": extras,
             "e2e": e2e,
@@ -523,7 +629,6 @@ def run_ours(args, cfg_base):
             "gpu_launches": launches_per_step * args.steps,
         }
         print(json.dumps(line), flush=True)
-    plan.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -541,6 +646,9 @@ def main():
     ap.add_argument("--e2e-chunks", type=int, default=8)
     ap.add_argument("--e2e-no-graph", action="store_true", help="launch the e2e round trip chunk by chunk")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--legs", default="C4,C5", help="extra fixed-record legs (strong scaling), '' for none")
+    ap.add_argument("--leg-steps", type=int, default=3)
+    ap.add_argument("--c5-chunk", type=int, default=1 << 20, help="C5 frames per chunk (T buffer 16 GiB)")
     ap.add_argument("--ref-frames", type=int, default=512)
     ap.add_argument("--ref-procs", type=int, default=0, help="reference arm processes (default: every core)")
     args = ap.parse_args()

@@ -35,6 +35,9 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // U = Im Za + Im Zb, V = Re Za - Re Zb;  -Im(S'/S) = (V P + U Q) / (alpha (P^2 + Q^2)).
 // Branch-free (the bins of a thread interleave): select chains instead of early returns.
 // cm, km: the frame's R23 margins (see fwd_margins); unsure = the fp32 result is not final.
+// FULLWARP: every lane of the warp calls it together (the fused kernel); else the vote uses the
+// active mask (the multi-pass kernel's strided bin loop).
+template <bool FULLWARP = true>
 __device__ __forceinline__ int bin_target(const FwdArgs& a, float gam4, float cm, float km, int k, float2 za,
                                           float2 zb, float2& PQ, float2& UV, float& mag4, bool& unsure) {
     PQ = __fadd2_rn(za, make_float2(zb.x, -zb.y));                           // (P, Q) = 2 S
@@ -61,7 +64,7 @@ __device__ __forceinline__ int bin_target(const FwdArgs& a, float gam4, float cm
     // band's plane land far outside it).
     const bool cand = src && (unsigned)(l + 1) <= (unsigned)a.bins + 1u && fin;
     unsure = false;
-    if (__any_sync(__activemask(), cand)) {
+    if (__any_sync(FULLWARP ? 0xffffffffu : __activemask(), cand)) {
         const float rs = rsqrtf(mag4);
         const float mg = cm * fmaf(fabsf(UV.x) + fabsf(UV.y), rsq, rs);
         const float fr = t - fl;

@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(kBinThreads) mp_bins_kernel(const FwdArgs a, c
             float2 PQ, UV;
             float mag4;
             bool unsure;
-            bin_target(a, gam4, 0.0f, -1.0f, k, Z[k], Z[(N - k) & (N - 1)], PQ, UV, mag4, unsure);
+            bin_target<false>(a, gam4, 0.0f, -1.0f, k, Z[k], Z[(N - k) & (N - 1)], PQ, UV, mag4, unsure);
             if constexpr (MODE == kModeStft) {
                 a.S[fi * K + k] = make_float2(0.5f * PQ.x, 0.5f * PQ.y);
                 a.Sd[fi * K + k] = make_float2(UV.x * a.inv_alpha2, -UV.y * a.inv_alpha2);
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kBinThreads) mp_bins_kernel(const FwdArgs a, c
             float2 PQ, UV;
             float mag4;
             bool unsure;
-            const int l = bin_target(a, gam4, cm, km, k, Z[k], Z[(N - k) & (N - 1)], PQ, UV, mag4, unsure);
+            const int l = bin_target<false>(a, gam4, cm, km, k, Z[k], Z[(N - k) & (N - 1)], PQ, UV, mag4, unsure);
             lrow[k] = unsure ? -4 : l;                                 // -4: pending fp64 decision
         }
         __syncthreads();

@@ -129,28 +129,29 @@ class ShardedRun:
         self.y = torch.empty(sh.span_hi - sh.span_lo, dtype=torch.float32, device=plan.device) if inverse else None
         self.own = None
 
-    def step(self):
+    def step(self, forward_only: bool = False):
+        """One pass; ``forward_only`` runs just the chunked forward (timing of the forward share)."""
         sh, plan = self.sh, self.plan
-        if self.inverse:
+        inv = self.inverse and not forward_only
+        if inv:
             self.y.zero_()
         for fb in range(sh.frame_begin, sh.frame_end, self.chunk):
             fe = min(sh.frame_end, fb + self.chunk)
             T = self.T[:fe - fb]
             plan.forward(self.x, fb, fe, x_off=sh.span_lo, out=T)
-            if self.inverse:
+            if inv:
                 plan.inverse_accumulate(T, fb, fe, self.y, y_off=sh.span_lo)
-        if self.inverse:
+        if inv:
             recv = exchange_seams(self.y, sh, self.hop, self.c, self.group)
             self.own = finalize_owned(plan, self.y, sh, recv)
         return self.own
 
     @property
     def launches_per_step(self) -> int:
+        """Library kernels per step: per chunk the forward (main, R23 re-decision, R23 repair) and the
+        accumulate (inverse kernel, CTA-seam kernel); one finalize."""
         chunks = -(-self.sh.frames // self.chunk)
-        if not self.inverse:
-            return chunks
-        # forward + accumulate (+ seam kernel) per chunk, zero fill, finalize
-        return chunks * 3 + 2
+        return chunks * 3 if not self.inverse else chunks * 5 + 1
 
 
 def own_slice(y_span: torch.Tensor, sh: Shard) -> torch.Tensor:

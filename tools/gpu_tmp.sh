@@ -1,3 +1,3 @@
-timeout 1500 python -m pytest tests -m gpu -q -rf --durations=8 > gpurun_out/pytest_r2a.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_r2a.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r2a.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke_r2a.log
-timeout 900 python bench.py > gpurun_out/bench_r2a.json 2> gpurun_out/bench_r2a.err; echo "bench exit $?" >> gpurun_out/bench_r2a.err
+timeout 300 python tools/time_cfg.py C3 1 > gpurun_out/plain_k.log 2>&1 && \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"inv_kernel" -c 1 -o gpurun_out/prof_c3_inv_r2 python tools/time_cfg.py C3 1 > gpurun_out/ncu_full.log 2>&1
+echo "ncu exit $?" >> gpurun_out/ncu_full.log
