@@ -365,13 +365,13 @@ def store_peak_gbs(dev, gib=4, reps=5):
     """Write-only HBM bandwidth on this GPU (C5's forward traffic is ~all writes): a
     `fill_` of a buffer larger than L2, CUDA events, best of `reps`."""
     import torch
-    buf = torch.empty(gib << 30, dtype=torch.uint8, device=dev)
-    buf.fill_(1)
+    buf = torch.empty(gib << 28, dtype=torch.float32, device=dev)
+    buf.fill_(1.0)
     best = float("inf")
     for _ in range(reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        buf.fill_(2)
+        buf.fill_(2.0)
         b.record()
         torch.cuda.synchronize()
         best = min(best, a.elapsed_time(b))

@@ -82,10 +82,17 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
 
     const int64_t nfr = a.frame_end - a.frame_begin;
     // list mode (R23 repair): tile t is the single frame flist[t] (group 0), inline re-decision
+    // list mode (R23 repair): tile t holds the frames flist[t G .. t G + G) (within the launch, one per
+    // group), gathered straight from global memory (bounds-checked); inline re-decision
     const bool lmode = a.flist != nullptr;
-    const int64_t ntiles = lmode ? (int64_t)*a.flist_n : (nfr + G - 1) / G;
-    auto tile_first = [&](int64_t t) -> int64_t { return lmode ? (int64_t)__ldg(a.flist + t) : t * G; };
-    const int tile_g = lmode ? 1 : G;
+    const int64_t nlist = lmode ? (int64_t)*a.flist_n : 0;
+    const int64_t ntiles = lmode ? (nlist + G - 1) / G : (nfr + G - 1) / G;
+    const int64_t v_lo_x = a.x_off > 0 ? a.x_off : 0;
+    const int64_t v_hi_x = min(a.n, a.x_off + a.x_len);
+    auto xglob = [&](int64_t frame, int j) -> float {           // sample j of frame (within the launch)
+        const int64_t sj = (a.frame_begin + frame) * a.hop - a.c + j;
+        return (sj >= v_lo_x && sj < v_hi_x) ? __ldg(a.x + (sj - a.x_off)) : 0.0f;
+    };
     const int64_t tiles_per_cta = (ntiles + gridDim.x - 1) / gridDim.x;
     const int64_t t_begin = (int64_t)blockIdx.x * tiles_per_cta;
     const int64_t t_end = min(ntiles, t_begin + tiles_per_cta);
@@ -101,8 +108,8 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
         fence_mbar_init();
     }
     __syncthreads();
-    if (threadIdx.x == 0 && t_begin < t_end) {
-        const TileIn ti = tile_in(a, a.frame_begin + tile_first(t_begin), tile_g, x_aligned);
+    if (threadIdx.x == 0 && t_begin < t_end && !lmode) {
+        const TileIn ti = tile_in(a, a.frame_begin + t_begin * G, G, x_aligned);
         if (ti.bulk) {
             mbar_arrive_tx(&mbar[0], ti.bytes);
             bulk_g2s(xbuf, a.x + ti.a_lo, ti.bytes, &mbar[0]);
@@ -114,24 +121,25 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
         const int bsel = (int)((tile - t_begin) & 1);
         float* xb = xbuf + bsel * a.lay.xcap;
         // prefetch tile + 1 into the other buffer (freed by the barrier that ended tile - 1)
-        if (threadIdx.x == 0 && tile + 1 < t_end) {
-            const TileIn tn = tile_in(a, a.frame_begin + tile_first(tile + 1), tile_g, x_aligned);
+        if (threadIdx.x == 0 && tile + 1 < t_end && !lmode) {
+            const TileIn tn = tile_in(a, a.frame_begin + (tile + 1) * G, G, x_aligned);
             if (tn.bulk) {
                 fence_proxy_async();
                 mbar_arrive_tx(&mbar[bsel ^ 1], tn.bytes);
                 bulk_g2s(xbuf + (bsel ^ 1) * a.lay.xcap, a.x + tn.a_lo, tn.bytes, &mbar[bsel ^ 1]);
             }
         }
-        const int64_t f_first = tile_first(tile);    // first frame of the tile within the launch
-        const TileIn ti = tile_in(a, a.frame_begin + f_first, tile_g, x_aligned);
+        const TileIn ti = tile_in(a, a.frame_begin + tile * G, G, x_aligned);
         int pad = ti.pad;
-        if (ti.bulk) {
+        if (lmode) {
+            pad = 0;
+        } else if (ti.bulk) {
             mbar_wait(&mbar[bsel], (phase >> bsel) & 1);
             phase ^= 1u << bsel;
         } else {
             const int64_t v_lo = a.x_off > 0 ? a.x_off : 0;
             const int64_t v_hi = min(a.n, a.x_off + a.x_len);
-            const int span = (tile_g - 1) * a.hop + a.L;
+            const int span = (G - 1) * a.hop + a.L;
             for (int i = threadIdx.x; i < span; i += TPB) {
                 const int64_t s = ti.s_lo + i;
                 xb[i] = (s >= v_lo && s < v_hi) ? __ldg(a.x + (s - a.x_off)) : 0.0f;
@@ -140,14 +148,25 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
             __syncthreads();
         }
 
-        const int64_t fi = lmode ? (group == 0 ? f_first : nfr) : f_first + group;   // frame within the launch
+        const int64_t li = tile * G + group;
+        const int64_t fi = lmode ? (li < nlist ? (int64_t)__ldg(a.flist + li) : nfr) : li;   // frame within the launch
         const bool valid = fi < nfr;
         const float* xw = xb + pad + group * a.hop; // x[m H - c + j], j = 0..L-1 (j = tau + c)
 
         // ---- a1: gather + pack (circular placement), a2 step 1: 64-point DFT of row tg
         float2 v[64];
         float2 nacc = make_float2(0.0f, 0.0f);          // ||z_m||^2 partial (R23 margins)
-        if constexpr (FULLWIN) {
+        if (lmode) {
+#pragma unroll
+            for (int n1 = 0; n1 < 64; ++n1) {
+                const int n = N2 * n1 + tg;
+                const int j = ((n <= last_in) ? n : n - N) + a.c;
+                float2 val = make_float2(0.0f, 0.0f);
+                if (j >= 0 && valid) val = cscale(taps_s[j], xglob(fi, j));
+                v[n1] = val;
+                if constexpr (KEEPL) nacc = __ffma2_rn(val, val, nacc);
+            }
+        } else if constexpr (FULLWIN) {
             const float* xt = xw + tg;
             const float2* wt = taps_s + tg;
 #pragma unroll
@@ -378,8 +397,10 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                     if (lane == src) my &= my - 1;
                     const int k = __shfl_sync(0xffffffffu, bin_k(i), src);
                     const float* xs = xb + pad + ((wbase + src) / N2) * a.hop;
+                    const int64_t fsrc = __shfl_sync(0xffffffffu, fi, src);
                     double sr, si, dr, di;
-                    stft_bin_fp64([&](int j) { return xs[j]; }, a.taps64, a.tw64, N, a.L, a.c, k, sr, si, dr, di);
+                    stft_bin_fp64([&](int j) { return lmode ? xglob(fsrc, j) : xs[j]; }, a.taps64, a.tw64, N, a.L,
+                                  a.c, k, sr, si, dr, di);
                     const int ln = decide_fp64(a, gam64, k, sr, si, dr, di);
                     if (lane == 0 && !lmode) atomicAdd(a.r23_count, 1ull);
 #pragma unroll

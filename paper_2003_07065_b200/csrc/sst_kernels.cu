@@ -76,50 +76,68 @@ __global__ void finalize_kernel(float* y, int64_t y_off, int64_t y_len, InvArgs 
 // changed is listed once (dirty_bits / dirty_list / a.gq_n[1]) for the list-mode repair launch.
 __global__ void __launch_bounds__(256) redecide_kernel(const FwdArgs a, int mode, unsigned int* dirty_bits,
                                                       int* dirty_list) {
+    // one CTA per queue region (the main launch's CTA b), 8 lanes per queued bin: lane u of the
+    // octet takes taps j = u + 8 t of the direct Eq. 8 sum (a load instruction covers 4 bins x 8
+    // consecutive samples), with the twiddle recurrence w <- w W^{8 k} from W^{k (u - c)}
+    // (<= L/8 fp64 complex products, ~1e-14 relative); fixed 3-level xor reduction (deterministic)
     const unsigned reg = a.gq_cap / a.gq_ctas;
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int b = blockIdx.x;
+    const unsigned cnt = __ldg(a.gq_counts + b);
     const double gam64 = launch_gamma64(a);
     const int64_t v_lo = a.x_off > 0 ? a.x_off : 0;
     const int64_t v_hi = min(a.n, a.x_off + a.x_len);
     const int64_t K = a.nfft / 2 + 1;
-    // items (CTA region b, entry i) in a grid-stride walk over the concatenated regions
-    int64_t base = 0;
-    for (int b = 0; b < a.gq_ctas; ++b) {
-      const unsigned cnt = __ldg(a.gq_counts + b);
-      for (int64_t e = ((w0 - base) % nw + nw) % nw; e < cnt; e += nw) {
-        const int4 it = a.gq[(size_t)b * reg + e];
+    const unsigned msk = (unsigned)a.nfft - 1u;
+    const int u = threadIdx.x & 7;
+    const unsigned rounds = (cnt + 31) / 32;                         // 32 bins per CTA pass (256 / 8)
+    for (unsigned r = 0; r < rounds; ++r) {
+        const unsigned e = r * 32 + (threadIdx.x >> 3);
+        const bool ok = e < cnt;
+        const int4 it = ok ? a.gq[(size_t)b * reg + e] : make_int4(0, 0, 0, 0);
         const int64_t s0 = (a.frame_begin + it.x) * a.hop - a.c;
-        auto xat = [&](int j) -> float {
-            const int64_t sj = s0 + j;
-            return (sj >= v_lo && sj < v_hi) ? __ldg(a.x + (sj - a.x_off)) : 0.0f;
-        };
-        double sr, si, dr, di;
-        stft_bin_fp64(xat, a.taps64, a.tw64, a.nfft, a.L, a.c, it.y, sr, si, dr, di);
-        const int ln = decide_fp64(a, gam64, it.y, sr, si, dr, di);
-        if (lane == 0) {
-            atomicAdd(a.r23_count, 1ull);
-            if (ln != it.z) {
-                atomicAdd(a.r23_count + 1, 1ull);
-                if (mode == kModeTargets) {
-                    a.lout[(int64_t)it.x * K + it.y] = ln;
-                } else {
-                    const unsigned bit = 1u << (it.x & 31);
-                    if (!(atomicOr(dirty_bits + (it.x >> 5), bit) & bit)) dirty_list[atomicAdd(a.gq_n, 1u)] = it.x;
-                }
+        const int k = it.y;
+        double2 w = __ldg(a.tw64 + (((unsigned)k * (unsigned)(u - a.c)) & msk));   // W^{k (u - c)}
+        const double2 st = __ldg(a.tw64 + ((8u * (unsigned)k) & msk));             // W^{8 k}
+        double sr = 0.0, si = 0.0, dr = 0.0, di = 0.0;
+        if (ok) {
+            for (int j = u; j < a.L; j += 8) {
+                const int64_t sj = s0 + j;
+                const double xv = (sj >= v_lo && sj < v_hi) ? (double)__ldg(a.x + (sj - a.x_off)) : 0.0;
+                const double2 g = __ldg(a.taps64 + j);
+                const double p = xv * g.x, q = xv * g.y;
+                sr = fma(p, w.x, sr);
+                si = fma(p, w.y, si);
+                dr = fma(q, w.x, dr);
+                di = fma(q, w.y, di);
+                const double wr = fma(w.x, st.x, -w.y * st.y);
+                w.y = fma(w.x, st.y, w.y * st.x);
+                w.x = wr;
             }
         }
-      }
-      base += cnt;
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+            sr += __shfl_xor_sync(0xffffffffu, sr, o);
+            si += __shfl_xor_sync(0xffffffffu, si, o);
+            dr += __shfl_xor_sync(0xffffffffu, dr, o);
+            di += __shfl_xor_sync(0xffffffffu, di, o);
+        }
+        if (!ok || u != 0) continue;
+        const int ln = decide_fp64(a, gam64, k, sr, si, dr, di);
+        atomicAdd(a.r23_count, 1ull);
+        if (ln != it.z) {
+            atomicAdd(a.r23_count + 1, 1ull);
+            if (mode == kModeTargets) {
+                a.lout[(int64_t)it.x * K + k] = ln;
+            } else {
+                const unsigned bit = 1u << (it.x & 31);
+                if (!(atomicOr(dirty_bits + (it.x >> 5), bit) & bit)) dirty_list[atomicAdd(a.gq_n, 1u)] = it.x;
+            }
+        }
     }
 }
 
 cudaError_t launch_redecide(const FwdArgs& a, int mode, unsigned int* dirty_bits, int* dirty_list, cudaStream_t s) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    redecide_kernel<<<sms * 4, 256, 0, s>>>(a, mode, dirty_bits, dirty_list);
+    redecide_kernel<<<a.gq_ctas, 256, 0, s>>>(a, mode, dirty_bits, dirty_list);
     return cudaGetLastError();
 }
 
