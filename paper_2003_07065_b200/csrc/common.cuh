@@ -52,6 +52,17 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
                  : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef SST_BOUNDS
+    // bounded spin: a TMA completion that never arrives (bad byte count / address) traps
+    for (long long spin = 0;; ++spin) {
+        uint32_t done;
+        asm volatile(
+            "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+            : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+        if (done) return;
+        SST_CHECK(spin < (1ll << 26));
+    }
+#endif
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"

@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
             const int span = (G - 1) * a.hop + a.L;
             for (int i = threadIdx.x; i < span; i += TPB) {
                 const int64_t s = ti.s_lo + i;
+                SST_CHECK(i < a.lay.xcap && (s < v_lo || s >= v_hi || (s - a.x_off >= 0 && s - a.x_off < a.x_len)));
                 xb[i] = (s >= v_lo && s < v_hi) ? __ldg(a.x + (s - a.x_off)) : 0.0f;
             }
             pad = 0;
@@ -200,6 +201,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
         for (int k1 = 0; k1 < 64; ++k1) {
             float2 t = v[k1];
             if (k1 != 0) t = cmul(t, __ldg(a.tw + k1 * N2 + tg));   // W_N^{tg k1}, lane-contiguous
+            SST_CHECK(k1 * STRIDE + tg < CAP);
             buf[k1 * STRIDE + tg] = t;
         }
         group_sync<N2>(group);
@@ -380,6 +382,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                     for (int ii = 0; ii < NB; ++ii) li = (ii == i) ? bl[ii] : li;
                     const unsigned q = atomicAdd(&cq_n, 1u);
                     if (q >= reg) break;                               // region full: inline below
+                    SST_CHECK((size_t)blockIdx.x * reg + q < a.gq_cap && fi < nfr);
                     cq[q] = make_int4((int)fi, bin_k(i), li, 0);
                     my &= my - 1;
                 }
@@ -414,7 +417,10 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
             if constexpr (MODE == kModeTargets) {
 #pragma unroll
                 for (int i = 0; i < NB; ++i)
-                    if (bl[i] != -3) a.lout[fi * (int64_t)(N / 2 + 1) + bin_k(i)] = bl[i];
+                    if (bl[i] != -3) {
+                        SST_CHECK(fi < nfr && bin_k(i) <= N / 2);
+                        a.lout[fi * (int64_t)(N / 2 + 1) + bin_k(i)] = bl[i];
+                    }
             }
         }
 
@@ -472,6 +478,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                         long long xr, xi;
                         asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xr) : "f"(vr));
                         asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xi) : "f"(vi));
+                        SST_CHECK(lr >= 0 && lr < CH && (int)(acc - reinterpret_cast<int*>(buf)) + 3 * CH + lr < 2 * CAP);
                         atomicAdd(acc + lr, (int)(xr >> 20));
                         atomicAdd(acc + CH + lr, (int)(xr & 0xFFFFF));
                         atomicAdd(acc + 2 * CH + lr, (int)(xi >> 20));
@@ -498,6 +505,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                             t = make_float2(limbs_to_float(a0[i], a0[CH + i], iscale),
                                             limbs_to_float(a0[2 * CH + i], a0[3 * CH + i], iscale));
                         }
+                        SST_CHECK(fi < nfr && l0 + i < a.bins);
                         __stcs(trow + l0 + i, t);           // streaming: T is written once, read by the inverse later
                     }
                 group_sync<N2>(group);

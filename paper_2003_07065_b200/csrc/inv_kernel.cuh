@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
                 const bool inm = upper && !inb && q > 0 && (unsigned)lm < (unsigned)a.bins;
                 const int li = inb ? lbase + n1 * zstep : lm;
                 float2 ta = make_float2(0.0f, 0.0f), tb = make_float2(0.0f, 0.0f);
+                SST_CHECK(!(inb || inm) || (li >= 0 && li < a.bins));
                 if ((inb || inm) && vA) ta = __ldg(TA + li);
                 if ((inb || inm) && vB) tb = __ldg(TB + li);
                 if (n1 == 0 && q == 0 && b == 0) { ta.y = 0.0f; tb.y = 0.0f; }  // DC: real part only (R14)
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
             for (int kk = 0; kk < 64; ++kk) {
                 float2 t = v[kk];
                 if (kk != 0) t = cmulc(t, __ldg(a.tw + kk * N2 + tg));   // W_N^{-tg kk}
+                SST_CHECK(kk * STRIDE + tg < CAP);
                 buf[kk * STRIDE + tg] = t;
             }
             group_sync<N2>(group);
@@ -235,7 +237,10 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
                 }
 #pragma unroll
                 for (int jj = 0; jj < PPT; ++jj)
-                    if (slot[jj] >= 0) ring[slot[jj]] += y[jj].x;
+                    if (slot[jj] >= 0) {
+                        SST_CHECK(slot[jj] < a.lay.ring);
+                        ring[slot[jj]] += y[jj].x;
+                    }
                 __syncthreads();
                 if (hasB) {
 #pragma unroll
@@ -255,13 +260,17 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
             *slot = 0.0f;
             if (s < 0 || s >= a.n) continue;
             if (!first_cta && s < left_end) {
+                SST_CHECK(s - g_lo >= 0 && s - g_lo < a.seam_len);
                 a.seam[((int64_t)blockIdx.x * 2 + 0) * a.seam_len + (s - g_lo)] = val;
             } else if (!last_cta && s >= right_start) {
+                SST_CHECK(s - right_start >= 0 && s - right_start < a.seam_len);
                 a.seam[((int64_t)blockIdx.x * 2 + 1) * a.seam_len + (s - right_start)] = val;
             } else if (a.normalize) {
                 // (a per-sample 32-bit mod_pos here measured 4 % slower on C4: one more live register)
+                SST_CHECK(s - a.y_off >= 0 && s - a.y_off < a.y_len);
                 a.y[s - a.y_off] = val * inv_norm(s, a) * a.out_scale;
             } else {
+                SST_CHECK(s - a.y_off >= 0 && s - a.y_off < a.y_len);
                 a.y[s - a.y_off] += val;
             }
         }

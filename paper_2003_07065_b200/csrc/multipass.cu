@@ -275,6 +275,7 @@ __global__ void __launch_bounds__(kBinThreads) mp_bins_kernel(const FwdArgs a, c
             float mag4;
             bool unsure;
             const int l = bin_target<false>(a, gam4, cm, km, k, Z[k], Z[(N - k) & (N - 1)], PQ, UV, mag4, unsure);
+            SST_CHECK(k < K);
             lrow[k] = unsure ? -4 : l;                                 // -4: pending fp64 decision
         }
         __syncthreads();
@@ -327,6 +328,7 @@ __global__ void __launch_bounds__(kBinThreads) mp_bins_kernel(const FwdArgs a, c
                 for (int k = threadIdx.x; k < K; k += kBinThreads) {
                     const int lr = lrow[k] - l0;
                     if (lr >= 0 && lr < lc) {                               // -1/-2 give lr < 0 for l0 = 0
+                        SST_CHECK(2 * lr + 1 < 2 * ch);
                         const float2 S = S_of(k);
                         long long xr, xi;
                         asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xr) : "f"(S.x * scale));
@@ -442,6 +444,7 @@ __global__ void __launch_bounds__(256) mp_ola_kernel(const MpInvArgs a, int64_t 
     if (m_hi > a.frame_end - 1) m_hi = a.frame_end - 1;
     float acc = 0.0f;
     for (int64_t m = m_lo; m <= m_hi; ++m) acc += a.wf[(m - fb) * a.L + (s - m * H + a.c)];
+    SST_CHECK(s - a.y_off >= 0 && s - a.y_off < a.y_len);
     a.y[s - a.y_off] += acc;
 }
 

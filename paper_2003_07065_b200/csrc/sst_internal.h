@@ -5,6 +5,24 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// SST_BOUNDS (debug build libsst_bounds.so, `python __graft_entry__.py build bounds`): device-side
+// checks of every shared-memory and global index the kernels compute, and a spin limit on mbarrier
+// waits (a lost TMA completion traps instead of hanging).  compute-sanitizer is closed on the GPU
+// pool, so `SST_LIB=bounds pytest -m gpu` is the memory-safety run.
+#ifdef SST_BOUNDS
+#include <cstdio>
+#define SST_CHECK(cond)                                                                            \
+    do {                                                                                           \
+        if (!(cond)) {                                                                             \
+            printf("SST_BOUNDS: %s failed at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                             \
+            __trap();                                                                              \
+        }                                                                                          \
+    } while (0)
+#else
+#define SST_CHECK(cond) ((void)0)
+#endif
+
 namespace sst {
 
 enum FwdMode : int { kModeForward = 0, kModeStft = 1, kModeTargets = 2, kModeAbsmax = 3 };

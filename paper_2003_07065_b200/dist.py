@@ -187,6 +187,9 @@ def gather_band(T_local: torch.Tensor, sh: Shard, dst: int = 0, group=None):
     real view; ranks' row counts may differ by one.  Returns [F, B] on dst, None elsewhere."""
     if sh.world == 1:
         return T_local
+    if _staged(T_local, group):
+        out = gather_band(T_local.cpu(), sh, dst, group)
+        return None if out is None else out.to(T_local.device)
     rows_per = [frames_of_rank(sh, r) for r in range(sh.world)]
     mx = max(rows_per)
     real = torch.view_as_real(T_local.contiguous())                  # [rows, B, 2]
