@@ -242,6 +242,12 @@ sst_status sst_zone_mask(sst_plan* plan, float* T, int64_t ldT, int64_t rows, co
                          int32_t keep_inside, void* stream);
 sst_status sst_mode_full(sst_plan* plan, const float* T, int64_t ldT, int64_t rows, const int32_t* path,
                          int32_t half, float* x, void* stream);
+/* Mode retrieval by the downsampled inverse (§2.3, Eq. 25-26) with the zone applied inside
+ * the inverse kernel's loads of T (no masked copy of T, no extra pass): entries with
+ * |l - path[m]| <= half are used (keep_inside = 1) or only the others (keep_inside = 0).
+ * T as sst_inverse (all F rows); path device int32 [F]; y device float [N], overwritten.        */
+sst_status sst_inverse_zone(sst_plan* plan, const float* T, int64_t ldT, const int32_t* path, int32_t half,
+                            int32_t keep_inside, float* y, void* stream);
 
 /* ---------------------------------------------------------------- debug / parity ----------- */
 

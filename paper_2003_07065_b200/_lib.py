@@ -94,6 +94,7 @@ SIGNATURES = {
     "sst_ridge": (_i32, [_vp, _vp, _i64, _dbl, _i32, _i32, _vp, _vp, _vp]),
     "sst_zone_mask": (_i32, [_vp, _vp, _i64, _i64, _vp, _i32, _i32, _vp]),
     "sst_mode_full": (_i32, [_vp, _vp, _i64, _i64, _vp, _i32, _vp, _vp]),
+    "sst_inverse_zone": (_i32, [_vp, _vp, _i64, _vp, _i32, _i32, _vp, _vp]),
     "sst_stft": (_i32, [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp]),
     "sst_targets": (_i32, [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp]),
     "sst_absmax": (_i32, [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp]),

@@ -83,6 +83,9 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
             const bool vB = vA && fA + 1 < f_hi;
             const float2* TA = a.T + (vA ? fA : f_lo) * a.ldT;
             const float2* TB = vB ? TA + a.ldT : TA;
+            // mode retrieval zone: centre bins of frames A and B (none: keep everything)
+            const int zA = a.zone_path && vA ? __ldg(a.zone_path + fA) : 0;
+            const int zB = a.zone_path && vB ? __ldg(a.zone_path + fA + 1) : 0;
             float2 v[64];
             // band entries q in [k1, k2): l = z (q - k1) + b; mirror entries: l' = z (N - k1 - q) - b
             const int zstep = zoom * N2;                           // l step per row n1
@@ -105,8 +108,10 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
                 const int li = inb ? lbase + n1 * zstep : lm;
                 float2 ta = make_float2(0.0f, 0.0f), tb = make_float2(0.0f, 0.0f);
                 SST_CHECK(!(inb || inm) || (li >= 0 && li < a.bins));
-                if ((inb || inm) && vA) ta = __ldg(TA + li);
-                if ((inb || inm) && vB) tb = __ldg(TB + li);
+                const bool okA = !a.zone_path || ((abs(li - zA) <= a.zone_half) == (bool)a.zone_keep);
+                const bool okB = !a.zone_path || ((abs(li - zB) <= a.zone_half) == (bool)a.zone_keep);
+                if ((inb || inm) && vA && okA) ta = __ldg(TA + li);
+                if ((inb || inm) && vB && okB) tb = __ldg(TB + li);
                 if (n1 == 0 && q == 0 && b == 0) { ta.y = 0.0f; tb.y = 0.0f; }  // DC: real part only (R14)
                 if (n1 == 32 && q == N / 2 && b == 0) { ta.y = 0.0f; tb.y = 0.0f; }   // Nyquist (full band only)
                 v[n1] = inb ? make_float2(ta.x - tb.y, ta.y + tb.x)    // H_A + i H_B

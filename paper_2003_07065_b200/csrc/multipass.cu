@@ -50,6 +50,8 @@ struct MpPass {
     const float2* T;
     int64_t ldT, nfr;
     int zoom, k1, bins;
+    const int32_t* zone_path;       // mode retrieval zone (row 0 = first frame of the chunk), or null
+    int zone_half, zone_keep;
 };
 
 __device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
@@ -89,8 +91,11 @@ __device__ __forceinline__ float2 load_elem(const MpPass& a, int64_t t, int n) {
         if (!(inb || inm)) return make_float2(0.0f, 0.0f);
         const int li = inb ? a.zoom * (q - a.k1) + b : lm;
         float2 ta = make_float2(0.0f, 0.0f), tb = make_float2(0.0f, 0.0f);
-        if (vA) ta = __ldg(a.T + fA * a.ldT + li);
-        if (vB) tb = __ldg(a.T + (fA + 1) * a.ldT + li);
+        auto zok = [&](int64_t f) {
+            return !a.zone_path || ((abs(li - __ldg(a.zone_path + f)) <= a.zone_half) == (bool)a.zone_keep);
+        };
+        if (vA && zok(fA)) ta = __ldg(a.T + fA * a.ldT + li);
+        if (vB && zok(fA + 1)) tb = __ldg(a.T + (fA + 1) * a.ldT + li);
         if (b == 0 && (q == 0 || q == a.N / 2)) { ta.y = 0.0f; tb.y = 0.0f; }   // DC / Nyquist real (R14)
         return inb ? make_float2(ta.x - tb.y, ta.y + tb.x) : make_float2(ta.x + tb.y, tb.x - ta.y);
     }
@@ -386,8 +391,10 @@ __global__ void __launch_bounds__(256) mp_direct_kernel(const MpInvArgs a) {
     const int B = a.bins;
     const int64_t zN = (int64_t)a.zoom * a.nfft;
     const int64_t j0 = (int64_t)a.zoom * a.k1;
+    const int zc = a.zone_path ? __ldg(a.zone_path + f) : 0;
     for (int l = threadIdx.x; l < B; l += 256) {
         float2 t = a.T[f * a.ldT + l];
+        if (a.zone_path && ((abs(l - zc) <= a.zone_half) != (bool)a.zone_keep)) t = make_float2(0.0f, 0.0f);
         if (j0 + l == 0 || 2 * (j0 + l) == zN) t = make_float2(0.5f * t.x, 0.0f);
         trow[l] = t;
     }
@@ -520,6 +527,9 @@ cudaError_t launch_mp_inverse_accumulate(const MpInvArgs& a, cudaStream_t s) {
     p.zoom = a.zoom;
     p.k1 = a.k1;
     p.bins = a.bins;
+    p.zone_path = a.zone_path;
+    p.zone_half = a.zone_half;
+    p.zone_keep = a.zone_keep;
     p.out = a.buf0;
     e = run_pass<kLoadInv, +1>(p, 1, s);
     if (e != cudaSuccess) return e;

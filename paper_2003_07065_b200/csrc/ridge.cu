@@ -3,7 +3,10 @@
 //  ridge_emission: E[m, l] = log(|T[m, l]| + eps), eps = 1e-12 max|T|  (fp64)
 //  ridge_dp:       penalised dynamic programme over frames, one CTA, all in fp64:
 //                  V_m[l] = E[m, l] + max_{l'} (V_{m-1}[l'] - lambda (l - l')^2)  (smallest l').
-//                  Because the transition score has increasing differences in (l, l'), the
+//                  Per frame, when the range R of V_{m-1} allows (W = ceil(sqrt(R/lambda)) + 1 <= 192),
+//                  each l scans only [l - W, l + W]: every l' outside scores below l' = l, so this is
+//                  the brute-force argmax with its ties (one barrier per frame).  Otherwise:
+//                  because the transition score has increasing differences in (l, l'), the
 //                  smallest maximiser opt(l) is non-decreasing in l, so each frame is solved
 //                  exactly by level-synchronous divide and conquer: level d fixes the points
 //                  whose 1-based index has lowest set bit S/2^(d+1) (S = pow2 > B), searching
@@ -72,6 +75,15 @@ __device__ __forceinline__ void scan_thread(const double* V, int l, int a0, int 
     }
 }
 
+// ordered-key warp max / min of fp64 values (for the frame's range of V)
+__device__ __forceinline__ void warp_minmax(double& mx, double& mn) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+}
+
 __global__ void __launch_bounds__(kRidgeThreads, 1)
 ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int suppress, const double* floor_in,
                 int32_t* back, int32_t* paths) {
@@ -80,74 +92,121 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
     double* Vn = V + cols;                                 // [cols] current frame
     double* En = Vn + cols;                                // [cols] emission row of the frame, prefetched
     int* opt = reinterpret_cast<int*>(En + cols);          // [cols]
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = kRidgeThreads / 32;
+    __shared__ double pmax[2][NW], pmin[2][NW];            // per-warp range partials of V, by frame parity
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int S = 1;
     while (S <= cols) S <<= 1;                             // S > cols: every p in [1, cols] has a level
     int levels = 0;
     while ((1 << levels) < S) ++levels;
     const double floor_e = *floor_in;
+    // windowed step: with R = max V - min V, a source bin l' with lam (l - l')^2 > R scores below the
+    // candidate l' = l, so the smallest maximiser lies within W = ceil(sqrt(R / lam)) + 1 of l; an
+    // ascending scan of that window with a strict > is the brute-force argmax (same ties)
+    constexpr int kWin = 192;
 
     for (int q = 0; q < count; ++q) {
-        for (int l = tid; l < cols; l += kRidgeThreads) V[l] = E[l];
+        {
+            double mx = -INFINITY, mn = INFINITY;
+            for (int l = tid; l < cols; l += kRidgeThreads) {
+                const double v = E[l];
+                V[l] = v;
+                mx = fmax(mx, v);
+                mn = fmin(mn, v);
+            }
+            warp_minmax(mx, mn);
+            if (lane == 0) { pmax[0][warp] = mx; pmin[0][warp] = mn; }
+        }
         if (rows > 1)
             for (int l = tid; l < cols; l += kRidgeThreads) __pipeline_memcpy_async(En + l, E + cols + l, sizeof(double));
         __pipeline_commit();
         __syncthreads();
         for (int64_t m = 1; m < rows; ++m) {
             int32_t* bk = back + m * cols;
-            for (int d = 0; d < levels; ++d) {
-                const int step = S >> (d + 1);                 // points p = step (2i + 1), p <= cols
-                const int npts = (cols >= step) ? ((cols - step) / (2 * step) + 1) : 0;
-                if (npts <= NW) {
-                    // one warp per point: lanes split the candidate range, then a warp argmax
-                    for (int i = warp; i < npts; i += NW) {
-                        const int p = step * (2 * i + 1), l = p - 1;
-                        const int a0 = (p - step >= 1) ? opt[p - step - 1] : 0;
-                        const int a1 = (p + step <= cols) ? opt[p + step - 1] : cols - 1;
-                        double best = -INFINITY;
-                        int arg = a0;
-                        for (int a = a0 + lane; a <= a1; a += 32) {
-                            const double dd = (double)(l - a);
-                            const double v = V[a] - lam * (dd * dd);
-                            if (v > best) { best = v; arg = a; }
-                        }
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) {
-                            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                            const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
-                            if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
-                        }
-                        if (lane == 0) opt[l] = arg;
+            const int par = (int)((m - 1) & 1);
+            double R = 0.0, vmx = -INFINITY, vmn = INFINITY;
+#pragma unroll 4
+            for (int w = 0; w < NW; ++w) { vmx = fmax(vmx, pmax[par][w]); vmn = fmin(vmn, pmin[par][w]); }
+            R = vmx - vmn;
+            const double wd = (lam > 0.0 && R < 1e300) ? ceil(sqrt(R / lam)) + 1.0 : 1e300;
+            const bool windowed = wd <= (double)kWin;
+            double mx = -INFINITY, mn = INFINITY;
+            if (windowed) {
+                const int W = (int)wd;
+                __pipeline_wait_prior(0);                     // this frame's emissions (own copies)
+                for (int l = tid; l < cols; l += kRidgeThreads) {
+                    const int a0 = max(0, l - W), a1 = min(cols - 1, l + W);
+                    double best = -INFINITY;
+                    int arg = a0;
+                    for (int a = a0; a <= a1; ++a) {
+                        const double dd = (double)(l - a);
+                        const double v = V[a] - lam * (dd * dd);
+                        if (v > best) { best = v; arg = a; }
                     }
-                } else {
-                    for (int i = tid; i < npts; i += kRidgeThreads) {
-                        const int p = step * (2 * i + 1), l = p - 1;
-                        const int a0 = (p - step >= 1) ? opt[p - step - 1] : 0;
-                        const int a1 = (p + step <= cols) ? opt[p + step - 1] : cols - 1;
-                        double best;
-                        int arg;
-                        scan_thread(V, l, a0, a1, lam, best, arg);
-                        opt[l] = arg;
-                    }
+                    const double vn = En[l] + best;
+                    Vn[l] = vn;
+                    bk[l] = arg;
+                    mx = fmax(mx, vn);
+                    mn = fmin(mn, vn);
                 }
-                __syncthreads();
+            } else {
+                for (int d = 0; d < levels; ++d) {
+                    const int step = S >> (d + 1);                 // points p = step (2i + 1), p <= cols
+                    const int npts = (cols >= step) ? ((cols - step) / (2 * step) + 1) : 0;
+                    if (npts <= NW) {
+                        // one warp per point: lanes split the candidate range, then a warp argmax
+                        for (int i = warp; i < npts; i += NW) {
+                            const int p = step * (2 * i + 1), l = p - 1;
+                            const int a0 = (p - step >= 1) ? opt[p - step - 1] : 0;
+                            const int a1 = (p + step <= cols) ? opt[p + step - 1] : cols - 1;
+                            double best = -INFINITY;
+                            int arg = a0;
+                            for (int a = a0 + lane; a <= a1; a += 32) {
+                                const double dd = (double)(l - a);
+                                const double v = V[a] - lam * (dd * dd);
+                                if (v > best) { best = v; arg = a; }
+                            }
+#pragma unroll
+                            for (int o = 16; o > 0; o >>= 1) {
+                                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                                const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+                                if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
+                            }
+                            if (lane == 0) opt[l] = arg;
+                        }
+                    } else {
+                        for (int i = tid; i < npts; i += kRidgeThreads) {
+                            const int p = step * (2 * i + 1), l = p - 1;
+                            const int a0 = (p - step >= 1) ? opt[p - step - 1] : 0;
+                            const int a1 = (p + step <= cols) ? opt[p + step - 1] : cols - 1;
+                            double best;
+                            int arg;
+                            scan_thread(V, l, a0, a1, lam, best, arg);
+                            opt[l] = arg;
+                        }
+                    }
+                    __syncthreads();
+                }
+                __pipeline_wait_prior(0);                         // this frame's emissions (own copies)
+                for (int l = tid; l < cols; l += kRidgeThreads) {
+                    const int a = opt[l];
+                    const double dd = (double)(l - a);
+                    const double vn = En[l] + (V[a] - lam * (dd * dd));
+                    Vn[l] = vn;
+                    bk[l] = a;
+                    mx = fmax(mx, vn);
+                    mn = fmin(mn, vn);
+                }
             }
-            __pipeline_wait_prior(0);                         // this frame's emissions (own copies)
-            for (int l = tid; l < cols; l += kRidgeThreads) {
-                const int a = opt[l];
-                const double dd = (double)(l - a);
-                Vn[l] = En[l] + (V[a] - lam * (dd * dd));
-                bk[l] = a;
-            }
+            warp_minmax(mx, mn);
+            if (lane == 0) { pmax[par ^ 1][warp] = mx; pmin[par ^ 1][warp] = mn; }
             __syncthreads();
-            for (int l = tid; l < cols; l += kRidgeThreads) V[l] = Vn[l];
+            { double* t = V; V = Vn; Vn = t; }
             // prefetch the next frame's emission row (each thread copies the entries it reads)
             if (m + 1 < rows)
                 for (int l = tid; l < cols; l += kRidgeThreads)
                     __pipeline_memcpy_async(En + l, E + (m + 1) * cols + l, sizeof(double));
             __pipeline_commit();
-            __syncthreads();
         }
         // final argmax (smallest index), traceback, suppression
         if (warp == 0) {
@@ -172,6 +231,9 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
             }
         }
         __syncthreads();
+        // V / Vn swapped an odd or even number of times: restore the buffer order for the next ridge
+        V = reinterpret_cast<double*>(sm);
+        Vn = V + cols;
         if (q + 1 < count) {
             const int32_t* path = paths + (int64_t)q * rows;
             for (int64_t m = tid; m < rows; m += kRidgeThreads) {

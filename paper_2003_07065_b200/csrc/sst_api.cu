@@ -351,7 +351,8 @@ cudaError_t launch_fwd_any(const sst_plan* pl, const sst::FwdArgs& a, int mode, 
 // y (+)= the inverse of frames [fb, fe) on the multi-pass path (chunks of 2 mp_inv_pairs frames)
 cudaError_t mp_inverse_accumulate(const sst_plan* pl, const float2* T, int64_t ldT, int64_t fb, int64_t fe,
                                   int32_t k1, int32_t bins, int32_t zoom, float* y, int64_t y_off, int64_t y_len,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, const int32_t* zone_path = nullptr, int32_t zone_half = 0,
+                                  int32_t zone_keep = 1) {
     sst::MpInvArgs a{};
     a.ldT = ldT;
     a.n = pl->lay.n;
@@ -384,6 +385,9 @@ cudaError_t mp_inverse_accumulate(const sst_plan* pl, const float2* T, int64_t l
         a.frame_begin = c0;
         a.frame_end = std::min<int64_t>(fe, c0 + step);
         a.T = T + (c0 - fb) * ldT;
+        a.zone_path = zone_path ? zone_path + (c0 - fb) : nullptr;
+        a.zone_half = zone_half;
+        a.zone_keep = zone_keep;
         cudaError_t e = sst::launch_mp_inverse_accumulate(a, st);
         if (e != cudaSuccess) return e;
     }
@@ -820,19 +824,24 @@ static sst::InvArgs istft_args(const sst_plan* pl, const float* S, int64_t ldS, 
 }
 
 static sst_status run_inverse(sst_plan* plan, const float* T, int64_t ldT, int64_t fb, int64_t fe, float* y, int64_t y_off,
-                              int64_t y_len, int normalize, void* stream) {
+                              int64_t y_len, int normalize, void* stream, const int32_t* zone_path = nullptr,
+                              int32_t zone_half = 0, int32_t zone_keep = 1) {
     if (plan->mp) {
         cudaStream_t st = (cudaStream_t)stream;
         sst_status s = SST_OK;
         if (normalize) s = cuda_status(plan, cudaMemsetAsync(y, 0, sizeof(float) * (size_t)y_len, st), "memset");
         if (s != SST_OK) return s;
         s = cuda_status(plan, mp_inverse_accumulate(plan, reinterpret_cast<const float2*>(T), ldT, fb, fe, plan->lay.k1,
-                                                    plan->lay.bins, plan->lay.zoom, y, y_off, y_len, st), "inverse launch");
+                                                    plan->lay.bins, plan->lay.zoom, y, y_off, y_len, st, zone_path,
+                                                    zone_half, zone_keep), "inverse launch");
         if (s != SST_OK || !normalize) return s;
         return sst_inverse_finalize(plan, y, y_off, y_len, stream);
     }
     int grid = 0;
     sst::InvArgs a = inv_args(plan, T, ldT, fb, fe, y, y_off, y_len, normalize, &grid);
+    a.zone_path = zone_path;
+    a.zone_half = zone_half;
+    a.zone_keep = zone_keep;
     cudaStream_t st = (cudaStream_t)stream;
     sst_status s = cuda_status(plan, sst::launch_inverse(a, grid, st), "inverse launch");
     if (s != SST_OK) return s;
@@ -845,6 +854,15 @@ sst_status sst_inverse(sst_plan* plan, const float* T, int64_t ldT, float* y, vo
     if (ldT < plan->lay.bins) return fail(plan, SST_E_INVALID_ARGUMENT, "ldT < B");
     DeviceGuard guard(plan->device);
     return run_inverse(plan, T, ldT, 0, plan->lay.frames, y, 0, plan->lay.n, 1, stream);
+}
+
+sst_status sst_inverse_zone(sst_plan* plan, const float* T, int64_t ldT, const int32_t* path, int32_t half,
+                            int32_t keep_inside, float* y, void* stream) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    if (!T || !y || !path) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL T, path or y");
+    if (ldT < plan->lay.bins || half < 0) return fail(plan, SST_E_INVALID_ARGUMENT, "ldT < B or half < 0");
+    DeviceGuard guard(plan->device);
+    return run_inverse(plan, T, ldT, 0, plan->lay.frames, y, 0, plan->lay.n, 1, stream, path, half, keep_inside ? 1 : 0);
 }
 
 sst_status sst_inverse_accumulate(sst_plan* plan, const float* T, int64_t ldT, int64_t frame_begin, int64_t frame_end,

@@ -139,6 +139,11 @@ struct InvArgs {
     float* seam;                      // [ctas][2][seam_len] partial sums
     int32_t seam_len;                 // L - hop
     int64_t frames_per_cta;           // contiguous chunk per CTA (>= ceil(L/hop))
+    // zone of mode retrieval (R22) applied to the T loads: entry l of frame m is used only if
+    // (|l - zone_path[m]| <= zone_half) == zone_keep; zone_path == nullptr: no zone.  zone_path[0]
+    // is frame frame_begin.
+    const int32_t* zone_path;
+    int32_t zone_half, zone_keep;
 };
 
 // Large-N_f multi-pass path (multipass.cu), used for kMaxFusedNfft < N_f <= kMaxNfft
@@ -158,6 +163,8 @@ struct MpInvArgs {
     float* wf;                        // [F][L] windowed frames
     float* y; int64_t y_off, y_len;   // y += (accumulate)
     int direct;                       // 1: direct band sum per frame (mp_direct_kernel) instead of FFTs
+    const int32_t* zone_path;         // as InvArgs (row 0 = frame frame_begin)
+    int32_t zone_half, zone_keep;
 };
 
 void mp_factor(int nfft, int* r1, int* m);

@@ -262,10 +262,20 @@ class Plan:
                                 _stream(self.device)), self._h)
         return T
 
-    def retrieve_mode(self, T: torch.Tensor, path: torch.Tensor, half: int) -> torch.Tensor:
-        """§2.3: zone-masked copy of T through the downsampled inverse (Eq. 25-26)."""
-        Tm = self.zone_mask(T.clone(), path, half)
-        return self.inverse(Tm)
+    def retrieve_mode(self, T: torch.Tensor, path: torch.Tensor, half: int, keep_inside: bool = True,
+                      out: torch.Tensor | None = None) -> torch.Tensor:
+        """§2.3 mode retrieval: the downsampled inverse (Eq. 25-26) of T restricted to the zone
+        |l - path[m]| <= half (sst_inverse_zone: the zone is applied inside the inverse's T loads,
+        T is not copied or modified)."""
+        _rows(T, self.frames, self.bins, "T")
+        if path.numel() < self.frames:
+            raise ValueError("path must have one bin per frame")
+        if out is None:
+            out = torch.empty(self.n, dtype=torch.float32, device=self.device)
+        L.check(L.sst_inverse_zone(self._h, _ptr(T, self.device, torch.complex64, "T"), T.shape[1],
+                                   _ptr(path, self.device, torch.int32, "path"), int(half), int(bool(keep_inside)),
+                                   _ptr(out, self.device, torch.float32, "y"), _stream(self.device)), self._h)
+        return out
 
     def mode_full(self, T: torch.Tensor, path: torch.Tensor, half: int) -> torch.Tensor:
         """sst_mode_full: Eq. 15 (H_t = 1), float32 [rows]."""

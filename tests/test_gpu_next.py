@@ -139,11 +139,27 @@ def _oracle_ridges(To, lam, count, suppress=3):
     return np.array(out)
 
 
+@pytest.mark.parametrize("hop,zoom,lam,count", [(2, 1, 0.01, 2), (4, 2, 0.05, 2), (1, 1, 0.0, 1), (2, 1, 1e-4, 2)])
+def test_ridge_dp_exact_on_identical_emissions(P, hop, zoom, lam, count):
+    """Reading R22's DP on the GPU (one CTA, fp64; per frame the windowed scan when the range of V
+    allows it, else the exact divide and conquer -- lambda = 0 and 1e-4 take the latter, 0.01 / 0.05
+    the former) fed the ORACLE's emissions E: paths identical to the oracle's O(F B^2) recurrence
+    on every frame, suppression included (same fp64 arithmetic, same lowest-bin ties)."""
+    plan, x, T, To, g, c = _two_tone_plan(P, hop=hop, zoom=zoom)
+    Eo = O.ridge_emission(To)
+    floor = float(np.log(1e-12 * np.abs(To).max()))
+    E = torch.from_numpy(np.ascontiguousarray(Eo)).to(DEV)
+    fl = torch.tensor(floor, dtype=torch.float64, device=DEV)
+    paths = plan.ridge(E, fl, lam, count, 3).cpu().numpy()
+    po = _oracle_ridges(To, lam, count)
+    assert np.array_equal(paths, po)
+
+
 @pytest.mark.parametrize("hop,zoom,lam,count", [(2, 1, 0.01, 2), (4, 2, 0.05, 2), (1, 1, 0.0, 1)])
-def test_ridge_paths_match_oracle(P, hop, zoom, lam, count):
-    """GPU ridges of the GPU plane (one-CTA fp64 DP, exact divide and conquer per frame) vs the
-    oracle's O(F B^2) recurrence on the oracle's plane: the same path on >= 99 % of the frames
-    (the planes differ by fp32 rounding and boundary flips, which can move a near-tie)."""
+def test_ridge_paths_end_to_end(P, hop, zoom, lam, count):
+    """End to end on the GPU (GPU plane -> GPU emissions -> GPU DP) vs the oracle end to end: the
+    two planes differ by fp32 rounding (the emissions by ~1e-7), which can only move an exact
+    near-tie of the DP, so the paths agree on >= 99 % of the frames and find both components."""
     plan, x, T, To, g, c = _two_tone_plan(P, hop=hop, zoom=zoom)
     paths = plan.ridges(T, lam, count, 3).cpu().numpy()
     po = _oracle_ridges(To, lam, count)
@@ -167,6 +183,34 @@ def test_zone_mask_and_retrieve_mode(P):
     assert not torch.any(Tm[outside]) and not torch.any(Ti[~outside])
     y = plan.retrieve_mode(T, path, 10).cpu().numpy()
     yo = O.retrieve_mode(To, O.zone_mask(po, 10, plan.bins), g, c, 4, 512, 2, 0, x.size)
+    assert rel(y, yo) <= 1e-4
+    # the zone is applied inside the inverse kernel (sst_inverse_zone): T untouched, the masked-copy
+    # route gives the same samples, and the complementary zones add up to the whole inverse (Eq. 26
+    # is linear in T)
+    T0 = T.clone()
+    y_out = plan.retrieve_mode(T, path, 10, keep_inside=False)
+    assert torch.equal(T, T0)
+    assert rel(plan.inverse(Tm).cpu().numpy(), y) <= 1e-6
+    assert rel(plan.inverse(Ti).cpu().numpy(), y_out.cpu().numpy()) <= 1e-6
+    assert rel(y + y_out.cpu().numpy(), plan.inverse(T).cpu().numpy()) <= 1e-5
+
+
+@pytest.mark.parametrize("mp_path", ["fft", "direct"])
+def test_retrieve_mode_multipass(P, mp_path, monkeypatch):
+    """The zone inside the large-N_f inverse (both formulations) against the oracle."""
+    monkeypatch.setenv("SST_MP_INVERSE", mp_path)
+    N, fs, L, sigma, hop, nfft, f1, f2, z = 60000, 16384.0, 4001, 500.0, 512, 16384, 1000.0, 3000.0, 2
+    t = np.arange(N) / fs
+    x = (np.cos(2 * np.pi * (1500 * t + 80 * t * t)) + 0.7 * np.cos(2 * np.pi * 2500 * t)
+         + 0.05 * np.random.default_rng(5).standard_normal(N)).astype(np.float32)
+    g, gd, c = O.gaussian_window(L, sigma)
+    plan = P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=1e-6, device=0)
+    T = plan.forward(torch.from_numpy(x).to(DEV))
+    To = O.sst_forward(x.astype(np.float64), g, gd, c, hop, nfft, fs, f1, f2, z, 1e-6)
+    po = _oracle_ridges(To, 0.01, 1)[0]
+    path = torch.from_numpy(po.astype(np.int32)).to(DEV)
+    y = plan.retrieve_mode(T, path, 40).cpu().numpy()
+    yo = O.retrieve_mode(To, O.zone_mask(po, 40, plan.bins), g, c, hop, nfft, z, plan.layout["k1"], N)
     assert rel(y, yo) <= 1e-4
 
 
