@@ -3,15 +3,14 @@
 //  ridge_emission: E[m, l] = log(|T[m, l]| + eps), eps = 1e-12 max|T|  (fp64)
 //  ridge_dp:       penalised dynamic programme over frames, one CTA, all in fp64:
 //                  V_m[l] = E[m, l] + max_{l'} (V_{m-1}[l'] - lambda (l - l')^2)  (smallest l').
-//                  Per frame, when the range R of V_{m-1} allows (W = ceil(sqrt(R/lambda)) + 1 <= 192),
-//                  each l scans only [l - W, l + W]: every l' outside scores below l' = l, so this is
-//                  the brute-force argmax with its ties (one barrier per frame).  Otherwise:
-//                  because the transition score has increasing differences in (l, l'), the
+//                  Because the transition score has increasing differences in (l, l'), the
 //                  smallest maximiser opt(l) is non-decreasing in l, so each frame is solved
 //                  exactly by level-synchronous divide and conquer: level d fixes the points
 //                  whose 1-based index has lowest set bit S/2^(d+1) (S = pow2 > B), searching
 //                  only between the optima of their already-solved neighbours: O(B log B) per
-//                  frame instead of O(B^2), same result.  Backpointers (int32) go to global
+//                  frame instead of O(B^2), same result; each level gives its points 1024/P threads
+//                  (segmented warp argmax), so a level costs a few candidates per thread plus one
+//                  barrier.  Backpointers (int32) go to global
 //                  memory; one thread traces the path back.  After each ridge the zone
 //                  +-suppress bins is set to the floor emission log(eps).
 //  zone_mask:      T outside (or inside) the zone |l - path[m]| <= half set to zero.
@@ -64,26 +63,6 @@ cudaError_t launch_ridge_emission(const float2* T, int64_t rows, int64_t cols, i
 // ------------------------------------------------------------------------------ DP ------------
 constexpr int kRidgeThreads = 1024;
 
-// smallest maximiser of V[a] - lam (l - a)^2 over a in [a0, a1] by one thread
-__device__ __forceinline__ void scan_thread(const double* V, int l, int a0, int a1, double lam, double& best, int& arg) {
-    best = -INFINITY;
-    arg = a0;
-    for (int a = a0; a <= a1; ++a) {
-        const double d = (double)(l - a);
-        const double v = V[a] - lam * (d * d);
-        if (v > best) { best = v; arg = a; }
-    }
-}
-
-// ordered-key warp max / min of fp64 values (for the frame's range of V)
-__device__ __forceinline__ void warp_minmax(double& mx, double& mn) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    }
-}
-
 __global__ void __launch_bounds__(kRidgeThreads, 1)
 ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int suppress, const double* floor_in,
                 int32_t* back, int32_t* paths) {
@@ -92,114 +71,63 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
     double* Vn = V + cols;                                 // [cols] current frame
     double* En = Vn + cols;                                // [cols] emission row of the frame, prefetched
     int* opt = reinterpret_cast<int*>(En + cols);          // [cols]
-    constexpr int NW = kRidgeThreads / 32;
-    __shared__ double pmax[2][NW], pmin[2][NW];            // per-warp range partials of V, by frame parity
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
     int S = 1;
     while (S <= cols) S <<= 1;                             // S > cols: every p in [1, cols] has a level
     int levels = 0;
     while ((1 << levels) < S) ++levels;
     const double floor_e = *floor_in;
-    // windowed step: with R = max V - min V, a source bin l' with lam (l - l')^2 > R scores below the
-    // candidate l' = l, so the smallest maximiser lies within W = ceil(sqrt(R / lam)) + 1 of l; an
-    // ascending scan of that window with a strict > is the brute-force argmax (same ties)
-    constexpr int kWin = 192;
 
     for (int q = 0; q < count; ++q) {
-        {
-            double mx = -INFINITY, mn = INFINITY;
-            for (int l = tid; l < cols; l += kRidgeThreads) {
-                const double v = E[l];
-                V[l] = v;
-                mx = fmax(mx, v);
-                mn = fmin(mn, v);
-            }
-            warp_minmax(mx, mn);
-            if (lane == 0) { pmax[0][warp] = mx; pmin[0][warp] = mn; }
-        }
+        for (int l = tid; l < cols; l += kRidgeThreads) V[l] = E[l];
         if (rows > 1)
             for (int l = tid; l < cols; l += kRidgeThreads) __pipeline_memcpy_async(En + l, E + cols + l, sizeof(double));
         __pipeline_commit();
         __syncthreads();
         for (int64_t m = 1; m < rows; ++m) {
             int32_t* bk = back + m * cols;
-            const int par = (int)((m - 1) & 1);
-            double R = 0.0, vmx = -INFINITY, vmn = INFINITY;
-#pragma unroll 4
-            for (int w = 0; w < NW; ++w) { vmx = fmax(vmx, pmax[par][w]); vmn = fmin(vmn, pmin[par][w]); }
-            R = vmx - vmn;
-            const double wd = (lam > 0.0 && R < 1e300) ? ceil(sqrt(R / lam)) + 1.0 : 1e300;
-            const bool windowed = wd <= (double)kWin;
-            double mx = -INFINITY, mn = INFINITY;
-            if (windowed) {
-                const int W = (int)wd;
-                __pipeline_wait_prior(0);                     // this frame's emissions (own copies)
-                for (int l = tid; l < cols; l += kRidgeThreads) {
-                    const int a0 = max(0, l - W), a1 = min(cols - 1, l + W);
+            for (int d = 0; d < levels; ++d) {
+                const int step = S >> (d + 1);                 // points p = step (2i + 1), p <= cols
+                const int npts = (cols >= step) ? ((cols - step) / (2 * step) + 1) : 0;
+                // tpp threads per point (a power of two <= 32, so a point's threads share a warp): the
+                // ranges shrink like the point count grows, so each thread scans ~cols / kRidgeThreads
+                // candidates per level; segmented argmax over the tpp lanes (smallest index on ties)
+                int tpp = 32;
+                while (tpp > 1 && tpp * npts > kRidgeThreads) tpp >>= 1;
+                const int sub = lane & (tpp - 1);
+                const int groups = kRidgeThreads / tpp;
+                for (int i0 = 0; i0 < npts; i0 += groups) {
+                    const int i = i0 + tid / tpp;
+                    const bool live = i < npts;
+                    const int p = step * (2 * i + 1), l = p - 1;
+                    int a0 = 0, a1 = -1;
+                    if (live) {
+                        a0 = (p - step >= 1) ? opt[p - step - 1] : 0;
+                        a1 = (p + step <= cols) ? opt[p + step - 1] : cols - 1;
+                    }
                     double best = -INFINITY;
                     int arg = a0;
-                    for (int a = a0; a <= a1; ++a) {
+                    for (int a = a0 + sub; a <= a1; a += tpp) {
                         const double dd = (double)(l - a);
                         const double v = V[a] - lam * (dd * dd);
                         if (v > best) { best = v; arg = a; }
                     }
-                    const double vn = En[l] + best;
-                    Vn[l] = vn;
-                    bk[l] = arg;
-                    mx = fmax(mx, vn);
-                    mn = fmin(mn, vn);
-                }
-            } else {
-                for (int d = 0; d < levels; ++d) {
-                    const int step = S >> (d + 1);                 // points p = step (2i + 1), p <= cols
-                    const int npts = (cols >= step) ? ((cols - step) / (2 * step) + 1) : 0;
-                    if (npts <= NW) {
-                        // one warp per point: lanes split the candidate range, then a warp argmax
-                        for (int i = warp; i < npts; i += NW) {
-                            const int p = step * (2 * i + 1), l = p - 1;
-                            const int a0 = (p - step >= 1) ? opt[p - step - 1] : 0;
-                            const int a1 = (p + step <= cols) ? opt[p + step - 1] : cols - 1;
-                            double best = -INFINITY;
-                            int arg = a0;
-                            for (int a = a0 + lane; a <= a1; a += 32) {
-                                const double dd = (double)(l - a);
-                                const double v = V[a] - lam * (dd * dd);
-                                if (v > best) { best = v; arg = a; }
-                            }
-#pragma unroll
-                            for (int o = 16; o > 0; o >>= 1) {
-                                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                                const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
-                                if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
-                            }
-                            if (lane == 0) opt[l] = arg;
-                        }
-                    } else {
-                        for (int i = tid; i < npts; i += kRidgeThreads) {
-                            const int p = step * (2 * i + 1), l = p - 1;
-                            const int a0 = (p - step >= 1) ? opt[p - step - 1] : 0;
-                            const int a1 = (p + step <= cols) ? opt[p + step - 1] : cols - 1;
-                            double best;
-                            int arg;
-                            scan_thread(V, l, a0, a1, lam, best, arg);
-                            opt[l] = arg;
-                        }
+                    for (int o = tpp >> 1; o > 0; o >>= 1) {
+                        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                        const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+                        if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
                     }
-                    __syncthreads();
+                    if (live && sub == 0) opt[l] = arg;
                 }
-                __pipeline_wait_prior(0);                         // this frame's emissions (own copies)
-                for (int l = tid; l < cols; l += kRidgeThreads) {
-                    const int a = opt[l];
-                    const double dd = (double)(l - a);
-                    const double vn = En[l] + (V[a] - lam * (dd * dd));
-                    Vn[l] = vn;
-                    bk[l] = a;
-                    mx = fmax(mx, vn);
-                    mn = fmin(mn, vn);
-                }
+                __syncthreads();
             }
-            warp_minmax(mx, mn);
-            if (lane == 0) { pmax[par ^ 1][warp] = mx; pmin[par ^ 1][warp] = mn; }
+            __pipeline_wait_prior(0);                         // this frame's emissions (own copies)
+            for (int l = tid; l < cols; l += kRidgeThreads) {
+                const int a = opt[l];
+                const double dd = (double)(l - a);
+                Vn[l] = En[l] + (V[a] - lam * (dd * dd));
+                bk[l] = a;
+            }
             __syncthreads();
             { double* t = V; V = Vn; Vn = t; }
             // prefetch the next frame's emission row (each thread copies the entries it reads)
@@ -209,7 +137,7 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
             __pipeline_commit();
         }
         // final argmax (smallest index), traceback, suppression
-        if (warp == 0) {
+        if (tid < 32) {
             double best = -INFINITY;
             int arg = 0;
             for (int l = lane; l < cols; l += 32)
@@ -231,8 +159,7 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
             }
         }
         __syncthreads();
-        // V / Vn swapped an odd or even number of times: restore the buffer order for the next ridge
-        V = reinterpret_cast<double*>(sm);
+        V = reinterpret_cast<double*>(sm);                 // buffers back in their initial order
         Vn = V + cols;
         if (q + 1 < count) {
             const int32_t* path = paths + (int64_t)q * rows;
