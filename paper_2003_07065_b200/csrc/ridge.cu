@@ -8,9 +8,7 @@
 //                  exactly by level-synchronous divide and conquer: level d fixes the points
 //                  whose 1-based index has lowest set bit S/2^(d+1) (S = pow2 > B), searching
 //                  only between the optima of their already-solved neighbours: O(B log B) per
-//                  frame instead of O(B^2), same result; each level gives its points 1024/P threads
-//                  (segmented warp argmax), so a level costs a few candidates per thread plus one
-//                  barrier.  Backpointers (int32) go to global
+//                  frame instead of O(B^2), same result.  Backpointers (int32) go to global
 //                  memory; one thread traces the path back.  After each ridge the zone
 //                  +-suppress bins is set to the floor emission log(eps).
 //  zone_mask:      T outside (or inside) the zone |l - path[m]| <= half set to zero.
@@ -63,6 +61,17 @@ cudaError_t launch_ridge_emission(const float2* T, int64_t rows, int64_t cols, i
 // ------------------------------------------------------------------------------ DP ------------
 constexpr int kRidgeThreads = 1024;
 
+// smallest maximiser of V[a] - lam (l - a)^2 over a in [a0, a1] by one thread
+__device__ __forceinline__ void scan_thread(const double* V, int l, int a0, int a1, double lam, double& best, int& arg) {
+    best = -INFINITY;
+    arg = a0;
+    for (int a = a0; a <= a1; ++a) {
+        const double d = (double)(l - a);
+        const double v = V[a] - lam * (d * d);
+        if (v > best) { best = v; arg = a; }
+    }
+}
+
 __global__ void __launch_bounds__(kRidgeThreads, 1)
 ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int suppress, const double* floor_in,
                 int32_t* back, int32_t* paths) {
@@ -71,7 +80,8 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
     double* Vn = V + cols;                                 // [cols] current frame
     double* En = Vn + cols;                                // [cols] emission row of the frame, prefetched
     int* opt = reinterpret_cast<int*>(En + cols);          // [cols]
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kRidgeThreads / 32;
     int S = 1;
     while (S <= cols) S <<= 1;                             // S > cols: every p in [1, cols] has a level
     int levels = 0;
@@ -89,35 +99,37 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
             for (int d = 0; d < levels; ++d) {
                 const int step = S >> (d + 1);                 // points p = step (2i + 1), p <= cols
                 const int npts = (cols >= step) ? ((cols - step) / (2 * step) + 1) : 0;
-                // tpp threads per point (a power of two <= 32, so a point's threads share a warp): the
-                // ranges shrink like the point count grows, so each thread scans ~cols / kRidgeThreads
-                // candidates per level; segmented argmax over the tpp lanes (smallest index on ties)
-                int tpp = 32;
-                while (tpp > 1 && tpp * npts > kRidgeThreads) tpp >>= 1;
-                const int sub = lane & (tpp - 1);
-                const int groups = kRidgeThreads / tpp;
-                for (int i0 = 0; i0 < npts; i0 += groups) {
-                    const int i = i0 + tid / tpp;
-                    const bool live = i < npts;
-                    const int p = step * (2 * i + 1), l = p - 1;
-                    int a0 = 0, a1 = -1;
-                    if (live) {
-                        a0 = (p - step >= 1) ? opt[p - step - 1] : 0;
-                        a1 = (p + step <= cols) ? opt[p + step - 1] : cols - 1;
+                if (npts <= NW) {
+                    // one warp per point: lanes split the candidate range, then a warp argmax
+                    for (int i = warp; i < npts; i += NW) {
+                        const int p = step * (2 * i + 1), l = p - 1;
+                        const int a0 = (p - step >= 1) ? opt[p - step - 1] : 0;
+                        const int a1 = (p + step <= cols) ? opt[p + step - 1] : cols - 1;
+                        double best = -INFINITY;
+                        int arg = a0;
+                        for (int a = a0 + lane; a <= a1; a += 32) {
+                            const double dd = (double)(l - a);
+                            const double v = V[a] - lam * (dd * dd);
+                            if (v > best) { best = v; arg = a; }
+                        }
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                            const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+                            if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
+                        }
+                        if (lane == 0) opt[l] = arg;
                     }
-                    double best = -INFINITY;
-                    int arg = a0;
-                    for (int a = a0 + sub; a <= a1; a += tpp) {
-                        const double dd = (double)(l - a);
-                        const double v = V[a] - lam * (dd * dd);
-                        if (v > best) { best = v; arg = a; }
+                } else {
+                    for (int i = tid; i < npts; i += kRidgeThreads) {
+                        const int p = step * (2 * i + 1), l = p - 1;
+                        const int a0 = (p - step >= 1) ? opt[p - step - 1] : 0;
+                        const int a1 = (p + step <= cols) ? opt[p + step - 1] : cols - 1;
+                        double best;
+                        int arg;
+                        scan_thread(V, l, a0, a1, lam, best, arg);
+                        opt[l] = arg;
                     }
-                    for (int o = tpp >> 1; o > 0; o >>= 1) {
-                        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                        const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
-                        if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
-                    }
-                    if (live && sub == 0) opt[l] = arg;
                 }
                 __syncthreads();
             }
@@ -129,15 +141,16 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
                 bk[l] = a;
             }
             __syncthreads();
-            { double* t = V; V = Vn; Vn = t; }
+            for (int l = tid; l < cols; l += kRidgeThreads) V[l] = Vn[l];
             // prefetch the next frame's emission row (each thread copies the entries it reads)
             if (m + 1 < rows)
                 for (int l = tid; l < cols; l += kRidgeThreads)
                     __pipeline_memcpy_async(En + l, E + (m + 1) * cols + l, sizeof(double));
             __pipeline_commit();
+            __syncthreads();
         }
         // final argmax (smallest index), traceback, suppression
-        if (tid < 32) {
+        if (warp == 0) {
             double best = -INFINITY;
             int arg = 0;
             for (int l = lane; l < cols; l += 32)
@@ -159,8 +172,6 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
             }
         }
         __syncthreads();
-        V = reinterpret_cast<double*>(sm);                 // buffers back in their initial order
-        Vn = V + cols;
         if (q + 1 < count) {
             const int32_t* path = paths + (int64_t)q * rows;
             for (int64_t m = tid; m < rows; m += kRidgeThreads) {
