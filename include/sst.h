@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SST_ABI_VERSION 2
+#define SST_ABI_VERSION 3
 
 typedef enum {
     SST_OK = 0,
@@ -100,7 +100,13 @@ typedef struct {
     double df_eq46_hz;    /* Eq. 46 limit sqrt(2) sigma_f on df                        */
     double hf_bound46;    /* Eq. 46 as an H_f bound: N sqrt(2) sigma_f / fs            */
     uint32_t warnings;    /* SST_WARN_* bits: which of the bounds df exceeds (non-fatal)       */
+    int32_t forward_path; /* how sst_forward computes the STFT: SST_PATH_FUSED (one kernel per tile
+                             of frames, N_f <= 8192), SST_PATH_MULTIPASS (N_f > 8192) or
+                             SST_PATH_FILTERBANK (SST_SOURCE_TRUNCATE with a narrow band: the
+                             frequency-domain filter bank of P:L485, §6); set by sst_plan_create  */
 } sst_layout;
+
+enum { SST_PATH_FUSED = 0, SST_PATH_MULTIPASS = 1, SST_PATH_FILTERBANK = 2 };
 
 /* sst_layout.warnings (also reported as text by sst_last_error after sst_plan_create) */
 enum {
@@ -255,6 +261,11 @@ sst_status sst_inverse_zone(sst_plan* plan, const float* T, int64_t ldT, const i
  * [(fe-fb) * (N_f/2+1)].                                                                    */
 sst_status sst_stft(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len,
                     int64_t fb, int64_t fe, float* S, float* Sd, void* stream);
+/* S^g and S^{g'} of frames [fb, fe) for the band's source bins k in [k1, k2) only, computed by the
+ * plan's frequency-domain filter bank (SST_PATH_FILTERBANK plans; SST_E_UNSUPPORTED otherwise):
+ * S, Sd device complex64 [(fe-fb) * (k2-k1)], row i = frame fb + i.  Debug / parity.          */
+sst_status sst_stft_band(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len,
+                         int64_t fb, int64_t fe, float* S, float* Sd, void* stream);
 /* Target bin of every source coefficient (Eq. 13, 28): l device int32 [(fe-fb)*(N_f/2+1)];
  * -1 = masked (|S| <= gamma or truncated), -2 = out of band / non-finite (R10, R17).       */
 sst_status sst_targets(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len,

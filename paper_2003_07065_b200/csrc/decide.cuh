@@ -37,11 +37,11 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // cm, km: the frame's R23 margins (see fwd_margins); unsure = the fp32 result is not final.
 // FULLWARP: every lane of the warp calls it together (the fused kernel); else the vote uses the
 // active mask (the multi-pass kernel's strided bin loop).
+// Core on (P, Q) = 2 S and (U, V) = 2 alpha (Re S', -Im S') (shared with the filter-bank path, which
+// has S and S' directly).
 template <bool FULLWARP = true>
-__device__ __forceinline__ int bin_target(const FwdArgs& a, float gam4, float cm, float km, int k, float2 za,
-                                          float2 zb, float2& PQ, float2& UV, float& mag4, bool& unsure) {
-    PQ = __fadd2_rn(za, make_float2(zb.x, -zb.y));                           // (P, Q) = 2 S
-    UV = __fadd2_rn(make_float2(za.y, za.x), make_float2(zb.y, -zb.x));      // (U, V) = 2 alpha (Re, -Im) S'
+__device__ __forceinline__ int bin_target_pq(const FwdArgs& a, float gam4, float cm, float km, int k, float2 PQ,
+                                             float2 UV, float& mag4, bool& unsure) {
     const float2 sq = __fmul2_rn(PQ, PQ);
     mag4 = sq.x + sq.y;                                                      // 4 |S|^2
     const bool src = k >= a.src_lo && k < a.src_hi;
@@ -71,6 +71,14 @@ __device__ __forceinline__ int bin_target(const FwdArgs& a, float gam4, float cm
         unsure = cand && ((keep && fabsf(fr - 0.5f) > 0.5f - mg) || fabsf(mag4 - gam4) < km);
     }
     return keep ? lin : -1;
+}
+
+template <bool FULLWARP = true>
+__device__ __forceinline__ int bin_target(const FwdArgs& a, float gam4, float cm, float km, int k, float2 za,
+                                          float2 zb, float2& PQ, float2& UV, float& mag4, bool& unsure) {
+    PQ = __fadd2_rn(za, make_float2(zb.x, -zb.y));                           // (P, Q) = 2 S
+    UV = __fadd2_rn(make_float2(za.y, za.x), make_float2(zb.y, -zb.x));      // (U, V) = 2 alpha (Re, -Im) S'
+    return bin_target_pq<FULLWARP>(a, gam4, cm, km, k, PQ, UV, mag4, unsure);
 }
 
 // R23 margins of one frame from its packed-input norm ||z_m||_2 (nrm2 = ||z_m||^2):

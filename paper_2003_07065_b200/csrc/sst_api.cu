@@ -3,6 +3,7 @@
 // on the host: every step of the transform is a kernel in sst_kernels.cu.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -10,6 +11,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/sst.h"
@@ -42,6 +44,14 @@ struct sst_plan {
     unsigned int* d_dirty_bits = nullptr;   // [(F + 31) / 32]
     int* d_dirty_list = nullptr;    // [gq_cap]
     unsigned int gq_cap = 0;
+    // filter-bank forward (f3b): chosen at plan creation for SST_SOURCE_TRUNCATE with a narrow band
+    bool fb = false;
+    sst::FbArgs fbt{};              // geometry and device tables (x, frames, planes set per launch)
+    float2 *d_fb_gam = nullptr, *d_fb_gamd = nullptr, *d_fb_ph = nullptr, *d_fb_twns = nullptr, *d_fb_twp = nullptr;
+    float2 *d_fb_S = nullptr, *d_fb_Sd = nullptr;
+    float* d_fb_eta = nullptr;
+    int64_t fb_chunk = 0;
+    int fb_sq_grid = 0;
     float2* d_phz = nullptr;        // [z][64 + 2 N_f/64]
     double* d_renyi = nullptr;      // [kRenyiBlocks][2] partial sums
     unsigned long long* d_amax2 = nullptr;   // ridge emission: max |T| (double bits)
@@ -71,7 +81,9 @@ struct sst_plan {
         cudaGetDevice(&prev);
         cudaSetDevice(device);
         for (void* q : {(void*)d_taps, (void*)d_tw, (void*)d_taps64, (void*)d_tw64, (void*)d_mpl, (void*)d_r23, (void*)d_gq, (void*)d_gctr,
-                        (void*)d_dirty_bits, (void*)d_dirty_list, (void*)d_phz, (void*)d_renyi, (void*)d_amax2, (void*)d_back, (void*)d_inv_head, (void*)d_inv_tail,
+                        (void*)d_dirty_bits, (void*)d_dirty_list, (void*)d_fb_gam, (void*)d_fb_gamd,
+                        (void*)d_fb_ph, (void*)d_fb_twns, (void*)d_fb_twp, (void*)d_fb_S, (void*)d_fb_Sd,
+                        (void*)d_fb_eta, (void*)d_phz, (void*)d_renyi, (void*)d_amax2, (void*)d_back, (void*)d_inv_head, (void*)d_inv_tail,
                         (void*)d_inv_per, (void*)d_absmax, (void*)d_seam, (void*)d_twN, (void*)d_mp0, (void*)d_mp1, (void*)d_wf})
             if (q) cudaFree(q);
         cudaSetDevice(prev);
@@ -396,6 +408,132 @@ cudaError_t mp_inverse_accumulate(const sst_plan* pl, const float2* T, int64_t l
 
 }  // namespace
 
+namespace {
+
+// f3b: filter-bank geometry and tables (see filterbank.cu).  Returns false (plan keeps the fused
+// forward) when the band is not narrow, H does not divide the segment, or the tiles do not fit.
+bool setup_filterbank(sst_plan* pl) {
+    const sst_layout& ly = pl->lay;
+    const char* env = std::getenv("SST_FILTERBANK");            // "0": never, "1": whenever valid
+    const int force = env ? (env[0] == '1' ? 1 : (env[0] == '0' ? -1 : 0)) : 0;
+    if (force < 0 || pl->mp || !(pl->p.flags & SST_SOURCE_TRUNCATE)) return false;
+    const int32_t Nf = ly.nfft, L = ly.win_len, H = ly.hop, kb = ly.k2 - ly.k1;
+    if (ly.bins > 1024 || kb > 1024) return false;
+    if (!force && 4 * kb > Nf) return false;                     // narrow bands only (cost model below)
+    int64_t ns = 1;
+    while (ns < 4 * (int64_t)L) ns <<= 1;
+    if (ns < Nf) ns = Nf;
+    if (ns > 16384 || ns % H != 0) return false;
+    const int32_t P = (int32_t)(ns / H);
+    if ((P & (P - 1)) != 0 || P < 32) return false;
+    const int32_t fbn = (int32_t)((ns - L) / H + 1);
+    // Gamma[d] = sum_j g[j] e^{2 pi i d j / Ns} (fp64, from the actual taps) and its g' twin; half-support
+    // D = the largest |d| with |Gamma| or |Gamma'| above 1e-10 of the peak (the rest is dropped)
+    auto gam_at = [&](const std::vector<double>& w, int64_t d) {
+        double re = 0, im = 0;
+        for (int32_t j = 0; j < L; ++j) {
+            const double a = 2.0 * kPi * (double)((d * j) % ns) / (double)ns;
+            re += w[j] * std::cos(a);
+            im += w[j] * std::sin(a);
+        }
+        return std::pair<double, double>(re, im);
+    };
+    double pk = 0, pkd = 0;
+    {
+        auto v = gam_at(pl->g, 0);
+        pk = std::hypot(v.first, v.second);
+        for (int64_t d = 0; d < 64 && d < ns / 2; ++d) {
+            auto u = gam_at(pl->gd, d);
+            pkd = std::max(pkd, std::hypot(u.first, u.second));
+        }
+    }
+    int64_t D = 0;
+    for (int64_t d = 1; d < P / 2; ++d) {
+        auto v = gam_at(pl->g, d), w = gam_at(pl->g, -d), u = gam_at(pl->gd, d), t = gam_at(pl->gd, -d);
+        if (std::hypot(v.first, v.second) > 1e-10 * pk || std::hypot(w.first, w.second) > 1e-10 * pk ||
+            std::hypot(u.first, u.second) > 1e-10 * pkd || std::hypot(t.first, t.second) > 1e-10 * pkd)
+            D = d;
+        else if (d > 8 && d > 2 * D + 8)
+            break;
+    }
+    if (2 * D + 1 > P || D >= P / 2 - 1) return false;
+    // staging chunk: the largest power of two <= 32 bins that fits the transform CTA's shared memory
+    int kc = 32;
+    while (kc > 1 && (ns + 8 * P + (int64_t)fbn * kc * 2) * 8 > 227 * 1024 - 1024) kc >>= 1;
+    if ((ns + 8 * P + (int64_t)fbn * kc * 2) * 8 > 227 * 1024 - 1024) return false;
+    std::vector<float2> gam(2 * D + 1), gamd(2 * D + 1), ph(kb), twns(ns / 2), twp(P / 2);
+    for (int64_t d = -D; d <= D; ++d) {
+        auto v = gam_at(pl->g, d), u = gam_at(pl->gd, d);
+        gam[d + D] = make_float2((float)v.first, (float)v.second);
+        gamd[d + D] = make_float2((float)u.first, (float)u.second);
+    }
+    for (int32_t kk = 0; kk < kb; ++kk) {
+        const int64_t k = ly.k1 + kk;
+        const double a = 2.0 * kPi * (double)((k * ly.center) % Nf) / (double)Nf;
+        ph[kk] = make_float2((float)(std::cos(a) / ns), (float)(std::sin(a) / ns));
+    }
+    for (int64_t e = 0; e < ns / 2; ++e) {
+        const double a = -2.0 * kPi * (double)e / (double)ns;
+        twns[e] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    for (int32_t e = 0; e < P / 2; ++e) {
+        const double a = 2.0 * kPi * (double)e / (double)P;
+        twp[e] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    if (upload(pl, &pl->d_fb_gam, gam) != SST_OK || upload(pl, &pl->d_fb_gamd, gamd) != SST_OK ||
+        upload(pl, &pl->d_fb_ph, ph) != SST_OK || upload(pl, &pl->d_fb_twns, twns) != SST_OK ||
+        upload(pl, &pl->d_fb_twp, twp) != SST_OK)
+        return false;
+    pl->fb_chunk = std::min<int64_t>(ly.frames, 1 << 18);
+    if (cudaMalloc((void**)&pl->d_fb_S, sizeof(float2) * (size_t)pl->fb_chunk * kb) != cudaSuccess ||
+        cudaMalloc((void**)&pl->d_fb_Sd, sizeof(float2) * (size_t)pl->fb_chunk * kb) != cudaSuccess ||
+        cudaMalloc((void**)&pl->d_fb_eta, sizeof(float) * (size_t)pl->fb_chunk) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    sst::FbArgs& f = pl->fbt;
+    f.hop = H;
+    f.c = ly.center;
+    f.ns = (int32_t)ns;
+    f.lg_ns = 0;
+    while ((1ll << f.lg_ns) < ns) ++f.lg_ns;
+    f.P = P;
+    f.lg_P = 0;
+    while ((1 << f.lg_P) < P) ++f.lg_P;
+    f.fb = fbn;
+    f.kc = kc;
+    f.ratio = (int32_t)(ns / Nf);
+    f.D = (int32_t)D;
+    f.kb0 = ly.k1;
+    f.kb = kb;
+    f.gam = pl->d_fb_gam;
+    f.gamd = pl->d_fb_gamd;
+    f.ph = pl->d_fb_ph;
+    f.twns = pl->d_fb_twns;
+    f.twp = pl->d_fb_twp;
+    f.S = pl->d_fb_S;
+    f.Sd = pl->d_fb_Sd;
+    f.eta = pl->d_fb_eta;
+    f.alpha = (float)ly.alpha;
+    // R23 error model of the filter-bank S (calibrated like the fused one, tools/diag_margin.py): one S
+    // value off by eta_S = 4 u sqrt(log2(Ns P)) ||x_b|| ||g|| / sqrt(Ns) (S' likewise with ||g'||,
+    // taken through alpha); margins M times that, in the fused kernel's units (its eta is twice an S error)
+    double g2 = 0, gd2 = 0;
+    for (int32_t j = 0; j < L; ++j) { g2 += pl->g[j] * pl->g[j]; gd2 += pl->gd[j] * pl->gd[j]; }
+    const double gnorm = std::sqrt(g2) * std::max(1.0, ly.alpha * std::sqrt(gd2 / g2));
+    const double u = std::ldexp(1.0, -24);
+    const double etaS = 4.0 * u * std::sqrt(std::log2((double)ns * P)) * gnorm / std::sqrt((double)ns);
+    const double zr_scale = ly.zoom * Nf / (2.0 * kPi * ly.alpha);
+    f.cflag = (float)(pl->r23_m * zr_scale * 2.0 * etaS);
+    f.kflag = (float)(pl->r23_m * etaS);
+    pl->fb_sq_grid = sst::fb_squeeze_grid(pl->device);
+    pl->fb = true;
+    pl->lay.forward_path = SST_PATH_FILTERBANK;
+    return true;
+}
+
+}  // namespace
+
 namespace sst {
 void register_w64_uploader(cudaError_t (*fn)(const float2*)) { w64_uploaders().push_back(fn); }
 }  // namespace sst
@@ -546,6 +684,7 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
     if (Nf > sst::kMaxFusedNfft) {
         // multi-pass path: W_N table and scratch for a bounded chunk of frames (kMpScratch per buffer)
         pl->mp = true;
+        pl->lay.forward_path = SST_PATH_MULTIPASS;
         std::vector<float2> twN(Nf);
         for (int32_t k = 0; k < Nf; ++k) {
             const double a = -2.0 * kPi * k / Nf;
@@ -588,6 +727,7 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
         }
         if (pl->fwd_grid <= 0 || pl->inv_grid <= 0) { delete pl; return fail(nullptr, SST_E_CUDA, "occupancy query failed"); }
     }
+    if (!pl->mp) setup_filterbank(pl);
     pl->err.clear();
     if (pl->lay.warnings) {
         char buf[512];
@@ -643,6 +783,57 @@ sst_status sst_plan_counters(sst_plan* plan, uint64_t* out) {
 
 void sst_plan_destroy(sst_plan* plan) { delete plan; }
 
+// f3b forward: per chunk of frames, the filter-bank transform (S, S' planes of the band's source
+// bins), the decision + exact squeeze per frame (flagged bins queued, R23), the fp64 re-decisions and
+// a list-mode re-squeeze of the frames whose target changed
+static sst_status run_forward_fb(sst_plan* plan, const sst::FwdArgs& a, cudaStream_t st) {
+    for (int64_t c0 = a.frame_begin; c0 < a.frame_end; c0 += plan->fb_chunk) {
+        sst::FwdArgs b = a;
+        b.frame_begin = c0;
+        b.frame_end = std::min<int64_t>(a.frame_end, c0 + plan->fb_chunk);
+        b.T = a.T + (c0 - a.frame_begin) * a.ldT;
+        const int64_t n = b.frame_end - b.frame_begin;
+        sst::FbArgs f = plan->fbt;
+        f.x = b.x;
+        f.x_off = b.x_off;
+        f.x_len = b.x_len;
+        f.n = b.n;
+        f.frame_begin = b.frame_begin;
+        f.frame_end = b.frame_end;
+        sst_status s = cuda_status(plan, sst::launch_fb_transform(f, st), "filter-bank transform");
+        if (s != SST_OK) return s;
+        const int grid = (int)std::min<int64_t>(plan->fb_sq_grid, (n + 7) / 8);
+        const bool defer = b.redecide && plan->d_gq;
+        if (defer) {
+            s = cuda_status(plan, cudaMemsetAsync(plan->d_gctr, 0, sizeof(unsigned int), st), "memset");
+            if (s == SST_OK)
+                s = cuda_status(plan, cudaMemsetAsync(plan->d_dirty_bits, 0, sizeof(unsigned int) * (size_t)((n + 31) / 32), st),
+                                "memset");
+            if (s != SST_OK) return s;
+            b.gq = plan->d_gq;
+            b.gq_n = plan->d_gctr;
+            b.gq_counts = plan->d_gctr + 1;
+            b.gq_cap = plan->gq_cap;
+            b.gq_ctas = grid;
+        }
+        s = cuda_status(plan, sst::launch_fb_squeeze(f, b, grid, st), "filter-bank squeeze");
+        if (s != SST_OK || !defer) {
+            if (s != SST_OK) return s;
+            continue;
+        }
+        s = cuda_status(plan, sst::launch_redecide(b, sst::kModeForward, plan->d_dirty_bits, plan->d_dirty_list, st),
+                        "redecide launch");
+        if (s != SST_OK) return s;
+        sst::FwdArgs r = b;
+        r.gq = nullptr;
+        r.flist = plan->d_dirty_list;
+        r.flist_n = plan->d_gctr;
+        s = cuda_status(plan, sst::launch_fb_squeeze(f, r, plan->fb_sq_grid, st), "filter-bank repair");
+        if (s != SST_OK) return s;
+    }
+    return SST_OK;
+}
+
 static sst_status run_forward_mode(sst_plan* plan, int mode, const float* x, int64_t x_off, int64_t x_len, int64_t fb,
                                    int64_t fe, sst::FwdArgs& a, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
@@ -661,6 +852,7 @@ static sst_status run_forward_mode(sst_plan* plan, int mode, const float* x, int
         }
     }
     (void)x; (void)x_off; (void)x_len;
+    if (plan->fb && mode == sst::kModeForward) return run_forward_fb(plan, a, st);
     const int64_t nfr = a.frame_end - a.frame_begin;
     const bool defer = !plan->mp && a.redecide && plan->d_gq &&
                        (mode == sst::kModeForward || mode == sst::kModeTargets);
@@ -735,6 +927,29 @@ sst_status sst_stft(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len
     a.src_hi = plan->lay.nfft / 2 + 1;
     return cuda_status(plan, launch_fwd_any(plan, a, sst::kModeStft, (cudaStream_t)stream),
                        "stft launch");
+}
+
+sst_status sst_stft_band(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len, int64_t fb, int64_t fe, float* S,
+                         float* Sd, void* stream) {
+    if (!plan) return fail(nullptr, SST_E_INVALID_ARGUMENT, "NULL plan");
+    if (!plan->fb) return fail(plan, SST_E_UNSUPPORTED, "the plan does not use the filter-bank forward");
+    if (!x || !S || !Sd) return fail(plan, SST_E_INVALID_ARGUMENT, "NULL pointer");
+    sst_status s = check_frames(plan, fb, fe);
+    if (s != SST_OK) return s;
+    if (x_len < 0 || !covers_input(plan, x_off, x_len, fb, fe))
+        return fail(plan, SST_E_INVALID_ARGUMENT, "x slice does not cover the frames' samples");
+    DeviceGuard guard(plan->device);
+    sst::FbArgs f = plan->fbt;
+    f.x = x;
+    f.x_off = x_off;
+    f.x_len = x_len;
+    f.n = plan->lay.n;
+    f.frame_begin = fb;
+    f.frame_end = fe;
+    f.S = reinterpret_cast<float2*>(S);
+    f.Sd = reinterpret_cast<float2*>(Sd);
+    f.eta = nullptr;
+    return cuda_status(plan, sst::launch_fb_transform(f, (cudaStream_t)stream), "filter-bank transform");
 }
 
 sst_status sst_targets(sst_plan* plan, const float* x, int64_t x_off, int64_t x_len, int64_t fb, int64_t fe, int32_t* l,

@@ -146,6 +146,31 @@ struct InvArgs {
     int32_t zone_half, zone_keep;
 };
 
+// Frequency-domain filter-bank STFT for truncated narrow bands (filterbank.cu)
+struct FbArgs {
+    const float* x;
+    int64_t x_off, x_len, n;
+    int64_t frame_begin, frame_end;   // frames of the launch (global indices)
+    int32_t hop, c;
+    int32_t ns, lg_ns, P, lg_P;       // block segment length Ns, fold length P = Ns / H
+    int32_t fb, kc;                   // frames per block, band bins per staging chunk
+    int32_t ratio, D;                 // Ns / N_f; Gamma half-support
+    int32_t kb0, kb;                  // source bins [kb0, kb0 + kb) (= [k1, k2), SST_SOURCE_TRUNCATE)
+    const float2* gam;                // [2D + 1] Gamma[d - D] of g   (sum_j g[j] e^{2 pi i d j / Ns})
+    const float2* gamd;               // [2D + 1] of g'
+    const float2* ph;                 // [kb] e^{2 pi i k c / N_f} / Ns
+    const float2* twns;               // [Ns / 2] e^{-2 pi i e / Ns}
+    const float2* twp;                // [P / 2] e^{+2 pi i e / P}
+    float2* S; float2* Sd;            // planes [frames of the launch][kb]
+    float* eta;                       // [frames of the launch] ||x_b||_2 of the frame's block
+    float cflag, kflag;               // R23 margins per unit eta (filter-bank error model)
+    float alpha;
+};
+int fb_transform_smem(const FbArgs& a);
+cudaError_t launch_fb_transform(const FbArgs& a, cudaStream_t s);
+cudaError_t launch_fb_squeeze(const FbArgs& fb, const FwdArgs& a, int grid, cudaStream_t s);
+int fb_squeeze_grid(int device);
+
 // Large-N_f multi-pass path (multipass.cu), used for kMaxFusedNfft < N_f <= kMaxNfft
 constexpr int kMaxFusedNfft = 8192;
 constexpr int kMaxNfft = 65536;

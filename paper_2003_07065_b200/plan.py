@@ -297,6 +297,20 @@ class Plan:
                            S.data_ptr(), Sd.data_ptr(), _stream(self.device)), self._h)
         return S, Sd
 
+    def stft_band(self, x: torch.Tensor, frame_begin: int = 0, frame_end: int | None = None, x_off: int = 0):
+        """sst_stft_band: S, S' of the band's source bins [k1, k2) by the filter bank (f3b plans)."""
+        fb, fe = self._frames(frame_begin, frame_end)
+        kb = self.layout["k2"] - self.layout["k1"]
+        S = torch.empty((fe - fb, kb), dtype=torch.complex64, device=self.device)
+        Sd = torch.empty_like(S)
+        L.check(L.sst_stft_band(self._h, _ptr(x, self.device, torch.float32, "x"), int(x_off), x.numel(), fb, fe,
+                                S.data_ptr(), Sd.data_ptr(), _stream(self.device)), self._h)
+        return S, Sd
+
+    @property
+    def forward_path(self) -> int:
+        return self.layout["forward_path"]
+
     def targets(self, x: torch.Tensor, frame_begin: int = 0, frame_end: int | None = None, x_off: int = 0):
         fb, fe = self._frames(frame_begin, frame_end)
         out = torch.empty((fe - fb, self.src_bins), dtype=torch.int32, device=self.device)
