@@ -8,11 +8,14 @@
 // rewritten with X_b = DFT_Ns(x_b) and Ns = ratio N_f:
 //   S[m', k] = sum_j x_b[m' H + j] g[j] e^{-2 pi i k (j - c) / N_f}
 //            = e^{2 pi i k c / N_f} / Ns  sum_f X_b[f] Gamma[f - ratio k] e^{2 pi i f m' H / Ns},
-//   Gamma[d] = sum_j g[j] e^{2 pi i d j / Ns}   (|Gamma| negligible beyond |d| > D, chosen by the plan
-//                                               at 1e-10 of its peak from the actual taps)
+//   Gamma[d] = sum_j g[j] e^{2 pi i d j / Ns}   (all Ns values: a window cut at +-4 sigma has
+//                                               sidelobes decaying only like 1/d, so no truncation)
 // and since e^{2 pi i f m' H / Ns} depends on f only through q = f mod P (P = Ns / H), folding the
-// 2D + 1 products onto q turns each (k, window) into one P-point inverse DFT that yields S (or S')
-// for all Fb frames of the block:  S[., k] = phase_k / Ns * IDFT_P(Y_k)[m'].
+// products onto q (Y_k[q] = sum_{r < H} X_b[q + r P] Gamma[q + r P - ratio k], a fixed order) turns each
+// (k, window) into one P-point inverse DFT that yields S (or S') for all Fb frames of the block:
+// S[., k] = phase_k / Ns * IDFT_P(Y_k)[m'].  Cost per frame ~ 2 K_b H Ns/(Ns - L) complex MACs for the
+// folds against ~N_f log2 N_f / 2 butterflies for a per-frame FFT: the plan picks the filter bank only
+// where that is smaller (narrow bands at small H).
 // fb_transform: one CTA per block: the Ns-point FFT of x_b (in-place radix-2 in shared memory), then
 // per (k, window) one warp builds Y_k and runs the P-point inverse FFT in its own buffer; results go
 // through a staging tile to the S / S' planes [frame][K_b] (coalesced rows).
@@ -95,14 +98,17 @@ __global__ void __launch_bounds__(kFbThreads, 1) fb_transform_kernel(const FbArg
             const int kk = kk0 + (item >> 1), win = item & 1;
             const int k = a.kb0 + kk;
             const float2* gam = win ? a.gamd : a.gam;
-            for (int q = lane; q < a.P; q += 32) buf[q] = make_float2(0.0f, 0.0f);
-            __syncwarp();
-            // Y_k[q] = sum over f = ratio k + d, q = f mod P, of X_b[f mod Ns] Gamma[d]; 2D + 1 <= P: one
-            // product per q.  Placed in bit-reversed order for the in-place DIT inverse transform.
-            for (int d = lane; d <= 2 * a.D; d += 32) {
-                const int f = ((a.ratio * k + d - a.D) % a.ns + a.ns) % a.ns;
-                const float2 y = fmulc(X[f], __ldg(gam + d));
-                buf[brev_n((unsigned)(f & (a.P - 1)), a.lg_P)] = y;
+            // Y_k[q] = sum_{r < H} X_b[q + r P] Gamma[(q + r P - ratio k) mod Ns], placed in bit-reversed
+            // order for the in-place DIT inverse transform
+            const int sh = a.ratio * k;
+            for (int q = lane; q < a.P; q += 32) {
+                float2 acc = make_float2(0.0f, 0.0f);
+                for (int f = q; f < a.ns; f += a.P) {
+                    const float2 xv = X[f], gv = __ldg(gam + ((f - sh) & (a.ns - 1)));
+                    acc.x = fmaf(xv.x, gv.x, fmaf(-xv.y, gv.y, acc.x));
+                    acc.y = fmaf(xv.x, gv.y, fmaf(xv.y, gv.x, acc.y));
+                }
+                buf[brev_n((unsigned)q, a.lg_P)] = acc;
             }
             __syncwarp();
             // inverse DFT over P (e^{+2 pi i q m / P}), radix-2 DIT

@@ -412,6 +412,29 @@ namespace {
 
 // f3b: filter-bank geometry and tables (see filterbank.cu).  Returns false (plan keeps the fused
 // forward) when the band is not narrow, H does not divide the segment, or the tiles do not fit.
+// in-place iterative radix-2 DFT, fp64: a[k] <- sum_n a[n] e^{sign 2 pi i n k / n_pts}
+void fft64(std::vector<std::pair<double, double>>& a, int sign) {
+    const size_t n = a.size();
+    for (size_t i = 1, j = 0; i < n; ++i) {
+        size_t bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) std::swap(a[i], a[j]);
+    }
+    for (size_t len = 2; len <= n; len <<= 1) {
+        for (size_t i = 0; i < n; i += len)
+            for (size_t k = 0; k < len / 2; ++k) {
+                const double ang = sign * 2.0 * kPi * (double)k / (double)len;
+                const double wr = std::cos(ang), wi = std::sin(ang);
+                auto& u = a[i + k];
+                auto& v = a[i + k + len / 2];
+                const double tr = v.first * wr - v.second * wi, ti = v.first * wi + v.second * wr;
+                v = {u.first - tr, u.second - ti};
+                u = {u.first + tr, u.second + ti};
+            }
+    }
+}
+
 bool setup_filterbank(sst_plan* pl) {
     const sst_layout& ly = pl->lay;
     const char* env = std::getenv("SST_FILTERBANK");            // "0": never, "1": whenever valid
@@ -419,7 +442,6 @@ bool setup_filterbank(sst_plan* pl) {
     if (force < 0 || pl->mp || !(pl->p.flags & SST_SOURCE_TRUNCATE)) return false;
     const int32_t Nf = ly.nfft, L = ly.win_len, H = ly.hop, kb = ly.k2 - ly.k1;
     if (ly.bins > 1024 || kb > 1024) return false;
-    if (!force && 4 * kb > Nf) return false;                     // narrow bands only (cost model below)
     int64_t ns = 1;
     while (ns < 4 * (int64_t)L) ns <<= 1;
     if (ns < Nf) ns = Nf;
@@ -427,45 +449,27 @@ bool setup_filterbank(sst_plan* pl) {
     const int32_t P = (int32_t)(ns / H);
     if ((P & (P - 1)) != 0 || P < 32) return false;
     const int32_t fbn = (int32_t)((ns - L) / H + 1);
-    // Gamma[d] = sum_j g[j] e^{2 pi i d j / Ns} (fp64, from the actual taps) and its g' twin; half-support
-    // D = the largest |d| with |Gamma| or |Gamma'| above 1e-10 of the peak (the rest is dropped)
-    auto gam_at = [&](const std::vector<double>& w, int64_t d) {
-        double re = 0, im = 0;
-        for (int32_t j = 0; j < L; ++j) {
-            const double a = 2.0 * kPi * (double)((d * j) % ns) / (double)ns;
-            re += w[j] * std::cos(a);
-            im += w[j] * std::sin(a);
-        }
-        return std::pair<double, double>(re, im);
-    };
-    double pk = 0, pkd = 0;
-    {
-        auto v = gam_at(pl->g, 0);
-        pk = std::hypot(v.first, v.second);
-        for (int64_t d = 0; d < 64 && d < ns / 2; ++d) {
-            auto u = gam_at(pl->gd, d);
-            pkd = std::max(pkd, std::hypot(u.first, u.second));
-        }
-    }
-    int64_t D = 0;
-    for (int64_t d = 1; d < P / 2; ++d) {
-        auto v = gam_at(pl->g, d), w = gam_at(pl->g, -d), u = gam_at(pl->gd, d), t = gam_at(pl->gd, -d);
-        if (std::hypot(v.first, v.second) > 1e-10 * pk || std::hypot(w.first, w.second) > 1e-10 * pk ||
-            std::hypot(u.first, u.second) > 1e-10 * pkd || std::hypot(t.first, t.second) > 1e-10 * pkd)
-            D = d;
-        else if (d > 8 && d > 2 * D + 8)
-            break;
-    }
-    if (2 * D + 1 > P || D >= P / 2 - 1) return false;
+    int lgP = 0;
+    while ((1 << lgP) < P) ++lgP;
+    // cost model (complex multiply-adds per frame): folds + P-point inverse FFTs of 2 K_b bins per
+    // block and the block FFT, against the fused path's packed N_f-point FFT
+    const double fb_cost = (2.0 * kb * ((double)ns + 0.5 * P * lgP) + 0.5 * ns * std::log2((double)ns)) / fbn;
+    const double fused_cost = 0.5 * Nf * std::log2((double)Nf);
+    if (!force && fb_cost > 0.8 * fused_cost) return false;
+    // Gamma[d] = sum_j g[j] e^{2 pi i d j / Ns} for every d (an fp64 inverse-sign DFT of the zero-padded
+    // taps), and the same for g'
+    std::vector<std::pair<double, double>> G(ns, {0.0, 0.0}), Gd(ns, {0.0, 0.0});
+    for (int32_t j = 0; j < L; ++j) { G[j] = {pl->g[j], 0.0}; Gd[j] = {pl->gd[j], 0.0}; }
+    fft64(G, +1);
+    fft64(Gd, +1);
     // staging chunk: the largest power of two <= 32 bins that fits the transform CTA's shared memory
     int kc = 32;
     while (kc > 1 && (ns + 8 * P + (int64_t)fbn * kc * 2) * 8 > 227 * 1024 - 1024) kc >>= 1;
     if ((ns + 8 * P + (int64_t)fbn * kc * 2) * 8 > 227 * 1024 - 1024) return false;
-    std::vector<float2> gam(2 * D + 1), gamd(2 * D + 1), ph(kb), twns(ns / 2), twp(P / 2);
-    for (int64_t d = -D; d <= D; ++d) {
-        auto v = gam_at(pl->g, d), u = gam_at(pl->gd, d);
-        gam[d + D] = make_float2((float)v.first, (float)v.second);
-        gamd[d + D] = make_float2((float)u.first, (float)u.second);
+    std::vector<float2> gam(ns), gamd(ns), ph(kb), twns(ns / 2), twp(P / 2);
+    for (int64_t d = 0; d < ns; ++d) {
+        gam[d] = make_float2((float)G[d].first, (float)G[d].second);
+        gamd[d] = make_float2((float)Gd[d].first, (float)Gd[d].second);
     }
     for (int32_t kk = 0; kk < kb; ++kk) {
         const int64_t k = ly.k1 + kk;
@@ -503,7 +507,6 @@ bool setup_filterbank(sst_plan* pl) {
     f.fb = fbn;
     f.kc = kc;
     f.ratio = (int32_t)(ns / Nf);
-    f.D = (int32_t)D;
     f.kb0 = ly.k1;
     f.kb = kb;
     f.gam = pl->d_fb_gam;

@@ -154,10 +154,10 @@ struct FbArgs {
     int32_t hop, c;
     int32_t ns, lg_ns, P, lg_P;       // block segment length Ns, fold length P = Ns / H
     int32_t fb, kc;                   // frames per block, band bins per staging chunk
-    int32_t ratio, D;                 // Ns / N_f; Gamma half-support
+    int32_t ratio;                    // Ns / N_f
     int32_t kb0, kb;                  // source bins [kb0, kb0 + kb) (= [k1, k2), SST_SOURCE_TRUNCATE)
-    const float2* gam;                // [2D + 1] Gamma[d - D] of g   (sum_j g[j] e^{2 pi i d j / Ns})
-    const float2* gamd;               // [2D + 1] of g'
+    const float2* gam;                // [Ns] Gamma[d] of g   (sum_j g[j] e^{2 pi i d j / Ns})
+    const float2* gamd;               // [Ns] of g'
     const float2* ph;                 // [kb] e^{2 pi i k c / N_f} / Ns
     const float2* twns;               // [Ns / 2] e^{-2 pi i e / Ns}
     const float2* twp;                // [P / 2] e^{+2 pi i e / P}

@@ -54,12 +54,24 @@ def _plan(P, spec, gamma):
     return P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=gamma, flags=P.SST_SOURCE_TRUNCATE, device=0)
 
 
+def test_filterbank_choice(P, monkeypatch):
+    """The plan's cost model picks the filter bank for the narrow C2 / C3 bands and keeps the fused
+    path for C4 (K_b H too large against N_f log N_f) and without SST_SOURCE_TRUNCATE."""
+    monkeypatch.delenv("SST_FILTERBANK", raising=False)
+    assert _plan(P, FB[0], 1e-4).forward_path == P.SST_PATH_FILTERBANK
+    assert _plan(P, FB[1], 1e-4).forward_path == P.SST_PATH_FILTERBANK
+    assert _plan(P, FB[2], 1e-4).forward_path == P.SST_PATH_FUSED
+    N, fs, L, sigma, hop, nfft, f1, f2, z = FB[0]
+    assert P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=1e-4, device=0).forward_path == P.SST_PATH_FUSED
+
+
 @pytest.mark.parametrize("spec", FB, ids=IDS)
 def test_filterbank_forward(P, spec, monkeypatch):
     N, fs, L, sigma, hop, nfft, f1, f2, z = spec
     x = _sig(N, fs, N)
     g, gd, c = O.gaussian_window(L, sigma)
     gamma = 1e-6 * float(np.sum(g)) * float(np.abs(x).max())
+    monkeypatch.setenv("SST_FILTERBANK", "1")                 # every shape here, C4-like included
     plan = _plan(P, spec, gamma)
     assert plan.forward_path == P.SST_PATH_FILTERBANK
     xd = torch.from_numpy(x).to(DEV)
