@@ -518,14 +518,15 @@ bool setup_filterbank(sst_plan* pl) {
     f.Sd = pl->d_fb_Sd;
     f.eta = pl->d_fb_eta;
     f.alpha = (float)ly.alpha;
-    // R23 error model of the filter-bank S (calibrated like the fused one, tools/diag_margin.py): one S
-    // value off by eta_S = 4 u sqrt(log2(Ns P)) ||x_b|| ||g|| / sqrt(Ns) (S' likewise with ||g'||,
+    // R23 error model of the filter-bank S (calibrated on the GPU like the fused one,
+    // tools/diag_fb_margin.py: r errors <= 3.3 x the model with the constant 4, so 8 is used): one S
+    // value off by eta_S = 8 u sqrt(log2(Ns P)) ||x_b|| ||g|| / sqrt(Ns) (S' likewise with ||g'||,
     // taken through alpha); margins M times that, in the fused kernel's units (its eta is twice an S error)
     double g2 = 0, gd2 = 0;
     for (int32_t j = 0; j < L; ++j) { g2 += pl->g[j] * pl->g[j]; gd2 += pl->gd[j] * pl->gd[j]; }
     const double gnorm = std::sqrt(g2) * std::max(1.0, ly.alpha * std::sqrt(gd2 / g2));
     const double u = std::ldexp(1.0, -24);
-    const double etaS = 4.0 * u * std::sqrt(std::log2((double)ns * P)) * gnorm / std::sqrt((double)ns);
+    const double etaS = 8.0 * u * std::sqrt(std::log2((double)ns * P)) * gnorm / std::sqrt((double)ns);
     const double zr_scale = ly.zoom * Nf / (2.0 * kPi * ly.alpha);
     f.cflag = (float)(pl->r23_m * zr_scale * 2.0 * etaS);
     f.kflag = (float)(pl->r23_m * etaS);

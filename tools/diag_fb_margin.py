@@ -1,6 +1,6 @@
 """R23 margin calibration of the filter-bank forward (f3b): the fp32 error of r from the filter
 bank's S, S' (sst_stft_band, truncate plans) against the fp64 oracle, in units of the plan's error
-model eta_S = 4 u sqrt(log2(Ns P)) ||x_b|| ||g|| / sqrt(Ns) (see sst_api.cu setup_filterbank).
+model eta_S = 8 u sqrt(log2(Ns P)) ||x_b|| ||g|| / sqrt(Ns) (see sst_api.cu setup_filterbank).
     python tools/diag_fb_margin.py [frames]"""
 import os
 import sys
@@ -57,7 +57,7 @@ for name in ["C2", "C3", "C4"]:
         seg = xg[max(0, s0):max(0, s0 + ns)]
         nb[blocks == b] = np.sqrt(np.sum(seg.astype(np.float64) ** 2))
     gn = np.sqrt(np.sum(g ** 2)) * max(1.0, alpha * np.sqrt(np.sum(gd ** 2) / np.sum(g ** 2)))
-    etaS = 4 * 2.0 ** -24 * np.sqrt(np.log2(ns * Pn)) * nb[:, None] * gn / np.sqrt(ns)
+    etaS = 8 * 2.0 ** -24 * np.sqrt(np.log2(ns * Pn)) * nb[:, None] * gn / np.sqrt(ns)
     zr_scale = cfg.zoom * Nf / (2 * np.pi * alpha)
     aS = np.abs(S)
     UV = np.abs(2 * alpha * Sd.real) + np.abs(2 * alpha * Sd.imag)
