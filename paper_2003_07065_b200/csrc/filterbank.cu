@@ -46,11 +46,15 @@ __device__ __forceinline__ unsigned brev_n(unsigned v, int lg) { return __brev(v
 }  // namespace
 
 // ------------------------------------------------------------------------------ transform ----
+// HH: the fold length H (compile time for the usual 4..64, unrolled; 0: runtime).  GSM: Gamma of the
+// current window staged in shared memory (windows then processed one after the other).
+template <int HH, bool GSM>
 __global__ void __launch_bounds__(kFbThreads, 1) fb_transform_kernel(const FbArgs a) {
     extern __shared__ __align__(16) float2 fsm[];
     float2* X = fsm;                                         // [ns] spectrum of x_b (in place)
     float2* wb = X + a.ns;                                   // [warps][P] inverse-FFT buffers
     float2* stg = wb + kFbWarps * a.P;                       // [fb][kc][2] staging tile
+    float2* gsm = stg + (size_t)a.fb * a.kc * 2;             // [ns] Gamma of one window (GSM)
     __shared__ float red[kFbWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t nfr = a.frame_end - a.frame_begin;
@@ -92,21 +96,44 @@ __global__ void __launch_bounds__(kFbThreads, 1) fb_transform_kernel(const FbArg
     const float eta = sqrtf(nrm2);                           // ||x_b||_2 (the plan's constants do the rest)
 
     float2* buf = wb + warp * a.P;
+    const int H = HH ? HH : a.ns / a.P;
+    for (int pass = 0; pass < (GSM ? 2 : 1); ++pass) {
+    if constexpr (GSM) {
+        const float2* src = pass ? a.gamd : a.gam;
+        for (int i = tid; i < a.ns; i += kFbThreads) gsm[i] = __ldg(src + i);
+        __syncthreads();
+    }
     for (int kk0 = 0; kk0 < a.kb; kk0 += a.kc) {
         const int kn = min(a.kc, a.kb - kk0);
-        for (int item = warp; item < 2 * kn; item += kFbWarps) {
-            const int kk = kk0 + (item >> 1), win = item & 1;
+        for (int item = warp; item < (GSM ? 1 : 2) * kn; item += kFbWarps) {
+            const int kk = kk0 + (GSM ? item : (item >> 1)), win = GSM ? pass : (item & 1);
             const int k = a.kb0 + kk;
-            const float2* gam = win ? a.gamd : a.gam;
+            const float2* gam = GSM ? gsm : (win ? a.gamd : a.gam);
             // Y_k[q] = sum_{r < H} X_b[q + r P] Gamma[(q + r P - ratio k) mod Ns], placed in bit-reversed
             // order for the in-place DIT inverse transform
             const int sh = a.ratio * k;
             for (int q = lane; q < a.P; q += 32) {
                 float2 acc = make_float2(0.0f, 0.0f);
-                for (int f = q; f < a.ns; f += a.P) {
-                    const float2 xv = X[f], gv = __ldg(gam + ((f - sh) & (a.ns - 1)));
-                    acc.x = fmaf(xv.x, gv.x, fmaf(-xv.y, gv.y, acc.x));
-                    acc.y = fmaf(xv.x, gv.y, fmaf(xv.y, gv.x, acc.y));
+                if constexpr (HH > 0) {
+                    float2 xv[HH], gv[HH];
+#pragma unroll
+                    for (int r = 0; r < HH; ++r) {                // all loads first, then the fixed-order sum
+                        const int f = q + r * a.P;
+                        xv[r] = X[f];
+                        gv[r] = GSM ? gam[(f - sh) & (a.ns - 1)] : __ldg(gam + ((f - sh) & (a.ns - 1)));
+                    }
+#pragma unroll
+                    for (int r = 0; r < HH; ++r) {
+                        acc.x = fmaf(xv[r].x, gv[r].x, fmaf(-xv[r].y, gv[r].y, acc.x));
+                        acc.y = fmaf(xv[r].x, gv[r].y, fmaf(xv[r].y, gv[r].x, acc.y));
+                    }
+                } else {
+                    for (int r = 0; r < H; ++r) {
+                        const int f = q + r * a.P;
+                        const float2 xv = X[f], gv = __ldg(gam + ((f - sh) & (a.ns - 1)));
+                        acc.x = fmaf(xv.x, gv.x, fmaf(-xv.y, gv.y, acc.x));
+                        acc.y = fmaf(xv.x, gv.y, fmaf(xv.y, gv.x, acc.y));
+                    }
                 }
                 buf[brev_n((unsigned)q, a.lg_P)] = acc;
             }
@@ -125,20 +152,21 @@ __global__ void __launch_bounds__(kFbThreads, 1) fb_transform_kernel(const FbArg
             }
             const float2 ph = __ldg(a.ph + kk);               // e^{2 pi i k c / N_f} / Ns
             for (int m = lane; m < a.fb; m += 32)
-                stg[((int64_t)m * a.kc + (item >> 1)) * 2 + win] = fmulc(buf[m], ph);
+                stg[((int64_t)m * a.kc + (kk - kk0)) * 2 + win] = fmulc(buf[m], ph);
             __syncwarp();
         }
         __syncthreads();
-        // staging -> planes: row m0 + m, columns kk0 .. kk0 + kn
+        // staging -> planes: row m0 + m, columns kk0 .. kk0 + kn (GSM: the pass's window only)
         for (int idx = tid; idx < a.fb * kn; idx += kFbThreads) {
             const int m = idx / kn, kk = idx - m * kn;
             const int64_t fr = m0 + m;
             if (fr >= 0 && fr < nfr) {
-                a.S[fr * a.kb + kk0 + kk] = stg[((int64_t)m * a.kc + kk) * 2 + 0];
-                a.Sd[fr * a.kb + kk0 + kk] = stg[((int64_t)m * a.kc + kk) * 2 + 1];
+                if (!GSM || pass == 0) a.S[fr * a.kb + kk0 + kk] = stg[((int64_t)m * a.kc + kk) * 2 + 0];
+                if (!GSM || pass == 1) a.Sd[fr * a.kb + kk0 + kk] = stg[((int64_t)m * a.kc + kk) * 2 + 1];
             }
         }
         __syncthreads();
+    }
     }
     if (a.eta)
         for (int m = tid; m < a.fb; m += kFbThreads)
@@ -147,6 +175,7 @@ __global__ void __launch_bounds__(kFbThreads, 1) fb_transform_kernel(const FbArg
 
 // ------------------------------------------------------------------------------ squeeze ------
 // one warp per frame; list mode (a.flist) processes the listed frames with inline fp64 re-decision
+template <int NBMAX>
 __global__ void __launch_bounds__(kFbThreads) fb_squeeze_kernel(const FbArgs fb, const FwdArgs a) {
     extern __shared__ __align__(16) int lsm[];
     __shared__ unsigned cq_n;
@@ -170,8 +199,7 @@ __global__ void __launch_bounds__(kFbThreads) fb_squeeze_kernel(const FbArgs fb,
     __syncthreads();
     const int64_t v_lo = a.x_off > 0 ? a.x_off : 0;
     const int64_t v_hi = min(a.n, a.x_off + a.x_len);
-    constexpr int NBMAX = 32;                                 // source bins per lane (K_b <= 1024)
-    const int nb = (fb.kb + 31) / 32;
+    const int nb = (fb.kb + 31) / 32;                         // source bins per lane (<= NBMAX)
 
     for (int64_t it = (int64_t)blockIdx.x * kFbWarps + warp; it < nitems; it += (int64_t)gridDim.x * kFbWarps) {
         const int64_t fi = lmode ? (int64_t)__ldg(a.flist + it) : it;
@@ -289,15 +317,29 @@ __global__ void __launch_bounds__(kFbThreads) fb_squeeze_kernel(const FbArgs fb,
 // ------------------------------------------------------------------------------ launchers ----
 int fb_transform_smem(const FbArgs& a) { return (a.ns + kFbWarps * a.P + a.fb * a.kc * 2) * (int)sizeof(float2); }
 
+template <int HH>
+static cudaError_t launch_fbt(const FbArgs& a, unsigned blocks, cudaStream_t s) {
+    const int base = fb_transform_smem(a);
+    const bool gsm = base + a.ns * (int)sizeof(float2) <= 227 * 1024;
+    const int smem = base + (gsm ? a.ns * (int)sizeof(float2) : 0);
+    auto kern = gsm ? fb_transform_kernel<HH, true> : fb_transform_kernel<HH, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<blocks, kFbThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_fb_transform(const FbArgs& a, cudaStream_t s) {
     const int64_t nfr = a.frame_end - a.frame_begin;
     if (nfr <= 0) return cudaSuccess;
-    const int64_t blocks = (a.frame_end - 1) / a.fb - a.frame_begin / a.fb + 1;
-    const int smem = fb_transform_smem(a);
-    cudaError_t e = cudaFuncSetAttribute(fb_transform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    fb_transform_kernel<<<(unsigned)blocks, kFbThreads, smem, s>>>(a);
-    return cudaGetLastError();
+    const unsigned blocks = (unsigned)((a.frame_end - 1) / a.fb - a.frame_begin / a.fb + 1);
+    switch (a.ns / a.P) {
+        case 4: return launch_fbt<4>(a, blocks, s);
+        case 8: return launch_fbt<8>(a, blocks, s);
+        case 16: return launch_fbt<16>(a, blocks, s);
+        case 32: return launch_fbt<32>(a, blocks, s);
+        default: return launch_fbt<0>(a, blocks, s);
+    }
 }
 
 int fb_squeeze_grid(int device) {
@@ -306,12 +348,22 @@ int fb_squeeze_grid(int device) {
     return 2 * sms;
 }
 
-cudaError_t launch_fb_squeeze(const FbArgs& fb, const FwdArgs& a, int grid, cudaStream_t s) {
+template <int NBMAX>
+static cudaError_t launch_fbs(const FbArgs& fb, const FwdArgs& a, int grid, cudaStream_t s) {
     const int smem = kFbWarps * 4 * a.bins * (int)sizeof(int);
-    cudaError_t e = cudaFuncSetAttribute(fb_squeeze_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(fb_squeeze_kernel<NBMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    fb_squeeze_kernel<<<grid, kFbThreads, smem, s>>>(fb, a);
+    fb_squeeze_kernel<NBMAX><<<grid, kFbThreads, smem, s>>>(fb, a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_fb_squeeze(const FbArgs& fb, const FwdArgs& a, int grid, cudaStream_t s) {
+    const int nb = (fb.kb + 31) / 32;
+    if (nb <= 2) return launch_fbs<2>(fb, a, grid, s);
+    if (nb <= 4) return launch_fbs<4>(fb, a, grid, s);
+    if (nb <= 8) return launch_fbs<8>(fb, a, grid, s);
+    if (nb <= 16) return launch_fbs<16>(fb, a, grid, s);
+    return launch_fbs<32>(fb, a, grid, s);
 }
 
 }  // namespace sst

@@ -463,9 +463,15 @@ bool setup_filterbank(sst_plan* pl) {
     fft64(G, +1);
     fft64(Gd, +1);
     // staging chunk: the largest power of two <= 32 bins that fits the transform CTA's shared memory
+    // together with one window's Gamma (Ns float2, staged per pass); without it if even 4 bins do not fit
+    auto smem_of = [&](int kcv, bool gsm) { return (ns + 8 * P + (int64_t)fbn * kcv * 2 + (gsm ? ns : 0)) * 8; };
     int kc = 32;
-    while (kc > 1 && (ns + 8 * P + (int64_t)fbn * kc * 2) * 8 > 227 * 1024 - 1024) kc >>= 1;
-    if ((ns + 8 * P + (int64_t)fbn * kc * 2) * 8 > 227 * 1024 - 1024) return false;
+    while (kc > 4 && smem_of(kc, true) > 227 * 1024 - 1024) kc >>= 1;
+    if (smem_of(kc, true) > 227 * 1024 - 1024) {
+        kc = 32;
+        while (kc > 1 && smem_of(kc, false) > 227 * 1024 - 1024) kc >>= 1;
+        if (smem_of(kc, false) > 227 * 1024 - 1024) return false;
+    }
     std::vector<float2> gam(ns), gamd(ns), ph(kb), twns(ns / 2), twp(P / 2);
     for (int64_t d = 0; d < ns; ++d) {
         gam[d] = make_float2((float)G[d].first, (float)G[d].second);

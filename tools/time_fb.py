@@ -33,9 +33,10 @@ for name in sys.argv[1:] or ["C2", "C3", "C4"]:
         torch.cuda.synchronize()
         res[mode] = (a.elapsed_time(b) / 5, plan.forward_path, plan.counters())
         if mode == "1":
-            T1 = T.clone()
+            T1 = T[::97].clone()
         else:
-            d = float((T - T1).abs().pow(2).sum().sqrt() / T1.abs().pow(2).sum().sqrt())
+            T0 = T[::97]
+            d = float((T0 - T1).abs().pow(2).sum().sqrt() / T1.abs().pow(2).sum().sqrt())
         plan.close()
         del T
     print(f"{name} truncate forward: filter bank {res['1'][0]:.3f} ms (path {res['1'][1]}, R23 {res['1'][2]}); "
