@@ -56,8 +56,13 @@ enum {
     SST_SOURCE_TRUNCATE = 2u,   /* only source bins k in [k1, k2) are reassigned (R12)  */
     SST_DETERMINISTIC = 4u,     /* accepted, no effect: every result is bitwise reproducible run to
                                    run (exact fixed-point squeeze sums, fixed-order OLA)            */
-    SST_DISCRETE_CONSTANT = 8u  /* inverse divides by C_d = g[c] sum g / sum g^2 instead of
+    SST_DISCRETE_CONSTANT = 8u, /* inverse divides by C_d = g[c] sum g / sum g^2 instead of
                                    sqrt 2 (Eq. 24, R15)                                         */
+    SST_FILTER_BANK = 16u       /* with SST_SOURCE_TRUNCATE: compute the band's S, S' with the
+                                   frequency-domain filter bank (§6) instead of per-frame
+                                   FFTs (same results to fp32 rounding).  Without the flag the plan
+                                   uses it only where its cost model predicts a gain (measured on B200:
+                                   none of C2-C4)                                  */
 };
 
 typedef struct {

@@ -39,6 +39,7 @@ SST_GAMMA_RELATIVE = 1
 SST_SOURCE_TRUNCATE = 2
 SST_DETERMINISTIC = 4
 SST_DISCRETE_CONSTANT = 8
+SST_FILTER_BANK = 16
 
 SST_WARN_EQ37 = 1
 SST_WARN_EQ46 = 2

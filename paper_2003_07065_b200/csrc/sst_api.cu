@@ -142,7 +142,8 @@ sst_status validate(const sst_params* p, sst_layout* lay, std::string& msg) {
     if (p->zoom < 1) { msg = "subdivision z must be >= 1"; return SST_E_INVALID_ARGUMENT; }
     if (!std::isfinite(p->gamma) || p->gamma < 0) { msg = "gamma must be finite and >= 0"; return SST_E_INVALID_ARGUMENT; }
     if (!std::isfinite(p->sigma)) { msg = "sigma must be finite"; return SST_E_INVALID_ARGUMENT; }
-    if (p->flags & ~(uint32_t)(SST_GAMMA_RELATIVE | SST_SOURCE_TRUNCATE | SST_DETERMINISTIC | SST_DISCRETE_CONSTANT)) {
+    if (p->flags & ~(uint32_t)(SST_GAMMA_RELATIVE | SST_SOURCE_TRUNCATE | SST_DETERMINISTIC | SST_DISCRETE_CONSTANT |
+                               SST_FILTER_BANK)) {
         msg = "unknown flag bits"; return SST_E_INVALID_ARGUMENT;
     }
     if ((int64_t)L > (int64_t)p->nfft || (int64_t)p->nfft > p->n) {
@@ -437,8 +438,10 @@ void fft64(std::vector<std::pair<double, double>>& a, int sign) {
 
 bool setup_filterbank(sst_plan* pl) {
     const sst_layout& ly = pl->lay;
-    const char* env = std::getenv("SST_FILTERBANK");            // "0": never, "1": whenever valid
-    const int force = env ? (env[0] == '1' ? 1 : (env[0] == '0' ? -1 : 0)) : 0;
+    // SST_FILTER_BANK requests it; SST_FILTERBANK=0 / =1 (environment, tests only) forbid / force it
+    const char* env = std::getenv("SST_FILTERBANK");
+    int force = (pl->p.flags & SST_FILTER_BANK) ? 1 : 0;
+    if (env) force = env[0] == '1' ? 1 : (env[0] == '0' ? -1 : force);
     if (force < 0 || pl->mp || !(pl->p.flags & SST_SOURCE_TRUNCATE)) return false;
     const int32_t Nf = ly.nfft, L = ly.win_len, H = ly.hop, kb = ly.k2 - ly.k1;
     if (ly.bins > 1024 || kb > 1024) return false;
@@ -453,9 +456,12 @@ bool setup_filterbank(sst_plan* pl) {
     while ((1 << lgP) < P) ++lgP;
     // cost model (complex multiply-adds per frame): folds + P-point inverse FFTs of 2 K_b bins per
     // block and the block FFT, against the fused path's packed N_f-point FFT
+    // measured on B200 (tools/time_fb.py): the filter bank ran 1.8x / 2.0x / 3.1x the fused forward on
+    // C2 / C3 / C4 at modelled cost ratios 0.53 / 0.79 / 2.0 (its folds and P-point transforms are
+    // shared-memory-latency bound), so it is picked only below a modelled ratio of 0.25
     const double fb_cost = (2.0 * kb * ((double)ns + 0.5 * P * lgP) + 0.5 * ns * std::log2((double)ns)) / fbn;
     const double fused_cost = 0.5 * Nf * std::log2((double)Nf);
-    if (!force && fb_cost > 0.8 * fused_cost) return false;
+    if (!force && fb_cost > 0.25 * fused_cost) return false;
     // Gamma[d] = sum_j g[j] e^{2 pi i d j / Ns} for every d (an fp64 inverse-sign DFT of the zero-padded
     // taps), and the same for g'
     std::vector<std::pair<double, double>> G(ns, {0.0, 0.0}), Gd(ns, {0.0, 0.0});

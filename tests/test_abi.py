@@ -80,6 +80,7 @@ BASE = dict(n=4096, fs=1024.0, win_len=257, sigma=32.0, hop=1, nfft=4096, f1=0.0
     ({"f1": 0.1}, 1),                         # off-grid (R9)
     ({"fs": 0.0}, 1),
     ({"flags": 64}, 1),                       # unknown flag
+    ({"flags": 2 | 16}, 0),                   # SST_SOURCE_TRUNCATE | SST_FILTER_BANK
     ({"nfft": 3000}, 3),                      # not a power of two
     ({"nfft": 131072, "n": 131072}, 3),       # outside this build's N_f range (<= 65536)
     ({"nfft": 32768, "n": 573440, "fs": 10240.0, "win_len": 8193, "sigma": 1024.0, "hop": 667,

@@ -55,14 +55,18 @@ def _plan(P, spec, gamma):
 
 
 def test_filterbank_choice(P, monkeypatch):
-    """The plan's cost model picks the filter bank for the narrow C2 / C3 bands and keeps the fused
-    path for C4 (K_b H too large against N_f log N_f) and without SST_SOURCE_TRUNCATE."""
+    """SST_FILTER_BANK selects the filter bank for a truncated band; without it the plan's cost model
+    (calibrated on B200, where the fused forward is faster on C2-C4) keeps the fused path; never
+    without SST_SOURCE_TRUNCATE."""
     monkeypatch.delenv("SST_FILTERBANK", raising=False)
-    assert _plan(P, FB[0], 1e-4).forward_path == P.SST_PATH_FILTERBANK
-    assert _plan(P, FB[1], 1e-4).forward_path == P.SST_PATH_FILTERBANK
-    assert _plan(P, FB[2], 1e-4).forward_path == P.SST_PATH_FUSED
     N, fs, L, sigma, hop, nfft, f1, f2, z = FB[0]
-    assert P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=1e-4, device=0).forward_path == P.SST_PATH_FUSED
+    for spec in FB[:3]:
+        assert _plan(P, spec, 1e-4).forward_path == P.SST_PATH_FUSED
+    fl = P.SST_SOURCE_TRUNCATE | P.SST_FILTER_BANK
+    assert P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=1e-4, flags=fl, device=0).forward_path == \
+        P.SST_PATH_FILTERBANK
+    assert P.Plan(N, fs, L, sigma, hop, nfft, f1, f2, z, gamma=1e-4, flags=P.SST_FILTER_BANK,
+                  device=0).forward_path == P.SST_PATH_FUSED
 
 
 @pytest.mark.parametrize("spec", FB, ids=IDS)
