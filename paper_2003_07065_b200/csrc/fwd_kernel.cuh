@@ -66,9 +66,6 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ float wnrm[TPB / 32];               // per-warp ||z_m||^2 partials (groups of > 1 warp)
     __shared__ unsigned cq_n;                      // R23 deferral: entries this CTA queued
-    // touched band bins of the current chunk (BIG): CH bins per chunk, as in the squeeze below
-    constexpr int CH_BITS = (((N2 < 32 ? 2 * CAP - 32 : 2 * CAP) / 4) & ~3);
-    __shared__ unsigned tbm[BIG ? G : 1][BIG ? (CH_BITS + 31) / 32 : 1];
     float2* smem = reinterpret_cast<float2*>(smem_raw);
     float2* taps_s = reinterpret_cast<float2*>(smem_raw + a.lay.taps_off);
     float* xbuf = reinterpret_cast<float*>(smem_raw + a.lay.xb_off);
@@ -444,7 +441,6 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
             // 28 ints so that the warp's 32-bit accesses spread over the banks
             constexpr int CH = ((N2 < 32 ? 2 * CAP - 32 : 2 * CAP) / 4 / WPG) & ~3;
             static_assert(CH % 4 == 0 && CH > 0, "int4 zeroing");
-            static_assert(!BIG || CH <= CH_BITS, "touched-bin bitmap");
             const int lane = threadIdx.x & 31;
             const int wib = (WPG > 1) ? (tg >> 5) : 0;     // warp within the group
             const int ebank = (N2 < 32) ? ((32 - ((lane / N2) * N2) % 32) % 32) & ~3 : 0;
@@ -459,23 +455,15 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
             const float scale = __uint_as_float((unsigned)(127 + 39 - ex) << 23);
             const float iscale = __uint_as_float((unsigned)(127 - 39 + ex) << 23);
             if (WPG > 1 && lane == 0) wscale[threadIdx.x >> 5] = iscale;
-            // BIG (B > CAP, e.g. C5's 2048 bins from 257 source bins): most band bins of a frame receive
-            // nothing, so the squeeze marks the bins it touches in a per-group bitmap; the readout converts
-            // (and clears) only those and writes zeros elsewhere (two bins per 16-byte store), and only the
-            // frame's first chunk needs the accumulator zeroed (clear-on-read keeps it zero after that)
-            constexpr bool SPARSE = BIG && WPG == 1;
-            const bool vec2 = SPARSE && ((a.ldT & 1) == 0) && ((reinterpret_cast<uintptr_t>(a.T) & 15) == 0);
             for (int l0 = 0; l0 < a.bins; l0 += CH) {
                 const int lc = min(CH, a.bins - l0);
-                if (!SPARSE || l0 == 0) {
+                {
                     int4* z4 = reinterpret_cast<int4*>(reinterpret_cast<int*>(buf) + ebank);
                     const int lc4 = (lc + 3) >> 2;
 #pragma unroll
                     for (int q = 0; q < 4 * WPG; ++q)
                         for (int i = tg; i < lc4; i += N2) z4[q * (CH / 4) + i] = make_int4(0, 0, 0, 0);
                 }
-                if constexpr (SPARSE)
-                    for (int w = tg; w < (lc + 31) / 32; w += N2) tbm[group][w] = 0u;
                 group_sync<N2>(group);
 #pragma unroll
                 for (int i = 0; i < NB; ++i) {
@@ -495,35 +483,10 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                         atomicAdd(acc + CH + lr, (int)(xr & 0xFFFFF));
                         atomicAdd(acc + 2 * CH + lr, (int)(xi >> 20));
                         atomicAdd(acc + 3 * CH + lr, (int)(xi & 0xFFFFF));
-                        if constexpr (SPARSE) atomicOr(&tbm[group][lr >> 5], 1u << (lr & 31));
                     }
                 }
                 group_sync<N2>(group);
-                if constexpr (SPARSE) {
-                    int* a0 = reinterpret_cast<int*>(buf) + ebank;
-                    auto take = [&](int i) -> float2 {              // bin i of the chunk: converted if touched
-                        if (!((tbm[group][i >> 5] >> (i & 31)) & 1u)) return make_float2(0.0f, 0.0f);
-                        const float2 t = make_float2(limbs_to_float(a0[i], a0[CH + i], iscale),
-                                                     limbs_to_float(a0[2 * CH + i], a0[3 * CH + i], iscale));
-                        a0[i] = a0[CH + i] = a0[2 * CH + i] = a0[3 * CH + i] = 0;   // clear on read
-                        return t;
-                    };
-                    if (vec2) {
-                        for (int i = 2 * tg; i < lc; i += 2 * N2) {
-                            const float2 t0 = take(i);
-                            const float2 t1 = (i + 1 < lc) ? take(i + 1) : make_float2(0.0f, 0.0f);
-                            SST_CHECK(fi < nfr && l0 + i + 1 < a.bins + (i + 1 < lc ? 0 : 1));
-                            if (!valid) continue;
-                            if (i + 1 < lc) __stcs(reinterpret_cast<float4*>(trow + l0 + i), make_float4(t0.x, t0.y, t1.x, t1.y));
-                            else __stcs(trow + l0 + i, t0);
-                        }
-                    } else {
-                        for (int i = tg; i < lc; i += N2) {
-                            const float2 t = take(i);
-                            if (valid) __stcs(trow + l0 + i, t);
-                        }
-                    }
-                } else if (valid)
+                if (valid)
                     for (int i = tg; i < lc; i += N2) {
                         const int* a0 = reinterpret_cast<const int*>(buf) + ebank;
                         float2 t;
