@@ -19,7 +19,9 @@ namespace sst {
 // RM: every nonzero sub-spectrum entry q (band [k1, k2) or mirror [N - k2, N)) has
 // q / N2 in [0, RM) or [64 - RM, 64) (i.e. ceil(k2 / N2) <= RM): other rows of the step-1
 // input are compile-time zeros and cost nothing (narrow bands: C2, C3 use RM = 5, C4 RM = 8).
-template <int N2, bool FULLWIN, int RM>
+// ZONE: the mode-retrieval zone is applied to the T loads (a.zone_path); a separate
+// instantiation, so the plain inverse carries no zone arithmetic
+template <int N2, bool FULLWIN, int RM, bool ZONE>
 __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 256 ? 1 : 2) inv_kernel(const InvArgs a) {
     using Gm = Geom<N2, false>;
     constexpr int N = Gm::N;
@@ -84,8 +86,8 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
             const float2* TA = a.T + (vA ? fA : f_lo) * a.ldT;
             const float2* TB = vB ? TA + a.ldT : TA;
             // mode retrieval zone: centre bins of frames A and B (none: keep everything)
-            const int zA = a.zone_path && vA ? __ldg(a.zone_path + fA) : 0;
-            const int zB = a.zone_path && vB ? __ldg(a.zone_path + fA + 1) : 0;
+            const int zA = ZONE && vA ? __ldg(a.zone_path + fA) : 0;
+            const int zB = ZONE && vB ? __ldg(a.zone_path + fA + 1) : 0;
             float2 v[64];
             // band entries q in [k1, k2): l = z (q - k1) + b; mirror entries: l' = z (N - k1 - q) - b
             const int zstep = zoom * N2;                           // l step per row n1
@@ -108,8 +110,8 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
                 const int li = inb ? lbase + n1 * zstep : lm;
                 float2 ta = make_float2(0.0f, 0.0f), tb = make_float2(0.0f, 0.0f);
                 SST_CHECK(!(inb || inm) || (li >= 0 && li < a.bins));
-                const bool okA = !a.zone_path || ((abs(li - zA) <= a.zone_half) == (bool)a.zone_keep);
-                const bool okB = !a.zone_path || ((abs(li - zB) <= a.zone_half) == (bool)a.zone_keep);
+                const bool okA = !ZONE || ((abs(li - zA) <= a.zone_half) == (bool)a.zone_keep);
+                const bool okB = !ZONE || ((abs(li - zB) <= a.zone_half) == (bool)a.zone_keep);
                 if ((inb || inm) && vA && okA) ta = __ldg(TA + li);
                 if ((inb || inm) && vB && okB) tb = __ldg(TB + li);
                 if (n1 == 0 && q == 0 && b == 0) { ta.y = 0.0f; tb.y = 0.0f; }  // DC: real part only (R14)
@@ -284,9 +286,9 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
     }
 }
 
-template <int N2, bool FULLWIN, int RM>
+template <int N2, bool FULLWIN, int RM, bool ZONE = false>
 static cudaError_t launch_inv_b(const InvArgs& a, int grid, cudaStream_t s) {
-    auto kern = inv_kernel<N2, FULLWIN, RM>;
+    auto kern = inv_kernel<N2, FULLWIN, RM, ZONE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, a.lay.total);
     if (e != cudaSuccess) return e;
     kern<<<grid, Geom<N2, false>::TPB, a.lay.total, s>>>(a);
@@ -295,6 +297,7 @@ static cudaError_t launch_inv_b(const InvArgs& a, int grid, cudaStream_t s) {
 
 template <int N2, bool FULLWIN>
 static cudaError_t launch_inv_r(const InvArgs& a, int grid, cudaStream_t s) {
+    if (a.zone_path) return launch_inv_b<N2, FULLWIN, 64, true>(a, grid, s);   // mode retrieval (f1)
     const int rows = (a.k1 + a.bins / a.zoom + N2 - 1) / N2;   // ceil(k2 / N2)
     if (rows <= 5) return launch_inv_b<N2, FULLWIN, 5>(a, grid, s);   // C2, C3
     if (rows <= 8) return launch_inv_b<N2, FULLWIN, 8>(a, grid, s);
@@ -312,7 +315,7 @@ template <int N2>
 static int occ_inv(int hop, int L, int zoom, int device) {
     int nb = 0, sms = 0;
     const int smem = inv_layout(N2, L, hop, zoom).total;
-    auto kern = inv_kernel<N2, true, 64>;
+    auto kern = inv_kernel<N2, true, 64, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Geom<N2, false>::TPB, smem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
