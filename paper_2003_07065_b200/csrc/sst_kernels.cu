@@ -70,6 +70,7 @@ __global__ void finalize_kernel(float* y, int64_t y_off, int64_t y_len, InvArgs 
 }
 
 // ------------------------------------------------------------------------------- R23 ---------
+constexpr int kRedecideSplit = 8;   // CTAs per queue region (latency hiding: the per-bin sums are long)
 // Deferred fp64 re-decisions (reading R23): one warp per queued bin (frame within the launch, k, fp32
 // target), the direct Eq. 8 sum over the frame's samples in global memory, the oracle's decision in
 // fp64.  Targets mode: the fp64 target is written to a.lout.  Forward mode: a frame whose target
@@ -81,7 +82,8 @@ __global__ void __launch_bounds__(256) redecide_kernel(const FwdArgs a, int mode
     // consecutive samples), with the twiddle recurrence w <- w W^{8 k} from W^{k (u - c)}
     // (<= L/8 fp64 complex products, ~1e-14 relative); fixed 3-level xor reduction (deterministic)
     const unsigned reg = a.gq_cap / a.gq_ctas;
-    const int b = blockIdx.x;
+    const int b = blockIdx.x / kRedecideSplit;              // queue region (main launch's CTA)
+    const int sub = blockIdx.x % kRedecideSplit;            // this CTA's share of the region
     const unsigned cnt = __ldg(a.gq_counts + b);
     const double gam64 = launch_gamma64(a);
     const int64_t v_lo = a.x_off > 0 ? a.x_off : 0;
@@ -89,9 +91,10 @@ __global__ void __launch_bounds__(256) redecide_kernel(const FwdArgs a, int mode
     const int64_t K = a.nfft / 2 + 1;
     const unsigned msk = (unsigned)a.nfft - 1u;
     const int u = threadIdx.x & 7;
-    const unsigned rounds = (cnt + 31) / 32;                         // 32 bins per CTA pass (256 / 8)
+    const unsigned per = 32 * kRedecideSplit;                        // bins per pass over the region's CTAs
+    const unsigned rounds = (cnt + per - 1) / per;
     for (unsigned r = 0; r < rounds; ++r) {
-        const unsigned e = r * 32 + (threadIdx.x >> 3);
+        const unsigned e = r * per + sub * 32 + (threadIdx.x >> 3);
         const bool ok = e < cnt;
         const int4 it = ok ? a.gq[(size_t)b * reg + e] : make_int4(0, 0, 0, 0);
         const int64_t s0 = (a.frame_begin + it.x) * a.hop - a.c;
@@ -100,6 +103,7 @@ __global__ void __launch_bounds__(256) redecide_kernel(const FwdArgs a, int mode
         const double2 st = __ldg(a.tw64 + ((8u * (unsigned)k) & msk));             // W^{8 k}
         double sr = 0.0, si = 0.0, dr = 0.0, di = 0.0;
         if (ok) {
+#pragma unroll 4
             for (int j = u; j < a.L; j += 8) {
                 const int64_t sj = s0 + j;
                 const double xv = (sj >= v_lo && sj < v_hi) ? (double)__ldg(a.x + (sj - a.x_off)) : 0.0;
@@ -137,7 +141,7 @@ __global__ void __launch_bounds__(256) redecide_kernel(const FwdArgs a, int mode
 }
 
 cudaError_t launch_redecide(const FwdArgs& a, int mode, unsigned int* dirty_bits, int* dirty_list, cudaStream_t s) {
-    redecide_kernel<<<a.gq_ctas, 256, 0, s>>>(a, mode, dirty_bits, dirty_list);
+    redecide_kernel<<<a.gq_ctas * kRedecideSplit, 256, 0, s>>>(a, mode, dirty_bits, dirty_list);
     return cudaGetLastError();
 }
 
