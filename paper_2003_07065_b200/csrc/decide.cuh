@@ -30,6 +30,12 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return r;
 }
 
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // Per source bin k with Za = Z[k], Zb = Z[N-k]: returns target l (>= 0), -1 masked, -2 out of band.
 // S = (P, Q)/2 with P = Re Za + Re Zb, Q = Im Za - Im Zb;  S' = (U, -V)/(2 alpha) with
 // U = Im Za + Im Zb, V = Re Za - Re Zb;  -Im(S'/S) = (V P + U Q) / (alpha (P^2 + Q^2)).
@@ -65,10 +71,12 @@ __device__ __forceinline__ int bin_target_pq(const FwdArgs& a, float gam4, float
     const bool cand = src && (unsigned)(l + 1) <= (unsigned)a.bins + 1u && fin;
     unsure = false;
     if (__any_sync(FULLWARP ? 0xffffffffu : __activemask(), cand)) {
-        const float rs = rsqrtf(mag4);
+        // branch-free (bitwise &, |): a margin below the flush-to-zero range only under-flags bins whose
+        // |S| ~ 1e-19 ||z_m||, far below any threshold that matters
+        const float rs = rsqrt_approx(mag4);
         const float mg = cm * fmaf(fabsf(UV.x) + fabsf(UV.y), rsq, rs);
         const float fr = t - fl;
-        unsure = cand && ((keep && fabsf(fr - 0.5f) > 0.5f - mg) || fabsf(mag4 - gam4) < km);
+        unsure = cand & ((keep & (fabsf(fr - 0.5f) > 0.5f - mg)) | (fabsf(mag4 - gam4) < km));
     }
     return keep ? lin : -1;
 }

@@ -181,13 +181,21 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
                     const int col = tg + N2 * ci;
                     Fft<N2, +1>::run(u[ci]);
                     const float2 fb = __ldg(pb + col);                      // e(b col)
+                    // FULLWIN: the phase e(b tau) of consecutive k2 advances by e(64 b): a recurrence started
+                    // from the table at k2 = 0 and again at the wrap k2 = N2/2 (tau = p - N), <= N2/2 steps
+                    const float2 step = __ldg(pb + 64 + 1);                 // e(64 b)
+                    float2 ph = fb;
 #pragma unroll
                     for (int k2 = 0; k2 < N2; ++k2) {
                         const int p = col + 64 * k2;                  // output index tau mod N
                         float2 y = u[ci][k2];
                         if constexpr (FULLWIN) {
-                            // tau = p (k2 < N2/2) or p - N: compile-time split; e(b tau) = e(b col) e(b (64 k2 [- N]))
-                            if (rot) y = cmul(y, cmul(fb, __ldg(pb + 64 + (k2 < N2 / 2 ? 0 : N2) + k2)));
+                            // tau = p (k2 < N2/2) or p - N: e(b tau) = e(b col) e(b (64 k2 [- N]))
+                            if (k2 == N2 / 2) ph = cmul(fb, __ldg(pb + 64 + N2 + k2));
+                            if (rot) {
+                                y = cmul(y, ph);
+                                if (k2 + 1 < N2) ph = cmul(ph, step);
+                            }
                         } else {
                             const bool wrap = p > last_in;
                             if (rot && (!wrap || p - N >= -c)) y = cmul(y, cmul(fb, __ldg(pb + 64 + (wrap ? N2 : 0) + k2)));
