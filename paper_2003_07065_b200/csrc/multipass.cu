@@ -19,8 +19,10 @@
 // frames in ascending order: no atomics, deterministic) (a10, Eq. 26).  For narrow bands with a
 // large z (B L small against z N_f log N_f, e.g. the §5.2 Fig. 16(e) shape, z = 20) the plan
 // picks a direct band sum per frame instead (mp_direct_kernel), with the same windowing and OLA.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "decide.cuh"
 #include "sst_internal.h"
@@ -101,6 +103,51 @@ __device__ __forceinline__ float2 load_elem(const MpPass& a, int64_t t, int n) {
     }
 }
 
+// P-point transforms of the 16 columns of x ([P][kTS], element i of column al at x[i kTS + al]),
+// y the same-size scratch; every thread of the CTA (kPassThreads) calls it; returns the buffer
+// holding the result (natural order).  Twiddles W_P^e = W_N^{e N/P} from the plan's table.
+template <int P, int DIR, int NT = kPassThreads>
+__device__ __forceinline__ float2* stockham16(float2* x, float2* y, int N, const float2* twN) {
+    // Stockham (autosort) FFT over the 16 columns: radix-4 stages, then one radix-2 stage when
+    // log2 P is odd.  Radix 4 at length n = P/s: for p < m = n/4, q < s, with A..D = x[q + s(p + j m)],
+    //   y[q + s(4p + k)] = X_k W_n^{p k},  X = the 4-point DFT of (A, B, C, D)
+    const int tstep = N / P;
+    const int tid = threadIdx.x;
+    int s = 1, ls = 0;
+#pragma unroll 1
+    for (; 4 * s <= P; s <<= 2, ls += 2) {
+        const int m = P / (4 * s);
+        for (int bf = tid; bf < kTile * P / 4; bf += NT) {
+            const int al = bf & 15, rest = bf >> 4;
+            const int q = rest & (s - 1), p = rest >> ls;
+            const int i0 = (q + s * p) * kTS + al, im = s * m * kTS;
+            const float2 A = x[i0], B = x[i0 + im], C = x[i0 + 2 * im], D = x[i0 + 3 * im];
+            const float2 apc = make_float2(A.x + C.x, A.y + C.y), amc = make_float2(A.x - C.x, A.y - C.y);
+            const float2 bpd = make_float2(B.x + D.x, B.y + D.y), bmd = make_float2(B.x - D.x, B.y - D.y);
+            const float2 jb = DIR < 0 ? make_float2(bmd.y, -bmd.x) : make_float2(-bmd.y, bmd.x);   // -+i (B - D)
+            const int64_t e = (int64_t)p * s * tstep;                       // W_n^p = W_N^{p s N/P}
+            const int o0 = (q + 4 * s * p) * kTS + al, os = s * kTS;
+            y[o0] = make_float2(apc.x + bpd.x, apc.y + bpd.y);
+            y[o0 + os] = c_mul(make_float2(amc.x + jb.x, amc.y + jb.y), tw_at<DIR>(twN, e));
+            y[o0 + 2 * os] = c_mul(make_float2(apc.x - bpd.x, apc.y - bpd.y), tw_at<DIR>(twN, 2 * e));
+            y[o0 + 3 * os] = c_mul(make_float2(amc.x - jb.x, amc.y - jb.y), tw_at<DIR>(twN, 3 * e));
+        }
+        __syncthreads();
+        float2* tmp = x; x = y; y = tmp;
+    }
+    if (s < P) {                                                        // last radix-2 stage (n = 2)
+        for (int bf = tid; bf < kTile * P / 2; bf += NT) {
+            const int al = bf & 15, q = bf >> 4;
+            const float2 u = x[q * kTS + al], v = x[(q + s) * kTS + al];
+            y[q * kTS + al] = make_float2(u.x + v.x, u.y + v.y);
+            y[(q + s) * kTS + al] = make_float2(u.x - v.x, u.y - v.y);
+        }
+        __syncthreads();
+        float2* tmp = x; x = y; y = tmp;
+    }
+    return x;
+}
+
 template <int P, int PASS, int LOAD, int DIR>
 __global__ void __launch_bounds__(kPassThreads) mp_pass_kernel(const MpPass a) {
     extern __shared__ __align__(16) float2 mp_smem[];
@@ -122,44 +169,7 @@ __global__ void __launch_bounds__(kPassThreads) mp_pass_kernel(const MpPass a) {
         }
     }
     __syncthreads();
-    // Stockham (autosort) FFT over the 16 columns: radix-4 stages, then one radix-2 stage when
-    // log2 P is odd.  Radix 4 at length n = P/s: for p < m = n/4, q < s, with A..D = x[q + s(p + j m)],
-    //   y[q + s(4p + k)] = X_k W_n^{p k},  X = the 4-point DFT of (A, B, C, D)
-    float2* x = s0;
-    float2* y = s1;
-    const int tstep = a.N / P;
-    int s = 1, ls = 0;
-#pragma unroll 1
-    for (; 4 * s <= P; s <<= 2, ls += 2) {
-        const int m = P / (4 * s);
-        for (int bf = tid; bf < kTile * P / 4; bf += kPassThreads) {
-            const int al = bf & 15, rest = bf >> 4;
-            const int q = rest & (s - 1), p = rest >> ls;
-            const int i0 = (q + s * p) * kTS + al, im = s * m * kTS;
-            const float2 A = x[i0], B = x[i0 + im], C = x[i0 + 2 * im], D = x[i0 + 3 * im];
-            const float2 apc = make_float2(A.x + C.x, A.y + C.y), amc = make_float2(A.x - C.x, A.y - C.y);
-            const float2 bpd = make_float2(B.x + D.x, B.y + D.y), bmd = make_float2(B.x - D.x, B.y - D.y);
-            const float2 jb = DIR < 0 ? make_float2(bmd.y, -bmd.x) : make_float2(-bmd.y, bmd.x);   // -+i (B - D)
-            const int64_t e = (int64_t)p * s * tstep;                       // W_n^p = W_N^{p s N/P}
-            const int o0 = (q + 4 * s * p) * kTS + al, os = s * kTS;
-            y[o0] = make_float2(apc.x + bpd.x, apc.y + bpd.y);
-            y[o0 + os] = c_mul(make_float2(amc.x + jb.x, amc.y + jb.y), tw_at<DIR>(a.twN, e));
-            y[o0 + 2 * os] = c_mul(make_float2(apc.x - bpd.x, apc.y - bpd.y), tw_at<DIR>(a.twN, 2 * e));
-            y[o0 + 3 * os] = c_mul(make_float2(amc.x - jb.x, amc.y - jb.y), tw_at<DIR>(a.twN, 3 * e));
-        }
-        __syncthreads();
-        float2* tmp = x; x = y; y = tmp;
-    }
-    if (s < P) {                                                        // last radix-2 stage (n = 2)
-        for (int bf = tid; bf < kTile * P / 2; bf += kPassThreads) {
-            const int al = bf & 15, q = bf >> 4;
-            const float2 u = x[q * kTS + al], v = x[(q + s) * kTS + al];
-            y[q * kTS + al] = make_float2(u.x + v.x, u.y + v.y);
-            y[(q + s) * kTS + al] = make_float2(u.x - v.x, u.y - v.y);
-        }
-        __syncthreads();
-        float2* tmp = x; x = y; y = tmp;
-    }
+    const float2* x = stockham16<P, DIR>(s0, s1, a.N, a.twN);
     for (int idx = tid; idx < P * kTile; idx += kPassThreads) {
         const int k = idx >> 4, al = idx & 15;
         const int a_ = tile * kTile + al;
@@ -195,6 +205,105 @@ cudaError_t run_pass(const MpPass& a, int pass, cudaStream_t s) {
     }
 #undef SST_MP_CASE
     return cudaGetLastError();
+}
+
+// f3a: both passes of the four-step FFT in one thread-block cluster of kClu CTAs per transform,
+// the transpose between them through distributed shared memory.
+// CTA `rank` owns the column tiles [rank CT, (rank + 1) CT) in stage 1 (R1-point DFTs of
+// x[a + M i] times W_N^{a k1}, kept in its shared memory) and the row tiles [rank RT, (rank + 1) RT)
+// in stage 2: it reads rows k1 of every column from the 8 CTAs' shared memory (DSMEM, 16-column
+// segments), runs the M-point DFTs and writes Z[k1 + R1 k2] once.  The intermediate never reaches
+// HBM or L2, so a transform costs one gather of its input and one write of its output (the
+// two-pass path moves each frame through HBM/L2 twice more).  Buffers: stage 1 holds CT tiles of
+// [R1][kTS] in each of two halves; stage 2's RT tiles of [M][kTS] fill the same half sizes
+// (CT R1 = RT M = N / (16 kClu)): the gather lands in the free half, and after the cluster barrier
+// that ends all remote reads the stage-1 half becomes stage 2's scratch.
+constexpr int kClu = 8;
+constexpr int kCluThreads = 512;
+
+template <int R1, int M, int LOAD, int DIR>
+__global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kCluThreads) mp_cluster_kernel(const MpPass a) {
+    namespace cg = cooperative_groups;
+    constexpr int CT = M / (kTile * kClu), RT = R1 / (kTile * kClu);
+    constexpr int B1 = R1 * kTS, B2 = M * kTS;
+    static_assert(CT >= 1 && RT >= 1 && CT * B1 == RT * B2, "cluster FFT tiling");
+    extern __shared__ __align__(16) float2 mp_smem[];
+    float2* const hA = mp_smem;
+    float2* const hB = mp_smem + CT * B1;
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank();
+    const int64_t t = blockIdx.x / kClu;
+    const int tid = threadIdx.x;
+    // stage 1: gather (and for the forward, pack) the columns, R1-point DFTs, twiddle
+#pragma unroll 8
+    for (int idx = tid; idx < CT * R1 * kTile; idx += kCluThreads) {
+        const int ct = idx / (R1 * kTile), rem = idx - ct * (R1 * kTile);
+        const int i = rem >> 4, al = rem & 15;
+        hA[ct * B1 + i * kTS + al] = load_elem<LOAD>(a, t, (rank * CT + ct) * kTile + al + M * i);
+    }
+    __syncthreads();
+    float2* res = hA;
+#pragma unroll
+    for (int ct = 0; ct < CT; ++ct) res = stockham16<R1, DIR, kCluThreads>(hA + ct * B1, hB + ct * B1, a.N, a.twN) - ct * B1;
+    float2* const fre = res == hA ? hB : hA;
+    for (int idx = tid; idx < CT * R1 * kTile; idx += kCluThreads) {
+        const int ct = idx / (R1 * kTile), rem = idx - ct * (R1 * kTile);
+        const int k = rem >> 4, al = rem & 15;
+        const int a_ = (rank * CT + ct) * kTile + al;
+        if (a_ && k) {
+            float2& v = res[ct * B1 + k * kTS + al];
+            v = c_mul(v, tw_at<DIR>(a.twN, ((int64_t)a_ * k) & (a.N - 1)));      // W_N^{a k1}
+        }
+    }
+    cl.sync();                                            // stage-1 results visible cluster-wide
+    // transpose through DSMEM: row tile r, rows k1 = (rank RT + r) 16 + k1l, all M columns
+    constexpr int GATHER = RT * M * kTile;
+#pragma unroll 4
+    for (int idx = tid; idx < GATHER; idx += kCluThreads) {
+        const int al = idx & 15, k1l = (idx >> 4) & 15, rest = idx >> 8;
+        const int r = rest / (M / kTile), at = rest - r * (M / kTile);
+        const int src = at / CT, ct = at - src * CT;
+        const int k1 = (rank * RT + r) * kTile + k1l;
+        const float2* rp = cl.map_shared_rank(res, src);
+        fre[r * B2 + (at * kTile + al) * kTS + k1l] = rp[ct * B1 + k1 * kTS + al];
+    }
+    cl.sync();                                            // remote reads done: `res` is free
+#pragma unroll
+    for (int r = 0; r < RT; ++r) {
+        const float2* x = stockham16<M, DIR, kCluThreads>(fre + r * B2, res + r * B2, a.N, a.twN);
+        for (int idx = tid; idx < M * kTile; idx += kCluThreads) {
+            const int k = idx >> 4, al = idx & 15;
+            a.out[t * a.N + (rank * RT + r) * kTile + al + (int64_t)R1 * k] = x[k * kTS + al];
+        }
+    }
+}
+
+// The whole N-point transform of every item of the batch: pass 1 reads via LOAD, the result goes to
+// `out` in natural order.  Cluster kernel for the shapes it tiles (all N_f the multi-pass path
+// takes); the two-pass form through `tmp` otherwise or when SST_MP_TWO_PASS=1 (A/B timing).
+template <int LOAD, int DIR>
+cudaError_t run_fft(MpPass p, float2* tmp, float2* out, cudaStream_t s) {
+    if (p.count <= 0) return cudaSuccess;
+    static const bool two_pass = [] { const char* e = getenv("SST_MP_TWO_PASS"); return e && atoi(e) != 0; }();
+    void (*kern)(const MpPass) = nullptr;
+    if (!two_pass) {
+        if (p.R1 == 128 && p.M == 128) kern = mp_cluster_kernel<128, 128, LOAD, DIR>;
+        else if (p.R1 == 256 && p.M == 128) kern = mp_cluster_kernel<256, 128, LOAD, DIR>;
+        else if (p.R1 == 256 && p.M == 256) kern = mp_cluster_kernel<256, 256, LOAD, DIR>;
+    }
+    cudaError_t e;
+    if (kern && (int64_t)p.count * kClu < (int64_t)1 << 31) {
+        const int smem = 2 * (p.N / (kTile * kClu)) * kTS * (int)sizeof(float2);
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
+        p.out = out;
+        kern<<<(unsigned)(p.count * kClu), kCluThreads, smem, s>>>(p);
+        return cudaGetLastError();
+    }
+    p.out = tmp;
+    if ((e = run_pass<LOAD, DIR>(p, 1, s)) != cudaSuccess) return e;
+    p.in = tmp;
+    p.out = out;
+    return run_pass<kLoadBuf, DIR>(p, 2, s);
 }
 
 __device__ __forceinline__ float block_max(float v, float* red) {
@@ -285,22 +394,41 @@ __global__ void __launch_bounds__(kBinThreads) mp_bins_kernel(const FwdArgs a, c
         }
         __syncthreads();
         {
+            // pending bins, one at a time with the whole CTA: warp w sums part w of the taps in fp64
+            // (stft_bin_fp64_part's fixed decomposition), the parts are added in warp order, so the
+            // decision does not depend on scheduling.  A bin's sum is L / (32 NW) steps deep per
+            // lane instead of L / 32 on one warp while the other warps wait at the next barrier.
+            constexpr int NW = kBinThreads / 32;
+            __shared__ int plist[kBinThreads];
+            __shared__ int pcount;
+            __shared__ double4 ppart[NW];
             const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
             const double gam64 = launch_gamma64(a);
-            for (int b0 = warp * 32; b0 < K; b0 += kBinThreads) {
-                const int k0 = b0 + lane;
-                unsigned ball = __ballot_sync(0xffffffffu, k0 < K && lrow[k0] == -4);
-                while (ball) {
-                    const int k = b0 + __ffs(ball) - 1;
-                    ball &= ball - 1;
-                    double sr, si, dr, di;
-                    stft_bin_fp64(xat, a.taps64, a.tw64, N, a.L, a.c, k, sr, si, dr, di);
-                    const int ln = decide_fp64(a, gam64, k, sr, si, dr, di);
-                    __syncwarp();
-                    if (lane == 0) {
-                        lrow[k] = ln;
+            auto tap64 = [&](int j) { return __ldg(a.taps64 + j); };
+            for (int c0 = 0; c0 < K; c0 += kBinThreads) {
+                const int k = c0 + threadIdx.x;
+                const bool pend = k < K && lrow[k] == -4;
+                if (threadIdx.x == 0) pcount = 0;
+                __syncthreads();
+                if (pend) plist[atomicAdd(&pcount, 1)] = k;
+                const int np = __syncthreads_count(pend);
+                for (int i = 0; i < np; ++i) {
+                    const int kk = plist[i];
+                    const double4 pr = stft_bin_fp64_part(xat, tap64, a.tw64, N, a.L, a.c, kk, warp, NW);
+                    if (lane == 0) ppart[warp] = pr;
+                    __syncthreads();
+                    if (threadIdx.x == 0) {
+                        double sr = 0.0, si = 0.0, dr = 0.0, di = 0.0;
+                        for (int w = 0; w < NW; ++w) {
+                            sr += ppart[w].x;
+                            si += ppart[w].y;
+                            dr += ppart[w].z;
+                            di += ppart[w].w;
+                        }
+                        lrow[kk] = decide_fp64(a, gam64, kk, sr, si, dr, di);
                         atomicAdd(a.r23_count, 1ull);
                     }
+                    __syncthreads();
                 }
             }
         }
@@ -349,6 +477,278 @@ __global__ void __launch_bounds__(kBinThreads) mp_bins_kernel(const FwdArgs a, c
             }
         }
     }
+}
+
+// f3a fused forward: the cluster FFT with a3-a7 kept on chip.  After stage 2 each CTA holds the
+// spectrum rows k1 it owns (k = k1 + R1 k2); bin k pairs Z[k] (local) with Z[N - k] (row R1 - k1:
+// another CTA's shared memory, read through DSMEM), so the per-bin decision (decide.cuh, the same
+// bin_target as every other path) runs without the spectrum ever reaching HBM.  The frame's
+// ||z_m||^2 (R23 margins) and its max |S| (fixed-point scale) are reduced across the cluster in rank
+// order; each CTA squeezes its bins into a private int64 fixed-point row in shared memory (exact, any
+// order), and CTA r sums the 8 rows for the band slice [r B/8, (r+1) B/8) and writes it to T.  HBM
+// traffic per frame: the x gather (mostly L2 hits between overlapping frames) and the band row.
+// cluster barrier for the fused kernel: SST_CLU_RELAXED=1 builds a CTA-scope fence + relaxed arrive
+// (experiment: avoids the MEMBAR.ALL.GPU of the release arrive)
+__device__ __forceinline__ void cluster_sync_fast() {
+#ifdef SST_CLU_RELAXED
+    __threadfence_block();
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
+#else
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+#endif
+}
+
+constexpr int kPendRound = 8;                 // pending bins per cluster round (fused forward)
+
+template <int R1, int M>
+__global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kCluThreads) mp_fused_fwd_kernel(const MpPass p, const FwdArgs a) {
+    namespace cg = cooperative_groups;
+    constexpr int CT = M / (kTile * kClu), RT = R1 / (kTile * kClu);
+    constexpr int B1 = R1 * kTS, B2 = M * kTS;
+    constexpr int NW = kCluThreads / 32;
+    constexpr int KH = M / 2 + 1;                       // k2 <= M/2 covers every k <= N/2
+    constexpr int OWN = RT * kTile * KH;                // owned bin slots
+    static_assert(CT * B1 == RT * B2 && OWN * 12 <= CT * B1 * 8 && kCluThreads == kBinThreads, "fused tiling");
+    extern __shared__ __align__(16) float2 mp_smem[];
+    __shared__ float red[NW];
+    __shared__ float nrm_part, vmax_part;
+    __shared__ int plist[kCluThreads];
+    __shared__ int pcount;
+    __shared__ double4 ppart[kPendRound][NW];
+    float2* const hA = mp_smem;
+    float2* const hB = mp_smem + CT * B1;
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank();
+    const int64_t fi = blockIdx.x / kClu;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int N = p.N;
+    // stage 1 (+ this CTA's share of ||z_m||^2 = sum |z[n]|^2)
+    float e = 0.0f;
+#pragma unroll 8
+    for (int idx = tid; idx < CT * R1 * kTile; idx += kCluThreads) {
+        const int ct = idx / (R1 * kTile), rem = idx - ct * (R1 * kTile);
+        const int i = rem >> 4, al = rem & 15;
+        const float2 v = load_elem<kLoadFwd>(p, fi, (rank * CT + ct) * kTile + al + M * i);
+        e = fmaf(v.x, v.x, fmaf(v.y, v.y, e));
+        hA[ct * B1 + i * kTS + al] = v;
+    }
+    const float e_cta = block_sum(e, red);            // barrier inside: stage-1 tiles complete
+    if (tid == 0) nrm_part = e_cta;
+    float2* res = hA;
+#pragma unroll
+    for (int ct = 0; ct < CT; ++ct) res = stockham16<R1, -1, kCluThreads>(hA + ct * B1, hB + ct * B1, N, p.twN) - ct * B1;
+    float2* const fre = res == hA ? hB : hA;
+    for (int idx = tid; idx < CT * R1 * kTile; idx += kCluThreads) {
+        const int ct = idx / (R1 * kTile), rem = idx - ct * (R1 * kTile);
+        const int k = rem >> 4, al = rem & 15;
+        const int a_ = (rank * CT + ct) * kTile + al;
+        if (a_ && k) {
+            float2& v = res[ct * B1 + k * kTS + al];
+            v = c_mul(v, tw_at<-1>(p.twN, ((int64_t)a_ * k) & (N - 1)));
+        }
+    }
+    cluster_sync_fast();
+    float nrm2 = 0.0f;
+#pragma unroll
+    for (int r = 0; r < kClu; ++r) nrm2 += *cl.map_shared_rank(&nrm_part, r);
+    constexpr int GATHER = RT * M * kTile;
+#pragma unroll 4
+    for (int idx = tid; idx < GATHER; idx += kCluThreads) {
+        const int al = idx & 15, k1l = (idx >> 4) & 15, rest = idx >> 8;
+        const int r = rest / (M / kTile), at = rest - r * (M / kTile);
+        const int src = at / CT, ct = at - src * CT;
+        const int k1 = (rank * RT + r) * kTile + k1l;
+        const float2* rp = cl.map_shared_rank(res, src);
+        fre[r * B2 + (at * kTile + al) * kTS + k1l] = rp[ct * B1 + k1 * kTS + al];
+    }
+    cluster_sync_fast();
+    float2* zb = fre;
+#pragma unroll
+    for (int r = 0; r < RT; ++r) zb = stockham16<M, -1, kCluThreads>(fre + r * B2, res + r * B2, N, p.twN) - r * B2;
+    float2* const other = zb == fre ? res : fre;
+    float2* const Sst = other;                                        // [OWN] S = (Z[k] + conj Z[N-k]) / 2
+    int* const lst = reinterpret_cast<int*>(other + OWN);             // [OWN] target, < 0 none, -4 pending
+    cluster_sync_fast();                                                        // every CTA's spectrum rows visible
+    float gam4 = a.gamma2x4;
+    if (a.absmax_dev) {
+        const float gm = a.gamma_rel * __ldg(a.absmax_dev);
+        gam4 = 4.0f * gm * gm;
+    }
+    float cm, km;
+    fwd_margins(a, gam4, nrm2, cm, km);
+    for (int ib = tid; ib < OWN; ib += kCluThreads) {
+        const int r = ib / (kTile * KH), rem = ib - r * (kTile * KH);
+        const int k2 = rem >> 4, al = rem & 15;
+        const int k1 = (rank * RT + r) * kTile + al;
+        const int k = k1 + R1 * k2;
+        int l = -1;
+        float2 S = make_float2(0.0f, 0.0f);
+        if (k <= N / 2) {
+            const float2 za = zb[r * B2 + k2 * kTS + al];
+            const int k1b = k1 ? R1 - k1 : 0, k2b = k1 ? M - 1 - k2 : (M - k2) & (M - 1);   // N - k
+            const int ob = k1b / (RT * kTile), rb = (k1b / kTile) % RT, alb = k1b % kTile;
+            const float2 zm = cl.map_shared_rank(zb, ob)[rb * B2 + k2b * kTS + alb];
+            float2 PQ, UV;
+            float mag4;
+            bool unsure;
+            l = bin_target<false>(a, gam4, cm, km, k, za, zm, PQ, UV, mag4, unsure);
+            if (unsure) l = -4;
+            S = make_float2(0.5f * PQ.x, 0.5f * PQ.y);
+        }
+        Sst[ib] = S;
+        lst[ib] = l;
+    }
+    // Pending bins (R23) are re-decided by the whole cluster together: the cluster waits at its
+    // barriers for the slowest CTA anyway, so one CTA's pending bin should not run on 16 warps while
+    // 112 others idle.  Virtual warp (rank, warp) of kClu NW sums part rank NW + warp of the taps
+    // (stft_bin_fp64_part, a fixed decomposition); the owner adds the parts in a fixed tree.  The
+    // fixed-point scale takes max |S| over kept AND pending bins (a bound either way), so it is
+    // exchanged at the same barrier as the pending lists.
+    __syncthreads();
+    if (tid == 0) pcount = 0;
+    __syncthreads();
+    float vmax = 0.0f;
+    for (int ib = tid; ib < OWN; ib += kCluThreads) {
+        const int l = lst[ib];
+        if (l >= 0 || l == -4) {
+            const float2 S = Sst[ib];
+            vmax = fmaxf(vmax, fmaxf(fabsf(S.x), fabsf(S.y)));
+        }
+        if (l == -4) {
+            const int slot = atomicAdd(&pcount, 1);
+            if (slot < kCluThreads) plist[slot] = ib;
+        }
+    }
+    const float mloc = block_max(vmax, red);
+    if (tid == 0) vmax_part = mloc;
+    cluster_sync_fast();                                                        // remote Z reads done; lists, maxima visible
+    float m = 0.0f;
+    int cnt[kClu], total = 0;
+#pragma unroll
+    for (int r = 0; r < kClu; ++r) {
+        m = fmaxf(m, *cl.map_shared_rank(&vmax_part, r));
+        cnt[r] = min(*cl.map_shared_rank(&pcount, r), kCluThreads);
+        total += cnt[r];
+    }
+    if (total > 0) {                                                  // cluster-uniform
+        const int64_t s0 = (a.frame_begin + fi) * a.hop - a.c;
+        const int64_t v_lo = a.x_off > 0 ? a.x_off : 0;
+        const int64_t v_hi = a.n < a.x_off + a.x_len ? a.n : a.x_off + a.x_len;
+        auto xat = [&](int j) -> float {
+            const int64_t sj = s0 + j;
+            return (sj >= v_lo && sj < v_hi) ? __ldg(a.x + (sj - a.x_off)) : 0.0f;
+        };
+        auto tap64 = [&](int j) { return __ldg(a.taps64 + j); };
+        const double gam64 = launch_gamma64(a);
+        // item g -> (owner r, its bin k, its slot ib)
+        auto item = [&](int g, int& r, int& ib) {
+            r = 0;
+            while (g >= cnt[r]) g -= cnt[r++];
+            ib = cl.map_shared_rank(plist, r)[g];
+            const int rr = ib / (kTile * KH), rem = ib - rr * (kTile * KH);
+            return (r * RT + rr) * kTile + (rem & 15) + R1 * (rem >> 4);
+        };
+        for (int g0 = 0; g0 < total; g0 += kPendRound) {
+            const int nr = min(kPendRound, total - g0);
+            for (int g = 0; g < nr; ++g) {
+                int r, ib;
+                const int kk = item(g0 + g, r, ib);
+                const double4 pr = stft_bin_fp64_part(xat, tap64, a.tw64, N, a.L, a.c, kk, rank * NW + warp, kClu * NW);
+                if (lane == 0) ppart[g][warp] = pr;
+            }
+            cluster_sync_fast();                                                // parts visible
+            for (int g = warp; g < nr; g += NW) {
+                int r, ib;
+                const int kk = item(g0 + g, r, ib);
+                if (r != rank) continue;
+                double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
+#pragma unroll
+                for (int j = 0; j < kClu * NW / 32; ++j) {            // lane sums parts 4 lane .. 4 lane + 3
+                    const int part = lane * (kClu * NW / 32) + j;
+                    const double4 v = cl.map_shared_rank(&ppart[0][0], part / NW)[g * NW + part % NW];
+                    t.x += v.x;
+                    t.y += v.y;
+                    t.z += v.z;
+                    t.w += v.w;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    t.x += __shfl_xor_sync(0xffffffffu, t.x, o);
+                    t.y += __shfl_xor_sync(0xffffffffu, t.y, o);
+                    t.z += __shfl_xor_sync(0xffffffffu, t.z, o);
+                    t.w += __shfl_xor_sync(0xffffffffu, t.w, o);
+                }
+                if (lane == 0) {
+                    lst[ib] = decide_fp64(a, gam64, kk, t.x, t.y, t.z, t.w);
+                    atomicAdd(a.r23_count, 1ull);
+                }
+            }
+            cluster_sync_fast();                                                // parts consumed, decisions in place
+        }
+        if (pcount > kCluThreads) {                                   // list overflow (CTA-uniform): the rest here
+            for (int ib0 = 0; ib0 < OWN; ib0 += kCluThreads) {
+                const bool pend = ib0 + tid < OWN && lst[ib0 + tid] == -4;
+                __syncthreads();
+                if (tid == 0) pcount = 0;
+                __syncthreads();
+                if (pend) plist[atomicAdd(&pcount, 1)] = ib0 + tid;
+                const int np = __syncthreads_count(pend);
+                for (int i = 0; i < np; ++i) {
+                    const int jb = plist[i];
+                    const int rr = jb / (kTile * KH), rem = jb - rr * (kTile * KH);
+                    const int kk = (rank * RT + rr) * kTile + (rem & 15) + R1 * (rem >> 4);
+                    const double4 pr = stft_bin_fp64_part(xat, tap64, a.tw64, N, a.L, a.c, kk, warp, NW);
+                    if (lane == 0) ppart[0][warp] = pr;
+                    __syncthreads();
+                    if (tid == 0) {
+                        double sr = 0.0, si = 0.0, dr = 0.0, di = 0.0;
+                        for (int w = 0; w < NW; ++w) {
+                            sr += ppart[0][w].x;
+                            si += ppart[0][w].y;
+                            dr += ppart[0][w].z;
+                            di += ppart[0][w].w;
+                        }
+                        lst[jb] = decide_fp64(a, gam64, kk, sr, si, dr, di);
+                        atomicAdd(a.r23_count, 1ull);
+                    }
+                    __syncthreads();
+                }
+            }
+        }
+    }
+    // a6: exact fixed-point sums (mp_bins_kernel's scaling: |X| < 2^39, <= 2^15 + 1 terms per target)
+    const int ex = max(-87, (int)((__float_as_uint(m) >> 23) & 0xff) - 126);
+    const float scale = __uint_as_float((unsigned)(127 + 39 - ex) << 23);
+    const float iscale = __uint_as_float((unsigned)(127 - 39 + ex) << 23);
+    long long* const acc = reinterpret_cast<long long*>(zb);          // [bins][2]; the spectrum is dead
+    for (int i = tid; i < 2 * a.bins; i += kCluThreads) acc[i] = 0;
+    __syncthreads();
+    for (int ib = tid; ib < OWN; ib += kCluThreads) {
+        const int l = lst[ib];
+        if (l >= 0) {
+            SST_CHECK(l < a.bins);
+            const float2 S = Sst[ib];
+            long long xr, xi;
+            asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xr) : "f"(S.x * scale));
+            asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xi) : "f"(S.y * scale));
+            atomicAdd(reinterpret_cast<unsigned long long*>(acc + 2 * l), (unsigned long long)xr);
+            atomicAdd(reinterpret_cast<unsigned long long*>(acc + 2 * l + 1), (unsigned long long)xi);
+        }
+    }
+    cluster_sync_fast();                                                        // partial rows complete
+    float2* const trow = a.T + (fi + 0) * a.ldT;
+    const int l0 = (int)((int64_t)a.bins * rank / kClu), l1 = (int)((int64_t)a.bins * (rank + 1) / kClu);
+    for (int l = l0 + tid; l < l1; l += kCluThreads) {
+        long long sr = 0, si = 0;
+#pragma unroll
+        for (int r = 0; r < kClu; ++r) {
+            const long long* ap = cl.map_shared_rank(acc, r);
+            sr += ap[2 * l];
+            si += ap[2 * l + 1];
+        }
+        trow[l] = make_float2(__ll2float_rn(sr) * iscale, __ll2float_rn(si) * iscale);
+    }
+    cluster_sync_fast();                                                        // keep shared memory until all reads end
 }
 
 // a9 tail: combine the residues of each frame pair, window by g[tau + c]/N_f, write frames A, B
@@ -484,12 +884,22 @@ cudaError_t launch_mp_forward(const FwdArgs& f, int mode, const float2* twN, flo
     p.L = f.L;
     p.c = f.c;
     p.taps = f.taps;
-    p.out = buf0;
-    cudaError_t e = run_pass<kLoadFwd, -1>(p, 1, s);
-    if (e != cudaSuccess) return e;
-    p.in = buf0;
-    p.out = buf1;
-    if ((e = run_pass<kLoadBuf, -1>(p, 2, s)) != cudaSuccess) return e;
+    cudaError_t e;
+    static const bool unfused = [] { const char* v = getenv("SST_MP_UNFUSED"); return v && atoi(v) != 0; }();
+    if (mode == kModeForward && !unfused && nfr * kClu < ((int64_t)1 << 31)) {
+        void (*fk)(const MpPass, const FwdArgs) = nullptr;
+        int half = 0;                                                  // CT B1 float2
+        if (p.R1 == 128 && p.M == 128) { fk = mp_fused_fwd_kernel<128, 128>; half = 128 * kTS; }
+        else if (p.R1 == 256 && p.M == 128) { fk = mp_fused_fwd_kernel<256, 128>; half = 256 * kTS; }
+        else if (p.R1 == 256 && p.M == 256) { fk = mp_fused_fwd_kernel<256, 256>; half = 2 * 256 * kTS; }
+        if (fk && 2 * f.bins <= half) {
+            const int smem = 2 * half * (int)sizeof(float2);
+            if ((e = cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
+            fk<<<(unsigned)(nfr * kClu), kCluThreads, smem, s>>>(p, f);
+            return cudaGetLastError();
+        }
+    }
+    if ((e = run_fft<kLoadFwd, -1>(p, buf0, buf1, s)) != cudaSuccess) return e;
     const int ch = mp_bins_chunk(f.bins);
     switch (mode) {
         case kModeForward: {
@@ -530,12 +940,7 @@ cudaError_t launch_mp_inverse_accumulate(const MpInvArgs& a, cudaStream_t s) {
     p.zone_path = a.zone_path;
     p.zone_half = a.zone_half;
     p.zone_keep = a.zone_keep;
-    p.out = a.buf0;
-    e = run_pass<kLoadInv, +1>(p, 1, s);
-    if (e != cudaSuccess) return e;
-    p.in = a.buf0;
-    p.out = a.buf1;
-    if ((e = run_pass<kLoadBuf, +1>(p, 2, s)) != cudaSuccess) return e;
+    if ((e = run_fft<kLoadInv, +1>(p, a.buf0, a.buf1, s)) != cudaSuccess) return e;
     mp_combine_kernel<<<dim3((unsigned)pairs, (unsigned)((a.L + 255) / 256)), 256, 0, s>>>(a, a.buf1);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }

@@ -55,9 +55,14 @@ def main():
         pl = P.Plan(N, FS, L, SIGMA, s["hop"], 32768, s["f1"], s["f2"], s["zoom"], gamma=1e-6, device=0)
         T = torch.empty((pl.frames, pl.bins), dtype=torch.complex64, device="cuda")
         y = torch.empty(N, dtype=torch.float32, device="cuda")
+        c0 = pl.counters()
+        pl.forward(x, out=T)
+        c1 = pl.counters()
         fwd = timed(lambda: pl.forward(x, out=T))
         inv = timed(lambda: pl.inverse(T, out=y))
         res[name] = {"frames": pl.frames, "bins": pl.bins, "forward_ms": fwd, "inverse_ms": inv,
+                     "r23_redecided_per_frame": (c1["redecided"] - c0["redecided"]) / pl.frames,
+                     "r23_changed_per_frame": (c1["changed"] - c0["changed"]) / pl.frames,
                      "paper_sst_s": s["paper_s"]}
         pl.close()
     out = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out", "s52_timing.json")
