@@ -56,10 +56,9 @@ def _peaks():
         return 6650.0, 1965.0, "fallback"
 
 
-def _traffic(workload, kernel, frames):
-    """DRAM bytes (read + write) per launch of the dominant kernel, from the committed ncu --set full
-    capture of this bench command (profiles/traffic.json, written by tools/ncu_traffic.py); None if
-    there is no capture for this workload and frame count."""
+def _traffic_committed(workload, kernel, frames):
+    """DRAM bytes per launch from the committed ncu --set full capture (profiles/traffic.json, written
+    by tools/ncu_traffic.py); the fallback when ncu cannot run in this bench."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f)
@@ -67,6 +66,60 @@ def _traffic(workload, kernel, frames):
         return e["dram_bytes"] if e["frames"] == frames else None
     except Exception:
         return None
+
+
+TRAFFIC_KERNELS = {"forward": "fwd_kernel", "inverse": "inv_kernel"}
+
+
+def traffic_probe(workload):
+    """Child of the bench (under ncu): one forward + one inverse of the workload, nothing timed."""
+    import torch
+
+    import paper_2003_07065_b200 as P
+    cfg = get_config(workload)
+    g, _ = P.gaussian_window(cfg.L, cfg.sigma)
+    x_host = generate(cfg, 0, cfg.N)
+    gamma = 1e-6 * float(np.sum(g)) * float(np.abs(x_host).max())
+    plan = P.Plan(cfg.N, cfg.fs, cfg.L, cfg.sigma, cfg.hop, cfg.nfft, cfg.f1, cfg.f2, cfg.zoom, gamma=gamma, device=0)
+    x = torch.from_numpy(x_host).cuda()
+    T = plan.forward(x)
+    plan.inverse(T)
+    torch.cuda.synchronize()
+    plan.close()
+
+
+def measure_traffic(workload, kernel, frames, timeout=600):
+    """DRAM bytes (read + write) per launch of the dominant kernel, measured in this bench run: ncu
+    (dram__bytes_read.sum + dram__bytes_write.sum, --clock-control none) on a child process doing one
+    forward + one inverse of the same workload; the first launch of the kernel is the full-size one.
+    Falls back to the committed capture when ncu is unavailable or fails (reported in `source`)."""
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    name = TRAFFIC_KERNELS[kernel]
+    if os.path.exists(ncu):
+        cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none",
+               "-k", f"regex:^{name}", "-c", "1", "--csv", sys.executable, os.path.abspath(__file__),
+               "--traffic-probe", "--workload", workload]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+            import csv
+            import io
+            vals = {}
+            for row in csv.reader(io.StringIO(r.stdout)):
+                if len(row) > 10 and row[-3] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    unit, v = row[-2], float(row[-1].replace(",", ""))
+                    vals[row[-3]] = v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            if len(vals) == 2:
+                return {"bytes": vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"],
+                        "read": vals["dram__bytes_read.sum"], "write": vals["dram__bytes_write.sum"],
+                        "source": f"ncu in this run (first {name} launch of one forward + inverse)"}
+            err = (r.stderr or r.stdout)[-300:]
+        except Exception as e:  # noqa: BLE001
+            err = repr(e)
+    else:
+        err = "ncu not found"
+    b = _traffic_committed(workload, kernel, frames)
+    return {"bytes": b, "source": f"committed profiles/traffic.json ({err.strip()[:200]})"}
 
 
 def algorithmic_counts(cfg):
@@ -576,9 +629,9 @@ def run_ours(args, cfg_base):
     inv_gbs = inv_b * nfr_rank / (inv_ms * 1e-3) / 1e9 if inv_ms > 0 else 0.0
     dom = "forward" if fwd_ms >= inv_ms else "inverse"
     ach = fwd_tf if dom == "forward" else inv_tf
-    traffic = _traffic(cfg_base.name, dom, nfr_rank) if world == 1 else None
+    traffic = {"bytes": None, "source": "not measured (N > 1 or --no-traffic)"}
     roofline = {"bound": "alu", "kernel": f"sst_{dom}", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": ach / fp32_peak, "traffic": traffic,
+                "frac": ach / fp32_peak, "traffic": None,
                 "peak_source": f"derived: {FP32_PEAK_NOTE}",
                 "hbm": {"forward_gbs": fwd_gbs, "inverse_gbs": inv_gbs, "peak_gbs": hbm_gbs,
                         "forward_frac": fwd_gbs / hbm_gbs, "inverse_frac": inv_gbs / hbm_gbs,
@@ -598,6 +651,12 @@ def run_ours(args, cfg_base):
         del run
     plan.close()
     torch.cuda.empty_cache()
+    if world == 1 and not args.no_traffic:
+        traffic = measure_traffic(cfg_base.name, dom, nfr_rank)
+    roofline["traffic"] = traffic["bytes"]
+    roofline["traffic_source"] = traffic["source"]
+    if traffic["bytes"]:
+        roofline["traffic_vs_algorithmic"] = traffic["bytes"] / ((fwd_b if dom == "forward" else inv_b) * nfr_rank)
     legs = {}
     store = store_peak_gbs(dev) if args.legs else None
     for name in [s for s in args.legs.split(",") if s]:
@@ -651,7 +710,12 @@ def main():
     ap.add_argument("--c5-chunk", type=int, default=1 << 20, help="C5 frames per chunk (T buffer 16 GiB)")
     ap.add_argument("--ref-frames", type=int, default=512)
     ap.add_argument("--ref-procs", type=int, default=0, help="reference arm processes (default: every core)")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the ncu DRAM-traffic child run")
+    ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.traffic_probe:
+        traffic_probe(args.workload)
+        return
     if args.warmup < 3:
         print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
         args.warmup = 3

@@ -1,20 +1,23 @@
 // Large-N_f path (8192 < N_f <= 65536; the paper's §5.2 uses N_f = 2^15).
 //
 // A frame's packed buffer (N_f complex64 = 256 KiB at 2^15) no longer fits one CTA's shared
-// memory next to anything else, so the transform runs as a multi-pass four-step FFT through HBM
-// (the scratch of a chunk of frames stays mostly L2-resident):
-//   N_f = R1 M.  Pass 1: for every column a in [0, M) a P = R1-point DFT of x[a + M i], times
-//   W_N^{a k1}, stored at [k1][a].  Pass 2: for every row k1 a P = M-point DFT over a, stored at
-//   k1 + R1 k2 (natural order).  Each CTA owns 16 adjacent columns / rows, so every global load
-//   and store moves 128-byte segments, and runs a radix-4 Stockham (autosort) FFT over them in
-//   shared memory with twiddles rounded once from fp64 (the plan's W_N table).
-// Forward: pass 1 gathers and packs the frame on the fly (a1: z[n] = u (g + i alpha g'), circular
-// placement, as in the fused kernel), pass 2 writes the spectrum, and one CTA per frame then does
+// memory next to anything else, so the transform is a four-step FFT split over a thread-block
+// cluster of 8 CTAs (mp_cluster_kernel):
+//   N_f = R1 M.  Stage 1: for every column a in [0, M) a P = R1-point DFT of x[a + M i], times
+//   W_N^{a k1}, kept at [k1][a] in the shared memory of the CTA owning column a.  Stage 2: every
+//   CTA reads its rows k1 from all 8 CTAs through distributed shared memory, runs P = M-point
+//   DFTs over a and writes k1 + R1 k2 (natural order) once.  Each CTA works on tiles of 16
+//   adjacent columns / rows, so every global load and store moves 128-byte segments, and runs a
+//   radix-4 Stockham (autosort) FFT over them in shared memory with twiddles rounded once from
+//   fp64 (the plan's W_N table).  (The two-pass form through an HBM scratch, mp_pass_kernel, is
+//   kept for A/B timing: SST_MP_TWO_PASS=1.)
+// Forward: stage 1 gathers and packs the frame on the fly (a1: z[n] = u (g + i alpha g'), circular
+// placement, as in the fused kernel), stage 2 writes the spectrum, and one CTA per frame then does
 // a3-a7 with the fused path's own per-bin decision (decide.cuh) and an exact 64-bit fixed-point
 // squeeze in shared memory (order-independent, so bitwise reproducible).
 // Inverse: per frame pair and residue b the Hermitian-packed sub-spectrum G_b (the fused
-// inverse's split of the z N_f IDFT) is gathered from T in pass 1, transformed by
-// passes 1-2 (conjugate twiddles), combined over b with e^{i 2 pi b tau/(z N)}, windowed by
+// inverse's split of the z N_f IDFT) is gathered from T in stage 1, transformed by
+// both stages (conjugate twiddles), combined over b with e^{i 2 pi b tau/(z N)}, windowed by
 // g[tau + c]/N_f (a9), and overlap-added by a gather kernel (one thread per output sample,
 // frames in ascending order: no atomics, deterministic) (a10, Eq. 26).  For narrow bands with a
 // large z (B L small against z N_f log N_f, e.g. the §5.2 Fig. 16(e) shape, z = 20) the plan
@@ -479,278 +482,6 @@ __global__ void __launch_bounds__(kBinThreads) mp_bins_kernel(const FwdArgs a, c
     }
 }
 
-// f3a fused forward: the cluster FFT with a3-a7 kept on chip.  After stage 2 each CTA holds the
-// spectrum rows k1 it owns (k = k1 + R1 k2); bin k pairs Z[k] (local) with Z[N - k] (row R1 - k1:
-// another CTA's shared memory, read through DSMEM), so the per-bin decision (decide.cuh, the same
-// bin_target as every other path) runs without the spectrum ever reaching HBM.  The frame's
-// ||z_m||^2 (R23 margins) and its max |S| (fixed-point scale) are reduced across the cluster in rank
-// order; each CTA squeezes its bins into a private int64 fixed-point row in shared memory (exact, any
-// order), and CTA r sums the 8 rows for the band slice [r B/8, (r+1) B/8) and writes it to T.  HBM
-// traffic per frame: the x gather (mostly L2 hits between overlapping frames) and the band row.
-// cluster barrier for the fused kernel: SST_CLU_RELAXED=1 builds a CTA-scope fence + relaxed arrive
-// (experiment: avoids the MEMBAR.ALL.GPU of the release arrive)
-__device__ __forceinline__ void cluster_sync_fast() {
-#ifdef SST_CLU_RELAXED
-    __threadfence_block();
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
-#else
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-#endif
-}
-
-constexpr int kPendRound = 8;                 // pending bins per cluster round (fused forward)
-
-template <int R1, int M>
-__global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kCluThreads) mp_fused_fwd_kernel(const MpPass p, const FwdArgs a) {
-    namespace cg = cooperative_groups;
-    constexpr int CT = M / (kTile * kClu), RT = R1 / (kTile * kClu);
-    constexpr int B1 = R1 * kTS, B2 = M * kTS;
-    constexpr int NW = kCluThreads / 32;
-    constexpr int KH = M / 2 + 1;                       // k2 <= M/2 covers every k <= N/2
-    constexpr int OWN = RT * kTile * KH;                // owned bin slots
-    static_assert(CT * B1 == RT * B2 && OWN * 12 <= CT * B1 * 8 && kCluThreads == kBinThreads, "fused tiling");
-    extern __shared__ __align__(16) float2 mp_smem[];
-    __shared__ float red[NW];
-    __shared__ float nrm_part, vmax_part;
-    __shared__ int plist[kCluThreads];
-    __shared__ int pcount;
-    __shared__ double4 ppart[kPendRound][NW];
-    float2* const hA = mp_smem;
-    float2* const hB = mp_smem + CT * B1;
-    cg::cluster_group cl = cg::this_cluster();
-    const int rank = (int)cl.block_rank();
-    const int64_t fi = blockIdx.x / kClu;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int N = p.N;
-    // stage 1 (+ this CTA's share of ||z_m||^2 = sum |z[n]|^2)
-    float e = 0.0f;
-#pragma unroll 8
-    for (int idx = tid; idx < CT * R1 * kTile; idx += kCluThreads) {
-        const int ct = idx / (R1 * kTile), rem = idx - ct * (R1 * kTile);
-        const int i = rem >> 4, al = rem & 15;
-        const float2 v = load_elem<kLoadFwd>(p, fi, (rank * CT + ct) * kTile + al + M * i);
-        e = fmaf(v.x, v.x, fmaf(v.y, v.y, e));
-        hA[ct * B1 + i * kTS + al] = v;
-    }
-    const float e_cta = block_sum(e, red);            // barrier inside: stage-1 tiles complete
-    if (tid == 0) nrm_part = e_cta;
-    float2* res = hA;
-#pragma unroll
-    for (int ct = 0; ct < CT; ++ct) res = stockham16<R1, -1, kCluThreads>(hA + ct * B1, hB + ct * B1, N, p.twN) - ct * B1;
-    float2* const fre = res == hA ? hB : hA;
-    for (int idx = tid; idx < CT * R1 * kTile; idx += kCluThreads) {
-        const int ct = idx / (R1 * kTile), rem = idx - ct * (R1 * kTile);
-        const int k = rem >> 4, al = rem & 15;
-        const int a_ = (rank * CT + ct) * kTile + al;
-        if (a_ && k) {
-            float2& v = res[ct * B1 + k * kTS + al];
-            v = c_mul(v, tw_at<-1>(p.twN, ((int64_t)a_ * k) & (N - 1)));
-        }
-    }
-    cluster_sync_fast();
-    float nrm2 = 0.0f;
-#pragma unroll
-    for (int r = 0; r < kClu; ++r) nrm2 += *cl.map_shared_rank(&nrm_part, r);
-    constexpr int GATHER = RT * M * kTile;
-#pragma unroll 4
-    for (int idx = tid; idx < GATHER; idx += kCluThreads) {
-        const int al = idx & 15, k1l = (idx >> 4) & 15, rest = idx >> 8;
-        const int r = rest / (M / kTile), at = rest - r * (M / kTile);
-        const int src = at / CT, ct = at - src * CT;
-        const int k1 = (rank * RT + r) * kTile + k1l;
-        const float2* rp = cl.map_shared_rank(res, src);
-        fre[r * B2 + (at * kTile + al) * kTS + k1l] = rp[ct * B1 + k1 * kTS + al];
-    }
-    cluster_sync_fast();
-    float2* zb = fre;
-#pragma unroll
-    for (int r = 0; r < RT; ++r) zb = stockham16<M, -1, kCluThreads>(fre + r * B2, res + r * B2, N, p.twN) - r * B2;
-    float2* const other = zb == fre ? res : fre;
-    float2* const Sst = other;                                        // [OWN] S = (Z[k] + conj Z[N-k]) / 2
-    int* const lst = reinterpret_cast<int*>(other + OWN);             // [OWN] target, < 0 none, -4 pending
-    cluster_sync_fast();                                                        // every CTA's spectrum rows visible
-    float gam4 = a.gamma2x4;
-    if (a.absmax_dev) {
-        const float gm = a.gamma_rel * __ldg(a.absmax_dev);
-        gam4 = 4.0f * gm * gm;
-    }
-    float cm, km;
-    fwd_margins(a, gam4, nrm2, cm, km);
-    for (int ib = tid; ib < OWN; ib += kCluThreads) {
-        const int r = ib / (kTile * KH), rem = ib - r * (kTile * KH);
-        const int k2 = rem >> 4, al = rem & 15;
-        const int k1 = (rank * RT + r) * kTile + al;
-        const int k = k1 + R1 * k2;
-        int l = -1;
-        float2 S = make_float2(0.0f, 0.0f);
-        if (k <= N / 2) {
-            const float2 za = zb[r * B2 + k2 * kTS + al];
-            const int k1b = k1 ? R1 - k1 : 0, k2b = k1 ? M - 1 - k2 : (M - k2) & (M - 1);   // N - k
-            const int ob = k1b / (RT * kTile), rb = (k1b / kTile) % RT, alb = k1b % kTile;
-            const float2 zm = cl.map_shared_rank(zb, ob)[rb * B2 + k2b * kTS + alb];
-            float2 PQ, UV;
-            float mag4;
-            bool unsure;
-            l = bin_target<false>(a, gam4, cm, km, k, za, zm, PQ, UV, mag4, unsure);
-            if (unsure) l = -4;
-            S = make_float2(0.5f * PQ.x, 0.5f * PQ.y);
-        }
-        Sst[ib] = S;
-        lst[ib] = l;
-    }
-    // Pending bins (R23) are re-decided by the whole cluster together: the cluster waits at its
-    // barriers for the slowest CTA anyway, so one CTA's pending bin should not run on 16 warps while
-    // 112 others idle.  Virtual warp (rank, warp) of kClu NW sums part rank NW + warp of the taps
-    // (stft_bin_fp64_part, a fixed decomposition); the owner adds the parts in a fixed tree.  The
-    // fixed-point scale takes max |S| over kept AND pending bins (a bound either way), so it is
-    // exchanged at the same barrier as the pending lists.
-    __syncthreads();
-    if (tid == 0) pcount = 0;
-    __syncthreads();
-    float vmax = 0.0f;
-    for (int ib = tid; ib < OWN; ib += kCluThreads) {
-        const int l = lst[ib];
-        if (l >= 0 || l == -4) {
-            const float2 S = Sst[ib];
-            vmax = fmaxf(vmax, fmaxf(fabsf(S.x), fabsf(S.y)));
-        }
-        if (l == -4) {
-            const int slot = atomicAdd(&pcount, 1);
-            if (slot < kCluThreads) plist[slot] = ib;
-        }
-    }
-    const float mloc = block_max(vmax, red);
-    if (tid == 0) vmax_part = mloc;
-    cluster_sync_fast();                                                        // remote Z reads done; lists, maxima visible
-    float m = 0.0f;
-    int cnt[kClu], total = 0;
-#pragma unroll
-    for (int r = 0; r < kClu; ++r) {
-        m = fmaxf(m, *cl.map_shared_rank(&vmax_part, r));
-        cnt[r] = min(*cl.map_shared_rank(&pcount, r), kCluThreads);
-        total += cnt[r];
-    }
-    if (total > 0) {                                                  // cluster-uniform
-        const int64_t s0 = (a.frame_begin + fi) * a.hop - a.c;
-        const int64_t v_lo = a.x_off > 0 ? a.x_off : 0;
-        const int64_t v_hi = a.n < a.x_off + a.x_len ? a.n : a.x_off + a.x_len;
-        auto xat = [&](int j) -> float {
-            const int64_t sj = s0 + j;
-            return (sj >= v_lo && sj < v_hi) ? __ldg(a.x + (sj - a.x_off)) : 0.0f;
-        };
-        auto tap64 = [&](int j) { return __ldg(a.taps64 + j); };
-        const double gam64 = launch_gamma64(a);
-        // item g -> (owner r, its bin k, its slot ib)
-        auto item = [&](int g, int& r, int& ib) {
-            r = 0;
-            while (g >= cnt[r]) g -= cnt[r++];
-            ib = cl.map_shared_rank(plist, r)[g];
-            const int rr = ib / (kTile * KH), rem = ib - rr * (kTile * KH);
-            return (r * RT + rr) * kTile + (rem & 15) + R1 * (rem >> 4);
-        };
-        for (int g0 = 0; g0 < total; g0 += kPendRound) {
-            const int nr = min(kPendRound, total - g0);
-            for (int g = 0; g < nr; ++g) {
-                int r, ib;
-                const int kk = item(g0 + g, r, ib);
-                const double4 pr = stft_bin_fp64_part(xat, tap64, a.tw64, N, a.L, a.c, kk, rank * NW + warp, kClu * NW);
-                if (lane == 0) ppart[g][warp] = pr;
-            }
-            cluster_sync_fast();                                                // parts visible
-            for (int g = warp; g < nr; g += NW) {
-                int r, ib;
-                const int kk = item(g0 + g, r, ib);
-                if (r != rank) continue;
-                double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
-#pragma unroll
-                for (int j = 0; j < kClu * NW / 32; ++j) {            // lane sums parts 4 lane .. 4 lane + 3
-                    const int part = lane * (kClu * NW / 32) + j;
-                    const double4 v = cl.map_shared_rank(&ppart[0][0], part / NW)[g * NW + part % NW];
-                    t.x += v.x;
-                    t.y += v.y;
-                    t.z += v.z;
-                    t.w += v.w;
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    t.x += __shfl_xor_sync(0xffffffffu, t.x, o);
-                    t.y += __shfl_xor_sync(0xffffffffu, t.y, o);
-                    t.z += __shfl_xor_sync(0xffffffffu, t.z, o);
-                    t.w += __shfl_xor_sync(0xffffffffu, t.w, o);
-                }
-                if (lane == 0) {
-                    lst[ib] = decide_fp64(a, gam64, kk, t.x, t.y, t.z, t.w);
-                    atomicAdd(a.r23_count, 1ull);
-                }
-            }
-            cluster_sync_fast();                                                // parts consumed, decisions in place
-        }
-        if (pcount > kCluThreads) {                                   // list overflow (CTA-uniform): the rest here
-            for (int ib0 = 0; ib0 < OWN; ib0 += kCluThreads) {
-                const bool pend = ib0 + tid < OWN && lst[ib0 + tid] == -4;
-                __syncthreads();
-                if (tid == 0) pcount = 0;
-                __syncthreads();
-                if (pend) plist[atomicAdd(&pcount, 1)] = ib0 + tid;
-                const int np = __syncthreads_count(pend);
-                for (int i = 0; i < np; ++i) {
-                    const int jb = plist[i];
-                    const int rr = jb / (kTile * KH), rem = jb - rr * (kTile * KH);
-                    const int kk = (rank * RT + rr) * kTile + (rem & 15) + R1 * (rem >> 4);
-                    const double4 pr = stft_bin_fp64_part(xat, tap64, a.tw64, N, a.L, a.c, kk, warp, NW);
-                    if (lane == 0) ppart[0][warp] = pr;
-                    __syncthreads();
-                    if (tid == 0) {
-                        double sr = 0.0, si = 0.0, dr = 0.0, di = 0.0;
-                        for (int w = 0; w < NW; ++w) {
-                            sr += ppart[0][w].x;
-                            si += ppart[0][w].y;
-                            dr += ppart[0][w].z;
-                            di += ppart[0][w].w;
-                        }
-                        lst[jb] = decide_fp64(a, gam64, kk, sr, si, dr, di);
-                        atomicAdd(a.r23_count, 1ull);
-                    }
-                    __syncthreads();
-                }
-            }
-        }
-    }
-    // a6: exact fixed-point sums (mp_bins_kernel's scaling: |X| < 2^39, <= 2^15 + 1 terms per target)
-    const int ex = max(-87, (int)((__float_as_uint(m) >> 23) & 0xff) - 126);
-    const float scale = __uint_as_float((unsigned)(127 + 39 - ex) << 23);
-    const float iscale = __uint_as_float((unsigned)(127 - 39 + ex) << 23);
-    long long* const acc = reinterpret_cast<long long*>(zb);          // [bins][2]; the spectrum is dead
-    for (int i = tid; i < 2 * a.bins; i += kCluThreads) acc[i] = 0;
-    __syncthreads();
-    for (int ib = tid; ib < OWN; ib += kCluThreads) {
-        const int l = lst[ib];
-        if (l >= 0) {
-            SST_CHECK(l < a.bins);
-            const float2 S = Sst[ib];
-            long long xr, xi;
-            asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xr) : "f"(S.x * scale));
-            asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xi) : "f"(S.y * scale));
-            atomicAdd(reinterpret_cast<unsigned long long*>(acc + 2 * l), (unsigned long long)xr);
-            atomicAdd(reinterpret_cast<unsigned long long*>(acc + 2 * l + 1), (unsigned long long)xi);
-        }
-    }
-    cluster_sync_fast();                                                        // partial rows complete
-    float2* const trow = a.T + (fi + 0) * a.ldT;
-    const int l0 = (int)((int64_t)a.bins * rank / kClu), l1 = (int)((int64_t)a.bins * (rank + 1) / kClu);
-    for (int l = l0 + tid; l < l1; l += kCluThreads) {
-        long long sr = 0, si = 0;
-#pragma unroll
-        for (int r = 0; r < kClu; ++r) {
-            const long long* ap = cl.map_shared_rank(acc, r);
-            sr += ap[2 * l];
-            si += ap[2 * l + 1];
-        }
-        trow[l] = make_float2(__ll2float_rn(sr) * iscale, __ll2float_rn(si) * iscale);
-    }
-    cluster_sync_fast();                                                        // keep shared memory until all reads end
-}
-
 // a9 tail: combine the residues of each frame pair, window by g[tau + c]/N_f, write frames A, B
 __global__ void __launch_bounds__(256) mp_combine_kernel(const MpInvArgs a, const float2* Y) {
     const int64_t pair = blockIdx.x;
@@ -810,6 +541,7 @@ __global__ void __launch_bounds__(256) mp_direct_kernel(const MpInvArgs a) {
     };
     auto red = [&](int64_t x) { int64_t r = x % zN; return r < 0 ? r + zN : r; };
     const float2 w = e_of(red(tau));
+    const float2 wi = make_float2(-w.y, w.x);                           // i w: h w + t as two packed FMAs
     const int64_t step = red(32 * tau);
     int64_t rb = 0;                                                     // 32 lb tau mod z N
     float2 acc = make_float2(0.0f, 0.0f);
@@ -820,12 +552,12 @@ __global__ void __launch_bounds__(256) mp_direct_kernel(const MpInvArgs a) {
 #pragma unroll
             for (int ll = 30; ll >= 0; --ll) {
                 const float2 t = trow[l0 + ll];
-                h = make_float2(fmaf(h.x, w.x, fmaf(-h.y, w.y, t.x)), fmaf(h.x, w.y, fmaf(h.y, w.x, t.y)));
+                h = __ffma2_rn(make_float2(h.x, h.x), w, __ffma2_rn(make_float2(h.y, h.y), wi, t));
             }
         } else {
             for (int ll = n - 2; ll >= 0; --ll) {
                 const float2 t = trow[l0 + ll];
-                h = make_float2(fmaf(h.x, w.x, fmaf(-h.y, w.y, t.x)), fmaf(h.x, w.y, fmaf(h.y, w.x, t.y)));
+                h = __ffma2_rn(make_float2(h.x, h.x), w, __ffma2_rn(make_float2(h.y, h.y), wi, t));
             }
         }
         const float2 ph = e_of(rb);
@@ -885,20 +617,6 @@ cudaError_t launch_mp_forward(const FwdArgs& f, int mode, const float2* twN, flo
     p.c = f.c;
     p.taps = f.taps;
     cudaError_t e;
-    static const bool unfused = [] { const char* v = getenv("SST_MP_UNFUSED"); return v && atoi(v) != 0; }();
-    if (mode == kModeForward && !unfused && nfr * kClu < ((int64_t)1 << 31)) {
-        void (*fk)(const MpPass, const FwdArgs) = nullptr;
-        int half = 0;                                                  // CT B1 float2
-        if (p.R1 == 128 && p.M == 128) { fk = mp_fused_fwd_kernel<128, 128>; half = 128 * kTS; }
-        else if (p.R1 == 256 && p.M == 128) { fk = mp_fused_fwd_kernel<256, 128>; half = 256 * kTS; }
-        else if (p.R1 == 256 && p.M == 256) { fk = mp_fused_fwd_kernel<256, 256>; half = 2 * 256 * kTS; }
-        if (fk && 2 * f.bins <= half) {
-            const int smem = 2 * half * (int)sizeof(float2);
-            if ((e = cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
-            fk<<<(unsigned)(nfr * kClu), kCluThreads, smem, s>>>(p, f);
-            return cudaGetLastError();
-        }
-    }
     if ((e = run_fft<kLoadFwd, -1>(p, buf0, buf1, s)) != cudaSuccess) return e;
     const int ch = mp_bins_chunk(f.bins);
     switch (mode) {

@@ -3,7 +3,7 @@
 # the report is summarised on the box (gpurun_out/ must stay under 64 MiB) and then deleted
 TAG=${1:-r1}
 mkdir -p gpurun_out
-CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-extras"
+CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-extras --no-traffic --legs ''"
 $CMD > gpurun_out/ncu_bench_plain_$TAG.log 2>&1 && \
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"fwd_kernel|inv_kernel" -s 6 -c 2 \
    -o /tmp/prof_bench_$TAG -f $CMD > gpurun_out/ncu_bench_$TAG.log 2>&1
