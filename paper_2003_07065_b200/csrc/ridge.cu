@@ -8,7 +8,8 @@
 //                  exactly by level-synchronous divide and conquer: level d fixes the points
 //                  whose 1-based index has lowest set bit S/2^(d+1) (S = pow2 > B), searching
 //                  only between the optima of their already-solved neighbours: O(B log B) per
-//                  frame instead of O(B^2), same result.  Backpointers (int32) go to global
+//                  frame instead of O(B^2), same result.  Candidates are rounded as the oracle
+//                  rounds them (no fused multiply-add).  Backpointers (int32) go to global
 //                  memory; one thread traces the path back.  After each ridge the zone
 //                  +-suppress bins is set to the floor emission log(eps).
 //  zone_mask:      T outside (or inside) the zone |l - path[m]| <= half set to zero.
@@ -61,13 +62,20 @@ cudaError_t launch_ridge_emission(const float2* T, int64_t rows, int64_t cols, i
 // ------------------------------------------------------------------------------ DP ------------
 constexpr int kRidgeThreads = 1024;
 
+// V[a] - lam (l - a)^2 rounded as the oracle rounds it (product, then difference): written with
+// explicit _rn intrinsics so that the compiler cannot contract it into one fused multiply-add,
+// whose single rounding could order near-tied candidates differently from the oracle's argmax
+__device__ __forceinline__ double ridge_cand(const double* V, int l, int a, double lam) {
+    const double dd = (double)(l - a);
+    return __dsub_rn(V[a], __dmul_rn(lam, dd * dd));
+}
+
 // smallest maximiser of V[a] - lam (l - a)^2 over a in [a0, a1] by one thread
 __device__ __forceinline__ void scan_thread(const double* V, int l, int a0, int a1, double lam, double& best, int& arg) {
     best = -INFINITY;
     arg = a0;
     for (int a = a0; a <= a1; ++a) {
-        const double d = (double)(l - a);
-        const double v = V[a] - lam * (d * d);
+        const double v = ridge_cand(V, l, a, lam);
         if (v > best) { best = v; arg = a; }
     }
 }
@@ -76,7 +84,7 @@ __global__ void __launch_bounds__(kRidgeThreads, 1)
 ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int suppress, const double* floor_in,
                 int32_t* back, int32_t* paths) {
     extern __shared__ __align__(16) unsigned char sm[];
-    double* V = reinterpret_cast<double*>(sm);            // [cols] previous frame
+    double* V = reinterpret_cast<double*>(sm);            // [cols] previous frame (ping-pong with Vn)
     double* Vn = V + cols;                                 // [cols] current frame
     double* En = Vn + cols;                                // [cols] emission row of the frame, prefetched
     int* opt = reinterpret_cast<int*>(En + cols);          // [cols]
@@ -108,8 +116,7 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
                         double best = -INFINITY;
                         int arg = a0;
                         for (int a = a0 + lane; a <= a1; a += 32) {
-                            const double dd = (double)(l - a);
-                            const double v = V[a] - lam * (dd * dd);
+                            const double v = ridge_cand(V, l, a, lam);
                             if (v > best) { best = v; arg = a; }
                         }
 #pragma unroll
@@ -136,12 +143,11 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
             __pipeline_wait_prior(0);                         // this frame's emissions (own copies)
             for (int l = tid; l < cols; l += kRidgeThreads) {
                 const int a = opt[l];
-                const double dd = (double)(l - a);
-                Vn[l] = En[l] + (V[a] - lam * (dd * dd));
+                Vn[l] = __dadd_rn(En[l], ridge_cand(V, l, a, lam));
                 bk[l] = a;
             }
             __syncthreads();
-            for (int l = tid; l < cols; l += kRidgeThreads) V[l] = Vn[l];
+            { double* t = V; V = Vn; Vn = t; }                // ping-pong: the new row becomes V
             // prefetch the next frame's emission row (each thread copies the entries it reads)
             if (m + 1 < rows)
                 for (int l = tid; l < cols; l += kRidgeThreads)
