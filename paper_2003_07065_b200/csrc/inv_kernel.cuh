@@ -19,8 +19,12 @@ namespace sst {
 // RM: every nonzero sub-spectrum entry q (band [k1, k2) or mirror [N - k2, N)) has
 // q / N2 in [0, RM) or [64 - RM, 64) (i.e. ceil(k2 / N2) <= RM): other rows of the step-1
 // input are compile-time zeros and cost nothing (narrow bands: C2, C3 use RM = 5, C4 RM = 8).
+// RM = kRmFull: the full band (k1 = 0, B = z N/2, e.g. C5): every row is live and the T index of
+// an entry is affine in its row, so the loads need no per-entry index arithmetic.
 // ZONE: the mode-retrieval zone is applied to the T loads (a.zone_path); a separate
 // instantiation, so the plain inverse carries no zone arithmetic
+constexpr int kRmFull = 0;
+
 template <int N2, bool FULLWIN, int RM, bool ZONE>
 __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 256 ? 1 : 2) inv_kernel(const InvArgs a) {
     using Gm = Geom<N2, false>;
@@ -89,37 +93,66 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
             const int zA = ZONE && vA ? __ldg(a.zone_path + fA) : 0;
             const int zB = ZONE && vB ? __ldg(a.zone_path + fA + 1) : 0;
             float2 v[64];
-            // band entries q in [k1, k2): l = z (q - k1) + b; mirror entries: l' = z (N - k1 - q) - b
-            const int zstep = zoom * N2;                           // l step per row n1
-            const int lbase = zoom * (tg - k1) + b;                // band l at n1 = 0
-            const int mbase = zoom * (N - k1 - tg) - b;            // mirror l at n1 = 0
+            if constexpr (RM == kRmFull) {
+                // full band (k1 = 0, B = z N/2): rows n1 < 32 hold the band entries q = N2 n1 + tg
+                // (li = z q + b), rows n1 >= 32 the mirror entries (li = z (N - q) - b); li is affine
+                // in n1, so each entry is one load at a fixed stride from a per-thread base, with no
+                // index arithmetic or range tests.  The one empty entry is q = N/2 at b = 0 (li = B).
+                const int zs = zoom * N2;
+                const float2* pA = TA + (zoom * tg + b);
+                const float2* pB = TB + (zoom * tg + b);
 #pragma unroll
-            for (int n1 = 0; n1 < 64; ++n1) {
-                if (n1 >= RM && n1 < 64 - RM) {                   // outside band and mirror
-                    v[n1] = make_float2(0.0f, 0.0f);
-                    continue;
+                for (int n1 = 0; n1 < 32; ++n1) {
+                    SST_CHECK(zoom * (N2 * n1 + tg) + b < a.bins);
+                    float2 ta = vA ? __ldg(pA + n1 * zs) : make_float2(0.0f, 0.0f);
+                    float2 tb = vB ? __ldg(pB + n1 * zs) : make_float2(0.0f, 0.0f);
+                    if (n1 == 0 && tg == 0 && b == 0) { ta.y = 0.0f; tb.y = 0.0f; }   // DC: real part only (R14)
+                    v[n1] = make_float2(ta.x - tb.y, ta.y + tb.x);                  // H_A + i H_B
                 }
-                const int q = N2 * n1 + tg;                       // sub-spectrum index (coarse bin)
-                // RM < 32: rows below RM can only hold band entries, rows above 64 - RM only mirror
-                // entries (k2 <= RM N2 and N - k2 >= (64 - RM) N2)
-                const bool lower = (RM < 32) ? (n1 < RM) : true;
-                const bool upper = (RM < 32) ? (n1 >= 64 - RM) : true;
-                const bool inb = lower && (unsigned)(q - k1) < (unsigned)nr;
-                const int lm = mbase - n1 * zstep;
-                const bool inm = upper && !inb && q > 0 && (unsigned)lm < (unsigned)a.bins;
-                const int li = inb ? lbase + n1 * zstep : lm;
-                float2 ta = make_float2(0.0f, 0.0f), tb = make_float2(0.0f, 0.0f);
-                SST_CHECK(!(inb || inm) || (li >= 0 && li < a.bins));
-                const bool okA = !ZONE || ((abs(li - zA) <= a.zone_half) == (bool)a.zone_keep);
-                const bool okB = !ZONE || ((abs(li - zB) <= a.zone_half) == (bool)a.zone_keep);
-                if ((inb || inm) && vA && okA) ta = __ldg(TA + li);
-                if ((inb || inm) && vB && okB) tb = __ldg(TB + li);
-                if (n1 == 0 && q == 0 && b == 0) { ta.y = 0.0f; tb.y = 0.0f; }  // DC: real part only (R14)
-                if (n1 == 32 && q == N / 2 && b == 0) { ta.y = 0.0f; tb.y = 0.0f; }   // Nyquist (full band only)
-                v[n1] = inb ? make_float2(ta.x - tb.y, ta.y + tb.x)    // H_A + i H_B
-                            : make_float2(ta.x + tb.y, tb.x - ta.y);   // conj H_A + i conj H_B
+                const float2* mA = TA + (zoom * (N / 2 - tg) - b);                 // li at n1 = 32
+                const float2* mB = TB + (zoom * (N / 2 - tg) - b);
+                const bool m0 = tg != 0 || b != 0;                                  // q = N/2, b = 0: none
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const bool ok = j > 0 || m0;
+                    SST_CHECK(!ok || (zoom * (N / 2 - tg) - b - j * zs >= 0 && zoom * (N / 2 - tg) - b - j * zs < a.bins));
+                    const float2 ta = (vA && ok) ? __ldg(mA - j * zs) : make_float2(0.0f, 0.0f);
+                    const float2 tb = (vB && ok) ? __ldg(mB - j * zs) : make_float2(0.0f, 0.0f);
+                    v[32 + j] = make_float2(ta.x + tb.y, tb.x - ta.y);              // conj H_A + i conj H_B
+                }
+            } else {
+                // band entries q in [k1, k2): l = z (q - k1) + b; mirror entries: l' = z (N - k1 - q) - b
+                const int zstep = zoom * N2;                           // l step per row n1
+                const int lbase = zoom * (tg - k1) + b;                // band l at n1 = 0
+                const int mbase = zoom * (N - k1 - tg) - b;            // mirror l at n1 = 0
+#pragma unroll
+                for (int n1 = 0; n1 < 64; ++n1) {
+                    if (n1 >= RM && n1 < 64 - RM) {                   // outside band and mirror
+                        v[n1] = make_float2(0.0f, 0.0f);
+                        continue;
+                    }
+                    const int q = N2 * n1 + tg;                       // sub-spectrum index (coarse bin)
+                    // RM < 32: rows below RM can only hold band entries, rows above 64 - RM only mirror
+                    // entries (k2 <= RM N2 and N - k2 >= (64 - RM) N2)
+                    const bool lower = (RM < 32) ? (n1 < RM) : true;
+                    const bool upper = (RM < 32) ? (n1 >= 64 - RM) : true;
+                    const bool inb = lower && (unsigned)(q - k1) < (unsigned)nr;
+                    const int lm = mbase - n1 * zstep;
+                    const bool inm = upper && !inb && q > 0 && (unsigned)lm < (unsigned)a.bins;
+                    const int li = inb ? lbase + n1 * zstep : lm;
+                    float2 ta = make_float2(0.0f, 0.0f), tb = make_float2(0.0f, 0.0f);
+                    SST_CHECK(!(inb || inm) || (li >= 0 && li < a.bins));
+                    const bool okA = !ZONE || ((abs(li - zA) <= a.zone_half) == (bool)a.zone_keep);
+                    const bool okB = !ZONE || ((abs(li - zB) <= a.zone_half) == (bool)a.zone_keep);
+                    if ((inb || inm) && vA && okA) ta = __ldg(TA + li);
+                    if ((inb || inm) && vB && okB) tb = __ldg(TB + li);
+                    if (n1 == 0 && q == 0 && b == 0) { ta.y = 0.0f; tb.y = 0.0f; }  // DC: real part only (R14)
+                    if (n1 == 32 && q == N / 2 && b == 0) { ta.y = 0.0f; tb.y = 0.0f; }   // Nyquist (full band only)
+                    v[n1] = inb ? make_float2(ta.x - tb.y, ta.y + tb.x)    // H_A + i H_B
+                                : make_float2(ta.x + tb.y, tb.x - ta.y);   // conj H_A + i conj H_B
+                }
             }
-            if constexpr (RM < 32) FftSparse64<+1, RM>::run(v);   // zero rows skipped
+            if constexpr (RM != kRmFull && RM < 32) FftSparse64<+1, RM>::run(v);   // zero rows skipped
             else Fft<64, +1>::run(v);
 #pragma unroll
             for (int kk = 0; kk < 64; ++kk) {
@@ -306,6 +339,7 @@ static cudaError_t launch_inv_b(const InvArgs& a, int grid, cudaStream_t s) {
 template <int N2, bool FULLWIN>
 static cudaError_t launch_inv_r(const InvArgs& a, int grid, cudaStream_t s) {
     if (a.zone_path) return launch_inv_b<N2, FULLWIN, 64, true>(a, grid, s);   // mode retrieval (f1)
+    if (a.k1 == 0 && a.bins == a.zoom * (Geom<N2, false>::N / 2)) return launch_inv_b<N2, FULLWIN, kRmFull>(a, grid, s);   // C5
     const int rows = (a.k1 + a.bins / a.zoom + N2 - 1) / N2;   // ceil(k2 / N2)
     if (rows <= 5) return launch_inv_b<N2, FULLWIN, 5>(a, grid, s);   // C2, C3
     if (rows <= 8) return launch_inv_b<N2, FULLWIN, 8>(a, grid, s);
