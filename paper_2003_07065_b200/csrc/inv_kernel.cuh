@@ -99,15 +99,18 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
                 // in n1, so each entry is one load at a fixed stride from a per-thread base, with no
                 // index arithmetic or range tests.  The one empty entry is q = N/2 at b = 0 (li = B).
                 const int zs = zoom * N2;
+                // no validity predicates: an invalid item (vA false) is never combined, and with no
+                // frame B, TB = TA makes H_B Hermitian, so frame A's real part is unaffected and the
+                // imaginary part is not added (hasB false); every address stays inside row f_lo / fA
                 const float2* pA = TA + (zoom * tg + b);
                 const float2* pB = TB + (zoom * tg + b);
 #pragma unroll
                 for (int n1 = 0; n1 < 32; ++n1) {
                     SST_CHECK(zoom * (N2 * n1 + tg) + b < a.bins);
-                    float2 ta = vA ? __ldg(pA + n1 * zs) : make_float2(0.0f, 0.0f);
-                    float2 tb = vB ? __ldg(pB + n1 * zs) : make_float2(0.0f, 0.0f);
+                    float2 ta = __ldg(pA + n1 * zs);
+                    float2 tb = __ldg(pB + n1 * zs);
                     if (n1 == 0 && tg == 0 && b == 0) { ta.y = 0.0f; tb.y = 0.0f; }   // DC: real part only (R14)
-                    v[n1] = make_float2(ta.x - tb.y, ta.y + tb.x);                  // H_A + i H_B
+                    v[n1] = __fadd2_rn(ta, make_float2(-tb.y, tb.x));                // H_A + i H_B
                 }
                 const float2* mA = TA + (zoom * (N / 2 - tg) - b);                 // li at n1 = 32
                 const float2* mB = TB + (zoom * (N / 2 - tg) - b);
@@ -116,9 +119,9 @@ __global__ void __launch_bounds__(Geom<N2, false>::TPB, Geom<N2, false>::TPB == 
                 for (int j = 0; j < 32; ++j) {
                     const bool ok = j > 0 || m0;
                     SST_CHECK(!ok || (zoom * (N / 2 - tg) - b - j * zs >= 0 && zoom * (N / 2 - tg) - b - j * zs < a.bins));
-                    const float2 ta = (vA && ok) ? __ldg(mA - j * zs) : make_float2(0.0f, 0.0f);
-                    const float2 tb = (vB && ok) ? __ldg(mB - j * zs) : make_float2(0.0f, 0.0f);
-                    v[32 + j] = make_float2(ta.x + tb.y, tb.x - ta.y);              // conj H_A + i conj H_B
+                    const float2 ta = ok ? __ldg(mA - j * zs) : make_float2(0.0f, 0.0f);
+                    const float2 tb = ok ? __ldg(mB - j * zs) : make_float2(0.0f, 0.0f);
+                    v[32 + j] = __fadd2_rn(make_float2(ta.x, tb.x), make_float2(tb.y, -ta.y));   // conj H_A + i conj H_B
                 }
             } else {
                 // band entries q in [k1, k2): l = z (q - k1) + b; mirror entries: l' = z (N - k1 - q) - b
