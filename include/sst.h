@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SST_ABI_VERSION 3
+#define SST_ABI_VERSION 4
 
 typedef enum {
     SST_OK = 0,
@@ -109,9 +109,16 @@ typedef struct {
                              of frames, N_f <= 8192), SST_PATH_MULTIPASS (N_f > 8192) or
                              SST_PATH_FILTERBANK (SST_SOURCE_TRUNCATE with a narrow band: the
                              frequency-domain filter bank of P:L485, §6); set by sst_plan_create  */
+    int32_t inverse_path; /* how sst_inverse computes Eq. 25-26 (same results contract):
+                             SST_IPATH_RESIDUE (z N_f-point IDFT split into z residue sub-IFFTs
+                             per frame pair), SST_IPATH_NARROWBAND (full window, band within 8 of
+                             64 rows, hop % 8 == 0: residue sum inside the transform, C2/C3) or
+                             SST_IPATH_MULTIPASS (N_f > 8192); SST_INV_NB=0 in the environment at
+                             plan creation disables the narrow-band path                        */
 } sst_layout;
 
 enum { SST_PATH_FUSED = 0, SST_PATH_MULTIPASS = 1, SST_PATH_FILTERBANK = 2 };
+enum { SST_IPATH_RESIDUE = 0, SST_IPATH_NARROWBAND = 1, SST_IPATH_MULTIPASS = 2 };
 
 /* sst_layout.warnings (also reported as text by sst_last_error after sst_plan_create) */
 enum {

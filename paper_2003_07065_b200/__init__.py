@@ -10,7 +10,7 @@ from ._lib import (  # noqa: F401
     SSTError, SST_OK, SST_E_INVALID_ARGUMENT, SST_E_COVERAGE, SST_E_UNSUPPORTED, SST_E_CUDA,
     SST_E_OUT_OF_MEMORY, SST_E_INTERNAL, SST_GAMMA_RELATIVE, SST_SOURCE_TRUNCATE, SST_DETERMINISTIC,
     SST_DISCRETE_CONSTANT, SST_FILTER_BANK, SST_WARN_EQ37, SST_WARN_EQ46, SST_PATH_FUSED,
-    SST_PATH_MULTIPASS, SST_PATH_FILTERBANK, LIB_PATH,
+    SST_PATH_MULTIPASS, SST_PATH_FILTERBANK, SST_IPATH_RESIDUE, SST_IPATH_NARROWBAND, SST_IPATH_MULTIPASS, LIB_PATH,
 )
 from .plan import Plan, gaussian_window, make_params, validate, layout, gamma_bound  # noqa: F401
 

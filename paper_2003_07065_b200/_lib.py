@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes
 import os
 
-ABI_VERSION = 3                  # SST_ABI_VERSION of include/sst.h this binding mirrors
+ABI_VERSION = 4                  # SST_ABI_VERSION of include/sst.h this binding mirrors
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # SST_LIB=bounds loads the -DSST_BOUNDS debug build (device-side bounds asserts); SST_LIB_PATH
 # overrides the path (dev A/B builds only)
@@ -47,6 +47,9 @@ SST_WARN_EQ46 = 2
 SST_PATH_FUSED = 0
 SST_PATH_MULTIPASS = 1
 SST_PATH_FILTERBANK = 2
+SST_IPATH_RESIDUE = 0
+SST_IPATH_NARROWBAND = 1
+SST_IPATH_MULTIPASS = 2
 
 _i32, _i64, _u32, _dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_double
 _vp = ctypes.c_void_p
@@ -65,7 +68,7 @@ class sst_layout(ctypes.Structure):
                 ("src_bins", _i32), ("fs", _dbl), ("f0_hz", _dbl), ("df_hz", _dbl), ("dfz_hz", _dbl),
                 ("gamma_abs", _dbl), ("alpha", _dbl), ("hf", _dbl), ("hf_bound", _dbl),
                 ("sigma_f_hz", _dbl), ("df_eq37_hz", _dbl), ("df_eq46_hz", _dbl), ("hf_bound46", _dbl),
-                ("warnings", _u32), ("forward_path", _i32)]
+                ("warnings", _u32), ("forward_path", _i32), ("inverse_path", _i32)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

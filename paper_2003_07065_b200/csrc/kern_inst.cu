@@ -18,9 +18,14 @@ int SST_CAT(occ_fwd_n2_, SST_INST_N2)(int L, int H, int device) { return occ_fwd
 }  // namespace sst
 #else
 #include "inv_kernel.cuh"
+#include "inv_nb_kernel.cuh"
 namespace sst {
 cudaError_t SST_CAT(launch_inv_n2_, SST_INST_N2)(const InvArgs& a, int grid, cudaStream_t s) {
+    if (a.nb) return launch_nb<SST_INST_N2>(a, grid, s);
     return launch_inv_t<SST_INST_N2>(a, grid, s);
+}
+int SST_CAT(occ_inv_nb_n2_, SST_INST_N2)(int hop, int L, int zoom, int k1, int bins, int device) {
+    return occ_nb<SST_INST_N2>(hop, L, zoom, k1, bins, device);
 }
 int SST_CAT(occ_inv_n2_, SST_INST_N2)(int hop, int L, int zoom, int device) {
     return occ_inv<SST_INST_N2>(hop, L, zoom, device);

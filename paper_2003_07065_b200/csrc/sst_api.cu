@@ -34,6 +34,7 @@ struct sst_plan {
     double cst = 0;                 // C (sqrt 2 or C_d)
     // device tables
     float2* d_taps = nullptr;       // [L]  (g, alpha g')
+    float* d_gwin = nullptr;        // [L]  g / N_f (narrow-band inverse window table)
     float2* d_tw = nullptr;         // [N_f]
     double2* d_taps64 = nullptr;    // [L]  (g, g') fp64 (R23 re-decision)
     double2* d_tw64 = nullptr;      // [N_f] exp(-2 pi i e/N_f) fp64
@@ -71,6 +72,7 @@ struct sst_plan {
     int64_t mp_fwd_frames = 0, mp_inv_pairs = 0;
     int32_t n_head = 0, n_tail = 0;
     int fwd_grid = 0, inv_grid = 0;
+    int inv_grid_nb = 0;            // narrow-band inverse (inv_nb_kernel.cuh): resident CTAs, 0 = not used
     bool redecide = true;           // R23 (SST_NO_REDECIDE=1 turns it off: timing experiments only)
     double r23_m = 6.0;             // R23 margin factor over the R21 error model (SST_R23_M: experiments)
     const float* ext_absmax = nullptr;
@@ -80,7 +82,7 @@ struct sst_plan {
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(device);
-        for (void* q : {(void*)d_taps, (void*)d_tw, (void*)d_taps64, (void*)d_tw64, (void*)d_mpl, (void*)d_r23, (void*)d_gq, (void*)d_gctr,
+        for (void* q : {(void*)d_taps, (void*)d_gwin, (void*)d_tw, (void*)d_taps64, (void*)d_tw64, (void*)d_mpl, (void*)d_r23, (void*)d_gq, (void*)d_gctr,
                         (void*)d_dirty_bits, (void*)d_dirty_list, (void*)d_fb_gam, (void*)d_fb_gamd,
                         (void*)d_fb_ph, (void*)d_fb_twns, (void*)d_fb_twp, (void*)d_fb_S, (void*)d_fb_Sd,
                         (void*)d_fb_eta, (void*)d_phz, (void*)d_renyi, (void*)d_amax2, (void*)d_back, (void*)d_inv_head, (void*)d_inv_tail,
@@ -684,7 +686,10 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
     }
     if (const char* nr = std::getenv("SST_NO_REDECIDE")) pl->redecide = !(nr[0] == '1');
     if (const char* mm = std::getenv("SST_R23_M")) { const double v = std::atof(mm); if (v > 0) pl->r23_m = v; }
+    std::vector<float> gwin(L);
+    for (int32_t j = 0; j < L; ++j) gwin[j] = (float)(pl->g[j] / Nf);
     if ((s = upload(pl, &pl->d_taps, taps)) != SST_OK || (s = upload(pl, &pl->d_tw, tw)) != SST_OK ||
+        (s = upload(pl, &pl->d_gwin, gwin)) != SST_OK ||
         (s = upload(pl, &pl->d_taps64, taps64)) != SST_OK || (s = upload(pl, &pl->d_tw64, tw64)) != SST_OK ||
         (s = upload(pl, &pl->d_phz, phz)) != SST_OK || (s = upload(pl, &pl->d_inv_head, head)) != SST_OK ||
         (s = upload(pl, &pl->d_inv_tail, tail)) != SST_OK || (s = upload(pl, &pl->d_inv_per, per)) != SST_OK) {
@@ -701,6 +706,7 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
         // multi-pass path: W_N table and scratch for a bounded chunk of frames (kMpScratch per buffer)
         pl->mp = true;
         pl->lay.forward_path = SST_PATH_MULTIPASS;
+        pl->lay.inverse_path = SST_IPATH_MULTIPASS;
         std::vector<float2> twN(Nf);
         for (int32_t k = 0; k < Nf; ++k) {
             const double a = -2.0 * kPi * k / Nf;
@@ -736,9 +742,16 @@ sst_status sst_plan_create(const sst_params* p, int device, sst_plan** out) {
             return fail(nullptr, SST_E_OUT_OF_MEMORY, "cudaMalloc R23 queue");
         }
         pl->inv_grid = sst::inverse_max_grid(Nf, H, L, z, device);
+        // narrow-band inverse where it applies (SST_INV_NB=0: the residue-split kernel, A/B and tests)
+        const char* nbe = std::getenv("SST_INV_NB");
+        if (!(nbe && nbe[0] == '0') &&
+            sst::inv_nb_applicable(Nf, L, pl->lay.center, H, z, pl->lay.k1, pl->lay.bins))
+            pl->inv_grid_nb = sst::inverse_nb_max_grid(Nf, H, L, z, pl->lay.k1, pl->lay.bins, device);
+        pl->lay.inverse_path = pl->inv_grid_nb > 0 ? SST_IPATH_NARROWBAND : SST_IPATH_RESIDUE;
         const int32_t seam_len = std::max(0, L - H);
         if (seam_len > 0) {
-            ce = cudaMalloc((void**)&pl->d_seam, sizeof(float) * (size_t)pl->inv_grid * 2 * seam_len);
+            ce = cudaMalloc((void**)&pl->d_seam,
+                            sizeof(float) * (size_t)std::max(pl->inv_grid, pl->inv_grid_nb) * 2 * seam_len);
             if (ce != cudaSuccess) { delete pl; cudaGetLastError(); return fail(nullptr, SST_E_OUT_OF_MEMORY, "cudaMalloc seams"); }
         }
         if (pl->fwd_grid <= 0 || pl->inv_grid <= 0) { delete pl; return fail(nullptr, SST_E_CUDA, "occupancy query failed"); }
@@ -1002,7 +1015,7 @@ sst_status sst_absmax(sst_plan* plan, const float* x, int64_t x_off, int64_t x_l
 }
 
 static sst::InvArgs inv_args(const sst_plan* pl, const float* T, int64_t ldT, int64_t fb, int64_t fe, float* y,
-                             int64_t y_off, int64_t y_len, int normalize, int* grid) {
+                             int64_t y_off, int64_t y_len, int normalize, int* grid, bool allow_nb = true) {
     sst::InvArgs a{};
     a.T = reinterpret_cast<const float2*>(T);
     a.ldT = ldT;
@@ -1017,6 +1030,7 @@ static sst::InvArgs inv_args(const sst_plan* pl, const float* T, int64_t ldT, in
     a.k1 = pl->lay.k1;
     a.bins = pl->lay.bins;
     a.taps = pl->d_taps;
+    a.gwin = pl->d_gwin;
     a.tw = pl->d_tw;
     a.phz = pl->d_phz;
     a.inv_n = (float)(1.0 / pl->lay.nfft);
@@ -1033,9 +1047,12 @@ static sst::InvArgs inv_args(const sst_plan* pl, const float* T, int64_t ldT, in
     a.seam = pl->d_seam;
     a.seam_len = std::max(0, pl->lay.win_len - pl->lay.hop);
     a.lay = sst::inv_layout(pl->lay.nfft / 64, pl->lay.win_len, pl->lay.hop, pl->lay.zoom);
+    a.nb = (allow_nb && pl->inv_grid_nb > 0) ? 1 : 0;
+    if (a.nb) a.lay = sst::inv_nb_layout(pl->lay.nfft / 64, pl->lay.win_len, pl->lay.hop, pl->lay.zoom, pl->lay.bins);
+    const int ctas = a.nb ? pl->inv_grid_nb : pl->inv_grid;
     const int64_t F = fe - fb;
     const int64_t min_fpc = (pl->lay.win_len + pl->lay.hop - 1) / pl->lay.hop;
-    int64_t fpc = (F + pl->inv_grid - 1) / pl->inv_grid;
+    int64_t fpc = (F + ctas - 1) / ctas;
     if (fpc < min_fpc) fpc = min_fpc;
     a.frames_per_cta = fpc;
     *grid = (int)((F + fpc - 1) / fpc);
@@ -1045,7 +1062,7 @@ static sst::InvArgs inv_args(const sst_plan* pl, const float* T, int64_t ldT, in
 // plain STFT synthesis (Eq. 10-11): the inverse kernel on the full one-sided band, z = 1,
 // with the normalisation 1/(C d) rescaled by C (tables hold 1/(C d[n]))
 static sst::InvArgs istft_args(const sst_plan* pl, const float* S, int64_t ldS, float* y, int* grid) {
-    sst::InvArgs a = inv_args(pl, S, ldS, 0, pl->lay.frames, y, 0, pl->lay.n, 1, grid);
+    sst::InvArgs a = inv_args(pl, S, ldS, 0, pl->lay.frames, y, 0, pl->lay.n, 1, grid, false);
     a.zoom = 1;
     a.k1 = 0;
     a.bins = pl->lay.nfft / 2 + 1;
@@ -1069,7 +1086,7 @@ static sst_status run_inverse(sst_plan* plan, const float* T, int64_t ldT, int64
         return sst_inverse_finalize(plan, y, y_off, y_len, stream);
     }
     int grid = 0;
-    sst::InvArgs a = inv_args(plan, T, ldT, fb, fe, y, y_off, y_len, normalize, &grid);
+    sst::InvArgs a = inv_args(plan, T, ldT, fb, fe, y, y_off, y_len, normalize, &grid, zone_path == nullptr);
     a.zone_path = zone_path;
     a.zone_half = zone_half;
     a.zone_keep = zone_keep;

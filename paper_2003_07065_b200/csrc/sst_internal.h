@@ -73,6 +73,32 @@ __host__ __device__ inline InvLayout inv_layout(int n2, int L, int H, int zoom) 
     return v;
 }
 
+// narrow-band inverse (inv_nb_kernel.cuh): the z N_f-point band IDFT as 64 x J (J = z N2) with the
+// sum over residues inside the second stage (warp shuffles) instead of a shared-memory round trip.
+// Applies to full windows (L = N_f, c = N_f / 2), N_f in {1024, 2048}, z in {1, 2, 4, 8}, hop a
+// multiple of 8 (chunks of the 64 rows then own disjoint OLA slot classes mod 8) and a band whose
+// band/mirror rows fit 8 of the 64 rows (RM <= 8: C2, C3).
+__host__ __device__ inline int inv_nb_rows(int n2, int k1, int bins, int zoom) { return (k1 + bins / zoom + n2 - 1) / n2; }
+__host__ __device__ inline bool inv_nb_applicable(int nfft, int L, int c, int hop, int zoom, int k1, int bins) {
+    const int n2 = nfft / 64;
+    if (n2 != 16 && n2 != 32) return false;
+    if (L != nfft || c != nfft / 2 || hop < 8 || hop % 8 != 0 || hop > L) return false;
+    if (zoom != 1 && zoom != 2 && zoom != 4 && zoom != 8) return false;
+    return inv_nb_rows(n2, k1, bins, zoom) <= 8;
+}
+// [chunk buffer: N2 rows x (J + z) float2][OLA ring: ring = round_up(L + 3 hop, 64 z) slots (sample
+// index mod ring), stored bank-skewed (inv_nb_kernel.cuh: up to ring / (2 z) + 32 more floats)]
+// [T staging: 2 buffers x 2 rows x round_up(B, 2) float2][2 mbarriers]   (g_off = T staging offset)
+__host__ __device__ inline InvLayout inv_nb_layout(int n2, int L, int H, int zoom, int bins) {
+    InvLayout v{};
+    v.pairs = 1;
+    v.ring_off = round_up(n2 * (zoom * n2 + zoom) * 8, 16);
+    v.ring = round_up(L + 3 * H, 64 * zoom);
+    v.g_off = round_up(v.ring_off + (v.ring + (zoom > 1 ? v.ring / (2 * zoom) : 0) + 64) * 4, 16);
+    v.total = v.g_off + 2 * 2 * round_up(bins, 2) * 8 + 16;
+    return v;
+}
+
 struct FwdArgs {
     const float* x;          // points at global sample x_off
     int64_t x_off, x_len;
@@ -125,6 +151,7 @@ struct InvArgs {
     int64_t frame_begin, frame_end;   // frames in this launch; T row 0 = frame_begin
     int32_t hop, L, c, nfft, zoom, k1, bins;
     const float2* taps;               // .x = g
+    const float* gwin;                // [L] g / N_f (narrow-band kernel)
     const float2* tw;                 // [nfft] tw[k1 * N2 + t] = W_N^{t k1} (conjugated here)
     const float2* phz;                // [z][64 + 2 N2] phase factors of exp(+2 pi i b tau/(z N)), see sst_api.cu
     float inv_n;                      // 1 / N_f
@@ -144,6 +171,7 @@ struct InvArgs {
     // is frame frame_begin.
     const int32_t* zone_path;
     int32_t zone_half, zone_keep;
+    int32_t nb;                       // 1: narrow-band kernel (inv_nb_kernel.cuh; lay = inv_nb_layout)
 };
 
 // Frequency-domain filter-bank STFT for truncated narrow bands (filterbank.cu)
@@ -213,6 +241,8 @@ cudaError_t launch_finalize(float* y, int64_t y_off, int64_t y_len, int64_t n, i
                             const float* inv_per, float out_scale, cudaStream_t s, const float* seam = nullptr,
                             int64_t seam_off = 0, int64_t seam_len = 0);
 int inverse_max_grid(int nfft, int hop, int L, int zoom, int device);
+// resident CTAs of the narrow-band inverse (0: not applicable)
+int inverse_nb_max_grid(int nfft, int hop, int L, int zoom, int k1, int bins, int device);
 
 // Renyi sums over a complex64 plane: partial[2*blockIdx] = {sum |T|^2, sum |T|^(2 alpha)},
 // then out = {sum, sum, entropy}; fixed reduction order

@@ -242,7 +242,8 @@ cudaError_t launch_finalize(float* y, int64_t y_off, int64_t y_len, int64_t n, i
     cudaError_t launch_fwd_n2_##n2(const FwdArgs& a, int mode, int grid, cudaStream_t s);    \
     int occ_fwd_n2_##n2(int L, int H, int device);                                          \
     cudaError_t launch_inv_n2_##n2(const InvArgs& a, int grid, cudaStream_t s);              \
-    int occ_inv_n2_##n2(int hop, int L, int zoom, int device);
+    int occ_inv_n2_##n2(int hop, int L, int zoom, int device);                              \
+    int occ_inv_nb_n2_##n2(int hop, int L, int zoom, int k1, int bins, int device);
 SST_DECL_N2(2)
 SST_DECL_N2(4)
 SST_DECL_N2(8)
@@ -289,6 +290,13 @@ int inverse_max_grid(int nfft, int hop, int L, int zoom, int device) {
     SST_SWITCH_N2(nfft, SST_CALL)
 #undef SST_CALL
     return -1;
+}
+
+int inverse_nb_max_grid(int nfft, int hop, int L, int zoom, int k1, int bins, int device) {
+#define SST_CALL(n2) occ_inv_nb_n2_##n2(hop, L, zoom, k1, bins, device)
+    SST_SWITCH_N2(nfft, SST_CALL)
+#undef SST_CALL
+    return 0;
 }
 #undef SST_SWITCH_N2
 

@@ -311,6 +311,10 @@ class Plan:
     def forward_path(self) -> int:
         return self.layout["forward_path"]
 
+    @property
+    def inverse_path(self) -> int:
+        return self.layout["inverse_path"]
+
     def targets(self, x: torch.Tensor, frame_begin: int = 0, frame_end: int | None = None, x_off: int = 0):
         fb, fe = self._frames(frame_begin, frame_end)
         out = torch.empty((fe - fb, self.src_bins), dtype=torch.int32, device=self.device)

@@ -33,7 +33,7 @@ def test_exports_every_declared_symbol(P):
     for n in names:
         assert hasattr(_lib.lib, n), n
         assert n in _lib.SIGNATURES, n
-    assert _lib.lib.sst_abi_version() == _lib.ABI_VERSION == 3
+    assert _lib.lib.sst_abi_version() == _lib.ABI_VERSION == 4
 
 
 def test_status_strings(P):
