@@ -68,7 +68,7 @@ def _traffic_committed(workload, kernel, frames):
         return None
 
 
-TRAFFIC_KERNELS = {"forward": "fwd_kernel", "inverse": "inv_kernel"}
+TRAFFIC_KERNELS = {"forward": "fwd_kernel", "inverse": "inv_(nb_)?kernel"}   # residue-split / narrow-band inverse
 
 
 def traffic_probe(workload):
@@ -658,8 +658,8 @@ def run_ours(args, cfg_base):
     if traffic["bytes"]:
         roofline["traffic_vs_algorithmic"] = traffic["bytes"] / ((fwd_b if dom == "forward" else inv_b) * nfr_rank)
     legs = {}
-    store = store_peak_gbs(dev) if args.legs else None
-    for name in [s for s in args.legs.split(",") if s]:
+    store = store_peak_gbs(dev) if args.legs not in ("", "none", "''") else None
+    for name in [s for s in args.legs.split(",") if s and s not in ("none", "''")]:
         legs[name] = measure_leg(P, D, name, world, rank, local, dev, args.leg_steps, 3, args.c5_chunk, hbm_gbs, store)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -705,7 +705,7 @@ def main():
     ap.add_argument("--e2e-chunks", type=int, default=8)
     ap.add_argument("--e2e-no-graph", action="store_true", help="launch the e2e round trip chunk by chunk")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--legs", default="C4,C5", help="extra fixed-record legs (strong scaling), '' for none")
+    ap.add_argument("--legs", default="C4,C5", help="extra fixed-record legs (strong scaling), 'none' for none")
     ap.add_argument("--leg-steps", type=int, default=3)
     ap.add_argument("--c5-chunk", type=int, default=1 << 20, help="C5 frames per chunk (T buffer 16 GiB)")
     ap.add_argument("--ref-frames", type=int, default=512)

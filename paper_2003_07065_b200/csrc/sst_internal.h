@@ -78,6 +78,11 @@ __host__ __device__ inline InvLayout inv_layout(int n2, int L, int H, int zoom) 
 // Applies to full windows (L = N_f, c = N_f / 2), N_f in {1024, 2048}, z in {1, 2, 4, 8}, hop a
 // multiple of 8 (chunks of the 64 rows then own disjoint OLA slot classes mod 8) and a band whose
 // band/mirror rows fit 8 of the 64 rows (RM <= 8: C2, C3).
+// T staging buffers of the narrow-band inverse: 2 (the copy of pair p + 1 is issued when pair p starts)
+// or 1 (issued after pair p's last stage-1 read; half the shared footprint)
+#ifndef SST_NB_TBUF
+#define SST_NB_TBUF 1
+#endif
 __host__ __device__ inline int inv_nb_rows(int n2, int k1, int bins, int zoom) { return (k1 + bins / zoom + n2 - 1) / n2; }
 __host__ __device__ inline bool inv_nb_applicable(int nfft, int L, int c, int hop, int zoom, int k1, int bins) {
     const int n2 = nfft / 64;
@@ -88,14 +93,15 @@ __host__ __device__ inline bool inv_nb_applicable(int nfft, int L, int c, int ho
 }
 // [chunk buffer: N2 rows x (J + z) float2][OLA ring: ring = round_up(L + 3 hop, 64 z) slots (sample
 // index mod ring), stored bank-skewed (inv_nb_kernel.cuh: up to ring / (2 z) + 32 more floats)]
-// [T staging: 2 buffers x 2 rows x round_up(B, 2) float2][2 mbarriers]   (g_off = T staging offset)
+// [T staging: 2 buffers x 2 rows x round_up(B + 1, 2) float2 (entry B: a zero)][2 mbarriers]
+// (g_off = T staging offset)
 __host__ __device__ inline InvLayout inv_nb_layout(int n2, int L, int H, int zoom, int bins) {
     InvLayout v{};
     v.pairs = 1;
     v.ring_off = round_up(n2 * (zoom * n2 + zoom) * 8, 16);
     v.ring = round_up(L + 3 * H, 64 * zoom);
     v.g_off = round_up(v.ring_off + (v.ring + (zoom > 1 ? v.ring / (2 * zoom) : 0) + 64) * 4, 16);
-    v.total = v.g_off + 2 * 2 * round_up(bins, 2) * 8 + 16;
+    v.total = v.g_off + SST_NB_TBUF * 2 * round_up(bins + 1, 2) * 8 + 16;
     return v;
 }
 

@@ -21,8 +21,8 @@ for r in rows[hi + 1:]:
     seq.append((r[ki], v * scale))
 bench = json.load(open(sys.argv[2])) if len(sys.argv) > 2 else None
 # the step ends at the last whole-record inverse (plus its seam launch)
-inv_max = max(ms for k, ms in seq if "inv_kernel" in k)
-last_whole = max(i for i, (k, ms) in enumerate(seq) if "inv_kernel" in k and ms > 0.5 * inv_max)
+inv_max = max(ms for k, ms in seq if ("inv_kernel" in k or "inv_nb_kernel" in k))
+last_whole = max(i for i, (k, ms) in enumerate(seq) if ("inv_kernel" in k or "inv_nb_kernel" in k) and ms > 0.5 * inv_max)
 step, e2e = seq[:last_whole + 2], seq[last_whole + 2:]
 
 
@@ -35,7 +35,7 @@ def table(part):
     return [f"{k} | {n} | {t / n:.3f} | {100 * t / tot:.1f}%" for k, (n, t) in acc.items()]
 
 
-print("# ncu launch list of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras` (round 1, C3 workload)")
+print("# ncu launch list of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras` (C3 workload, --legs none)")
 print("# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised: compare shares)")
 print("## device-timed step (whole-record forward + inverse): kernel | launches | mean ms | share")
 print("\n".join(table(step)))

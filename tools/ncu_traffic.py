@@ -11,7 +11,7 @@ t = json.load(open(path)) if os.path.exists(path) else {}
 for r in rows[2:]:
     d = dict(zip(h, r))
     name = d["Kernel Name"]
-    kern = "forward" if "fwd_kernel" in name else "inverse" if "inv_kernel" in name else None
+    kern = "forward" if "fwd_kernel" in name else "inverse" if ("inv_kernel" in name or "inv_nb_kernel" in name) else None
     if kern is None:
         continue
     def mb(k):
