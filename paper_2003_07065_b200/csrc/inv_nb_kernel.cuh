@@ -29,26 +29,29 @@ namespace sst {
 #endif
 
 
-template <int N2, int Z>
+template <int N2, int Z, bool FULL>
 struct NbGeom {
     static constexpr int N = 64 * N2;
     static constexpr int J = Z * N2;          // columns j_lo = threads per CTA
     static constexpr int TPB = J;
-    static constexpr int RPC = N2;            // rows tau_lo per chunk (= TPB / Z stage-2 rows)
-    static constexpr int KPC = N2 / 8;        // DIT indices k1' per chunk (rows tau_lo = k1' + 8 k2)
+    // narrow band: N2 rows per chunk (one stage-2 task per thread); full band: 32 rows per chunk,
+    // 32 / N2 tasks per thread
+    static constexpr int RPC = FULL ? 32 : N2;
+    static constexpr int KPC = RPC / 8;       // DIT indices k1' per chunk (rows tau_lo = k1' + 8 k2)
     static constexpr int CH = 64 / RPC;       // chunks per frame pair
+    static constexpr int TPT = RPC * Z / TPB; // stage-2 tasks per thread and chunk
     static constexpr int S = J + Z;           // padded row stride (float2): conflict-free stage-2 reads
-    static constexpr int OPL = N2 / Z;        // outputs per thread after the residue sum
+    static constexpr int OPL = N2 / Z;        // outputs per task after the residue sum
     static constexpr int LOGZ = Z == 1 ? 0 : Z == 2 ? 1 : Z == 4 ? 2 : 3;
     // OLA ring bank skew.  After the residue sum, lane b of a row holds outputs k = b + Z i, i.e.
     // tau = tau_lo + 64 b + 64 Z i: the Z lanes of a row are 64 b apart, the same bank.  A warp's
-    // 32/Z rows have tau_lo offsets {0..KPC-1} + 8 {0..R-1} (R = 256/J).  Slot s is stored at
+    // 32/Z rows have tau_lo offsets {0..KPC-1} + 8 {0..R-1} (R = (32/Z)/KPC).  Slot s is stored at
     // phys(s) = s + sum_j o_j bit(s, 6 + j) + SUPER (s >> (6 + LOGZ)): o_j = KPC 2^j for the first
     // log2(8/KPC) bits of b, then 8 R 2^j', so that the warp's banks tile the 32 banks; each o_j
     // exceeds the sum of the smaller ones and SUPER (a multiple of 32) exceeds them all, so phys is
     // monotone (injective), and s -> s + 64 Z moves phys by 64 Z + SUPER (a lane's consecutive
     // outputs are one constant stride apart).  Off when 8 R > 32 (C2's geometry).
-    static constexpr int R = 256 / J;
+    static constexpr int R = (32 / Z) / KPC > 0 ? (32 / Z) / KPC : 1;
     static constexpr int LOGK = KPC == 1 ? 3 : KPC == 2 ? 2 : KPC == 4 ? 1 : 0;   // log2(8 / KPC)
     static constexpr bool SKEW = Z > 1 && 8 * R <= 32;
     __host__ __device__ static constexpr int o(int j) { return j < LOGK ? KPC << j : (8 * R) << (j - LOGK); }
@@ -66,11 +69,20 @@ struct NbGeom {
     }
 };
 
+// RM <= 8: narrow band (T rows staged by TMA); RM = kNbFull: full band (k1 = 0, B = z N/2: every row
+// nonzero, one full 64-point DFT per column, T loaded straight into registers)
+constexpr int kNbFull = 32;
+
 template <int N2, int Z, int RM>
-__global__ void __launch_bounds__(NbGeom<N2, Z>::TPB, SST_NB_WARPS * 32 / NbGeom<N2, Z>::TPB) inv_nb_kernel(const InvArgs a) {
-    using Gm = NbGeom<N2, Z>;
+__global__ void __launch_bounds__(NbGeom<N2, Z, RM == kNbFull>::TPB,
+                                  ((RM == kNbFull ? 12 : SST_NB_WARPS) * 32 / NbGeom<N2, Z, RM == kNbFull>::TPB < 16
+                                       ? (RM == kNbFull ? 12 : SST_NB_WARPS) * 32 / NbGeom<N2, Z, RM == kNbFull>::TPB : 16))
+inv_nb_kernel(const InvArgs a) {
+    constexpr bool FULL = RM == kNbFull;
+    using Gm = NbGeom<N2, Z, FULL>;
     constexpr int N = Gm::N, J = Gm::J, TPB = Gm::TPB, KPC = Gm::KPC, CH = Gm::CH, S = Gm::S, OPL = Gm::OPL;
-    static_assert(RM >= 1 && RM <= 8 && N2 >= 8 && Z <= 8, "narrow-band geometry");
+    constexpr int TPT = Gm::TPT, RPC = Gm::RPC;
+    static_assert((FULL || (RM >= 1 && RM <= 8)) && N2 >= 8 && Z <= 8 && (TPB >= 32 || Z == 1), "narrow-band geometry");
     static_assert(!Gm::SKEW || (Z < 2 || Gm::o(0) >= 1) && (Z < 4 || Gm::o(1) > Gm::o(0)) &&
                                    (Z < 8 || Gm::o(2) > Gm::o(0) + Gm::o(1)) && Gm::SUPER > Gm::o(0) + (Z >= 4 ? Gm::o(1) : 0) + (Z >= 8 ? Gm::o(2) : 0),
                   "skew must be monotone");
@@ -79,7 +91,7 @@ __global__ void __launch_bounds__(NbGeom<N2, Z>::TPB, SST_NB_WARPS * 32 / NbGeom
     float* ring = reinterpret_cast<float*>(smem_raw + a.lay.ring_off);
     const int t = threadIdx.x;
     const int tq = t / Z;                     // stage 1: column j_lo = t = Z tq + (t % Z)
-    const int r2 = t / Z, b = t % Z;          // stage 2: row r2 of the chunk, residue b
+    const int b = t % Z;                      // stage 2: residue b of rows t / Z + (TPB / Z) it
 
     const int64_t F = a.frame_end - a.frame_begin;
     const int64_t f_lo = (int64_t)blockIdx.x * a.frames_per_cta;
@@ -129,27 +141,29 @@ __global__ void __launch_bounds__(NbGeom<N2, Z>::TPB, SST_NB_WARPS * 32 / NbGeom
     };
 
     const float2* pb = a.phz + b * (64 + 2 * N2);     // e(b col) | e(64 b k) | e(b (64 k - N))
-    // T rows of a pair are staged in shared memory (two buffers): one TMA bulk copy per row, issued a
-    // pair ahead and completed on the buffer's mbarrier; cooperative loads where the rows are not
-    // 16-byte aligned / sized (odd ldT or B)
+    // narrow band: T rows of a pair are staged in shared memory: one TMA bulk copy per row, issued a
+    // pair ahead (two buffers) or after the previous pair's last stage-1 read (one buffer), completed on
+    // the buffer's mbarrier; cooperative loads where the rows are not 16-byte aligned / sized
     const int Bp = (B + 2) & ~1;                          // row stride; entries [B, Bp) stay zero
     float2* tst = reinterpret_cast<float2*>(smem_raw + a.lay.g_off);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw + a.lay.g_off + SST_NB_TBUF * 2 * Bp * 8);
-    const bool bulk = ((reinterpret_cast<uintptr_t>(a.T) & 15) == 0) && (a.ldT % 2 == 0) && (B % 2 == 0);
+    const bool bulk = !FULL && ((reinterpret_cast<uintptr_t>(a.T) & 15) == 0) && (a.ldT % 2 == 0) && (B % 2 == 0);
     auto issue = [&](int64_t f, int sel) {                // thread 0: rows f, f + 1 (< f_hi) -> buffer sel
         const int nrows = (f + 1 < f_hi) ? 2 : 1;
         fence_proxy_async();
         mbar_arrive_tx(&mbar[sel], (uint32_t)(nrows * B * 8));
         for (int r = 0; r < nrows; ++r) bulk_g2s(tst + (2 * sel + r) * Bp, a.T + (f + r) * a.ldT, (uint32_t)(B * 8), &mbar[sel]);
     };
-    for (int i = t; i < 2 * SST_NB_TBUF * (Bp - B); i += TPB) tst[(i / (Bp - B)) * Bp + B + i % (Bp - B)] = make_float2(0.0f, 0.0f);
-    if (t == 0) {
-        mbar_init(&mbar[0], 1);
-        mbar_init(&mbar[1], 1);
-        fence_mbar_init();
+    if constexpr (!FULL) {
+        for (int i = t; i < 2 * SST_NB_TBUF * (Bp - B); i += TPB) tst[(i / (Bp - B)) * Bp + B + i % (Bp - B)] = make_float2(0.0f, 0.0f);
+        if (t == 0) {
+            mbar_init(&mbar[0], 1);
+            mbar_init(&mbar[1], 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+        if (bulk && t == 0) issue(f_lo, 0);
     }
-    __syncthreads();
-    if (bulk && t == 0) issue(f_lo, 0);
     uint32_t phase = 0;                                   // bit s = parity of buffer s's next completion
     int base0 = 0;                                        // slot of the pair's first sample sA - c
     for (int64_t f0 = f_lo; f0 < f_hi; f0 += 2, base0 = (base0 + 2 * (int)H) % Rr) {
@@ -157,7 +171,47 @@ __global__ void __launch_bounds__(NbGeom<N2, Z>::TPB, SST_NB_WARPS * 32 / NbGeom
         const int sel = SST_NB_TBUF == 2 ? (int)(((f0 - f_lo) >> 1) & 1) : 0;
         const float2* tA = tst + 2 * sel * Bp;
         const float2* tB = tA + Bp;
-        if (bulk) {
+        float2 vf[FULL ? 64 : 1];                         // full band: the column's 64 stage-1 outputs
+        if constexpr (FULL) {
+            {
+                // L2 prefetch of the next pair's T rows (their DRAM latency overlaps this pair)
+                const int64_t fn = f0 + 2;
+                const int nrows = (int)min((int64_t)2, f_hi - fn);
+                const int lines = (B * 8 + 127) >> 7;
+                for (int i = t; i < nrows * lines; i += TPB) {
+                    const int r = i / lines, q = i - r * lines;
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(a.T + (fn + r) * a.ldT) + q * 128));
+                }
+            }
+            // column j_lo = t: rows j_hi < 32 band (l = j = J j_hi + t), rows >= 32 mirror (l = z N - j);
+            // l = B (row 32, t = 0: the Nyquist bin, outside the half-open band) is zero.  Without a frame
+            // B the pair reads frame A twice: G = (1 + i) H_A, whose IDFT has real part y_A (H_A is
+            // Hermitian) and an imaginary part that is never added
+            const float2* TA = a.T + f0 * a.ldT;
+            const float2* TB = hasB ? TA + a.ldT : TA;
+#pragma unroll
+            for (int jh = 0; jh < 32; ++jh) {
+                SST_CHECK(J * jh + t < B);
+                float2 ta = __ldg(TA + J * jh + t), tb = __ldg(TB + J * jh + t);
+                if (jh == 0 && t == 0) { ta.y = 0.0f; tb.y = 0.0f; }         // DC (j = 0): real part only (R14)
+                vf[jh] = __fadd2_rn(ta, make_float2(-tb.y, tb.x));           // H_A + i H_B
+            }
+            {
+                const float2* pA = TA + B - t;                               // l = J (64 - j_hi) - t
+                const float2* pB = TB + B - t;
+#pragma unroll
+                for (int jh = 32; jh < 64; ++jh) {
+                    const int off = -J * (jh - 32);
+                    float2 ta = __ldg(pA + (jh == 32 ? (t ? 0 : -J) : off)), tb = __ldg(pB + (jh == 32 ? (t ? 0 : -J) : off));
+                    if (jh == 32 && t == 0) { ta = make_float2(0.0f, 0.0f); tb = ta; }   // l = B: none
+                    SST_CHECK(jh == 32 || (B - t + off >= 0 && B - t + off < B));
+                    vf[jh] = __fadd2_rn(make_float2(ta.x, tb.x), make_float2(tb.y, -ta.y));   // conj H_A + i conj H_B
+                }
+            }
+            Fft<64, +1>::run(vf);
+#pragma unroll
+            for (int tl = 1; tl < 64; ++tl) vf[tl] = cmulc(vf[tl], __ldg(a.tw + tl * N2 + tq));   // e^{i 2 pi tq tau_lo / N}
+        } else if (bulk) {
             if (SST_NB_TBUF == 2 && t == 0 && f0 + 2 < f_hi) issue(f0 + 2, sel ^ 1);
             mbar_wait(&mbar[sel], (phase >> sel) & 1);
             phase ^= 1u << sel;
@@ -169,25 +223,28 @@ __global__ void __launch_bounds__(NbGeom<N2, Z>::TPB, SST_NB_WARPS * 32 / NbGeom
             }
             __syncthreads();
         }
-        // ---- inputs of column j_lo = t: band rows j_hi < RM (G = T_A + i T_B at l = j - z k1) and
-        // mirror rows j_hi >= 64 - RM (G = conj T_A + i conj T_B at l = z N - j - z k1), read from the
-        // staged rows for every chunk so that they are not live across stage 2
+        // ---- narrow band, inputs of column j_lo = t: band rows j_hi < RM (G = T_A + i T_B at
+        // l = j - z k1) and mirror rows j_hi >= 64 - RM (G = conj T_A + i conj T_B at l = z N - j - z k1),
+        // read from the staged rows for every chunk so that they are not live across stage 2
         // (entries outside the band, and frame B of a last odd frame, read the zero at index B)
-        auto load_inputs = [&](float2 (&in)[2 * RM]) {
+        constexpr int NIN = FULL ? 1 : 2 * RM;
+        auto load_inputs = [&](float2 (&in)[NIN]) {
+            if constexpr (!FULL) {
 #pragma unroll
-            for (int i = 0; i < RM; ++i) {
-                const int l = J * i + t - Z * k1;
-                const bool ok = (unsigned)l < (unsigned)B;
-                float2 ta = tA[ok ? l : B], tb = tB[ok && hasB ? l : B];
-                if (i == 0 && t == 0) { ta.y = 0.0f; tb.y = 0.0f; }          // DC (j = 0): real part only (R14)
-                in[i] = __fadd2_rn(ta, make_float2(-tb.y, tb.x));            // H_A + i H_B
-            }
+                for (int i = 0; i < RM; ++i) {
+                    const int l = J * i + t - Z * k1;
+                    const bool ok = (unsigned)l < (unsigned)B;
+                    float2 ta = tA[ok ? l : B], tb = tB[ok && hasB ? l : B];
+                    if (i == 0 && t == 0) { ta.y = 0.0f; tb.y = 0.0f; }      // DC (j = 0): real part only (R14)
+                    in[i] = __fadd2_rn(ta, make_float2(-tb.y, tb.x));        // H_A + i H_B
+                }
 #pragma unroll
-            for (int i = 0; i < RM; ++i) {
-                const int l = J * (RM - i) - t - Z * k1;                      // j = J (64 - RM + i) + t
-                const bool ok = (unsigned)l < (unsigned)B;
-                const float2 ta = tA[ok ? l : B], tb = tB[ok && hasB ? l : B];
-                in[RM + i] = __fadd2_rn(make_float2(ta.x, tb.x), make_float2(tb.y, -ta.y));   // conj H_A + i conj H_B
+                for (int i = 0; i < RM; ++i) {
+                    const int l = J * (RM - i) - t - Z * k1;                  // j = J (64 - RM + i) + t
+                    const bool ok = (unsigned)l < (unsigned)B;
+                    const float2 ta = tA[ok ? l : B], tb = tB[ok && hasB ? l : B];
+                    in[RM + i] = __fadd2_rn(make_float2(ta.x, tb.x), make_float2(tb.y, -ta.y));   // conj H_A + i conj H_B
+                }
             }
         };
         const int64_t sA = (a.frame_begin + f0) * H;
@@ -195,127 +252,149 @@ __global__ void __launch_bounds__(NbGeom<N2, Z>::TPB, SST_NB_WARPS * 32 / NbGeom
 #pragma unroll
         for (int ch = 0; ch < CH; ++ch) {
             // ---- stage 1: rows tau_lo = k1' + 8 k2, k1' in [KPC ch, KPC ch + KPC) (compile time)
-            float2 in[2 * RM];
-            load_inputs(in);
+            if constexpr (FULL) {
 #pragma unroll
-            for (int kk = 0; kk < KPC; ++kk) {
-                const int k1p = KPC * ch + kk;
-                float2 v[8];
-#pragma unroll
-                for (int n2 = 0; n2 < 8; ++n2) {
-                    // nonzero inputs of the 8-point sum over n1: n1 = 0 (row n2 < RM), n1 = 7 (row 56 + n2 >= 64 - RM)
-                    float2 acc = make_float2(0.0f, 0.0f);
-                    bool any = false;
-                    if (n2 < RM) { acc = in[n2]; any = true; }
-                    if (n2 >= 8 - RM) {
-                        const float2 u = mul_w8<+1>(in[2 * RM + n2 - 8], 7 * k1p);
-                        acc = any ? cadd(acc, u) : u;
-                        any = true;
-                    }
-                    v[n2] = (n2 * k1p == 0 || !any) ? acc : cmul(acc, twiddle<64, +1>(n2 * k1p));
+                for (int r = 0; r < RPC; ++r) {
+                    const int tau_lo = KPC * ch + (r % KPC) + 8 * (r / KPC);
+                    buf[r * S + t] = vf[tau_lo];
                 }
-                Fft<8, +1>::run(v);
+            } else {
+                float2 in[NIN];
+                load_inputs(in);
 #pragma unroll
-                for (int k2 = 0; k2 < 8; ++k2) {
-                    const int tau_lo = k1p + 8 * k2;
-                    float2 y = v[k2];
-                    // e(j_lo tau_lo) = e^{i 2 pi tq tau_lo / N} e(b' tau_lo): the first factor here, the
-                    // second (constant per stage-2 item) with the output phase below
-                    if (tau_lo != 0) y = cmulc(y, __ldg(a.tw + tau_lo * N2 + tq));
-                    SST_CHECK((kk + KPC * k2) * S + t < N2 * S);
-                    buf[(kk + KPC * k2) * S + t] = y;
+                for (int kk = 0; kk < KPC; ++kk) {
+                    const int k1p = KPC * ch + kk;
+                    float2 v[8];
+#pragma unroll
+                    for (int n2 = 0; n2 < 8; ++n2) {
+                        // nonzero inputs of the 8-point sum over n1: n1 = 0 (row n2 < RM), n1 = 7 (row 56 + n2 >= 64 - RM)
+                        float2 acc = make_float2(0.0f, 0.0f);
+                        bool any = false;
+                        if (n2 < RM) { acc = in[n2]; any = true; }
+                        if (n2 >= 8 - RM) {
+                            const float2 u = mul_w8<+1>(in[2 * RM + n2 - 8], 7 * k1p);
+                            acc = any ? cadd(acc, u) : u;
+                            any = true;
+                        }
+                        v[n2] = (n2 * k1p == 0 || !any) ? acc : cmul(acc, twiddle<64, +1>(n2 * k1p));
+                    }
+                    Fft<8, +1>::run(v);
+#pragma unroll
+                    for (int k2 = 0; k2 < 8; ++k2) {
+                        const int tau_lo = k1p + 8 * k2;
+                        float2 y = v[k2];
+                        // e(j_lo tau_lo) = e^{i 2 pi tq tau_lo / N} e(b' tau_lo): the first factor here, the
+                        // second (constant per stage-2 item) with the output phase below
+                        if (tau_lo != 0) y = cmulc(y, __ldg(a.tw + tau_lo * N2 + tq));
+                        SST_CHECK((kk + KPC * k2) * S + t < RPC * S);
+                        buf[(kk + KPC * k2) * S + t] = y;
+                    }
                 }
             }
             __syncthreads();
             if (ch == 0) flush(sA - c);                                       // earlier pairs are complete
-            if (SST_NB_TBUF == 1 && ch == CH - 1 && bulk && t == 0 && f0 + 2 < f_hi) issue(f0 + 2, 0);   // inputs read
+            if (!FULL && SST_NB_TBUF == 1 && ch == CH - 1 && bulk && t == 0 && f0 + 2 < f_hi) issue(f0 + 2, 0);   // inputs read
 
-            // ---- stage 2: row r2 (tau_lo = KPC ch + r2 % KPC + 8 (r2 / KPC)), residue b
-            const int tau_lo = KPC * ch + (r2 % KPC) + 8 * (r2 / KPC);
-            float2 x[N2];
+            // ---- stage 2, task it: row r2 = t / Z + (TPB / Z) it (tau_lo = KPC ch + r2 % KPC + 8 (r2 / KPC)),
+            // residue b; frame A (real part) is overlap-added now, frame B (imaginary part, H samples
+            // later) after the barrier (chunks and pairs are ordered by the barriers)
+            float yb[TPT][OPL];
+            int sb0[TPT][2];
 #pragma unroll
-            for (int i = 0; i < N2; ++i) x[i] = buf[r2 * S + Z * i + b];
-            Fft<N2, +1>::run(x);
-            if constexpr (Z > 1) {
-                // output phase e(b tau) = e(b tau_lo) e(64 b k'), k' = k (k < N2/2) or k - N2: two runs of
-                // a recurrence in e(64 b) started from the table (<= N2/2 - 1 steps each)
-                const float2 cb = __ldg(pb + tau_lo);
-                const float2 step = __ldg(pb + 64 + 1);
-                float2 ph = cb;
-                float2 ph2 = cmul(cb, __ldg(pb + 64 + N2 + N2 / 2));
+            for (int it = 0; it < TPT; ++it) {
+                const int r2 = t / Z + (TPB / Z) * it;
+                const int tau_lo = KPC * ch + (r2 % KPC) + 8 * (r2 / KPC);
+                float2 x[N2];
 #pragma unroll
-                for (int k = 0; k < N2 / 2; ++k) {
-                    x[k] = cmul(x[k], ph);
-                    x[k + N2 / 2] = cmul(x[k + N2 / 2], ph2);
-                    if (k + 1 < N2 / 2) {
-                        ph = cmul(ph, step);
-                        ph2 = cmul(ph2, step);
+                for (int i = 0; i < N2; ++i) x[i] = buf[r2 * S + Z * i + b];
+                Fft<N2, +1>::run(x);
+                if constexpr (Z > 1) {
+                    // output phase e(b tau) = e(b tau_lo) e(64 b k'), k' = k (k < N2/2) or k - N2: two runs of
+                    // a recurrence in e(64 b) started from the table (<= N2/2 - 1 steps each)
+                    const float2 cb = __ldg(pb + tau_lo);
+                    const float2 step = __ldg(pb + 64 + 1);
+                    float2 ph = cb;
+                    float2 ph2 = cmul(cb, __ldg(pb + 64 + N2 + N2 / 2));
+#pragma unroll
+                    for (int k = 0; k < N2 / 2; ++k) {
+                        x[k] = cmul(x[k], ph);
+                        x[k + N2 / 2] = cmul(x[k + N2 / 2], ph2);
+                        if (k + 1 < N2 / 2) {
+                            ph = cmul(ph, step);
+                            ph2 = cmul(ph2, step);
+                        }
+                    }
+                    // reduce-scatter over the Z lanes of the row (bits of k from the top bit of b down): lane b
+                    // ends with outputs k = b + Z i in x[Z i]
+#pragma unroll
+                    for (int lvl = 0; lvl < Gm::LOGZ; ++lvl) {
+                        const int m = Z >> (lvl + 1);
+                        const bool up = (b & m) != 0;
+#pragma unroll
+                        for (int k = 0; k < N2; ++k) {
+                            if ((k & (Z - 1)) & ~(2 * m - 1)) continue;   // k's lower bits above m already reduced away
+                            if (k & m) continue;
+                            const float2 snd = up ? x[k] : x[k | m];
+                            const float2 kp = up ? x[k | m] : x[k];
+                            float2 rcv;
+                            rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, m);
+                            rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, m);
+                            x[k] = cadd(kp, rcv);
+                        }
                     }
                 }
-                // reduce-scatter over the Z lanes of the row (bits of k from the top bit of b down): lane b
-                // ends with outputs k = b + Z i in x[Z i]
+                // window g[tau + c] / N.  Output i of this lane: k = b + Z i, tau = tau_lo + 64 k - (k >= N2/2 ?
+                // N : 0).  OPL >= 2: two runs of consecutive slots 64 Z apart (i < OPL/2, i >= OPL/2), each
+                // addressed from its first slot (phys stride 64 Z + SUPER, minus Rp once the run wraps the
+                // ring); OPL = 1: one output, wrapped by the lane's b
+                constexpr int HALF = (OPL + 1) / 2;        // first output of the second run (tau < 0)
+                constexpr int DP = 64 * Z + Gm::SUPER;
+                const int u0 = tau_lo + 64 * b + c;        // tau + c of output 0 (before the wrap)
+                int pa0[2];
 #pragma unroll
-                for (int lvl = 0; lvl < Gm::LOGZ; ++lvl) {
-                    const int m = Z >> (lvl + 1);
-                    const bool up = (b & m) != 0;
-#pragma unroll
-                    for (int k = 0; k < N2; ++k) {
-                        if ((k & (Z - 1)) & ~(2 * m - 1)) continue;   // k's lower bits above m already reduced away
-                        if (k & m) continue;
-                        const float2 snd = up ? x[k] : x[k | m];
-                        const float2 kp = up ? x[k | m] : x[k];
-                        float2 rcv;
-                        rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, m);
-                        rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, m);
-                        x[k] = cadd(kp, rcv);
-                    }
+                for (int run = 0; run < (OPL > 1 ? 2 : 1); ++run) {
+                    const int i0 = run ? HALF : 0;
+                    const bool wrap = OPL > 1 ? (run == 1) : (b >= N2 / 2);
+                    int sl = base0 + u0 + 64 * Z * i0 - (wrap ? N : 0);
+                    if (sl >= Rr) sl -= Rr;
+                    sb0[it][run] = sl;
+                    pa0[run] = Gm::phys(sl);
                 }
-            }
-            // window g[tau + c] / N and overlap-add: frame A (real part) now, frame B (imaginary part,
-            // H samples later) after the barrier; chunks own disjoint slot classes mod 8 (hop % 8 == 0)
-            // output i of this lane: k = b + Z i, tau = tau_lo + 64 k (- N for i >= OPL/2): two runs of
-            // consecutive slots 64 Z apart, each addressed from its first slot (phys stride 64 Z + SUPER,
-            // minus Rp once the run wraps the ring)
-            constexpr int HALF = (OPL + 1) / 2;            // first output of the second run (tau < 0)
-            constexpr int DP = 64 * Z + Gm::SUPER;
-            const int u0 = tau_lo + 64 * b + c;            // tau + c of output 0
-            float yb[OPL];
-            int pb0[2], sb0[2];
 #pragma unroll
-            for (int run = 0; run < 2; ++run) {
-                const int i0 = run ? HALF : 0;
-                int sl = base0 + u0 + 64 * Z * i0 - (run ? N : 0);
-                if (sl >= Rr) sl -= Rr;
-                sb0[run] = sl;
-                pb0[run] = Gm::phys(sl);
-            }
-#pragma unroll
-            for (int i = 0; i < OPL; ++i) {
-                const int run = i >= HALF, di = i - (run ? HALF : 0);
-                const int u = u0 + 64 * Z * i - (run ? N : 0);   // tau + c in [0, L)
-                SST_CHECK(u >= 0 && u < a.L);
-                const float gw = __ldg(a.gwin + u);                        // g / N_f
-                const int p = pb0[run] + DP * di - (sb0[run] + 64 * Z * di >= Rr ? Rp : 0);
-                SST_CHECK(p == Gm::phys((sb0[run] + 64 * Z * di) % Rr));
-                const float2 yv = cscale(x[Z * i], gw);
-                ring[p] += yv.x;
-                yb[i] = yv.y;
+                for (int i = 0; i < OPL; ++i) {
+                    const int run = (OPL > 1 && i >= HALF) ? 1 : 0, di = i - (run ? HALF : 0);
+                    const bool wrap = OPL > 1 ? (run == 1) : (b >= N2 / 2);
+                    const int u = u0 + 64 * Z * i - (wrap ? N : 0);   // tau + c in [0, L)
+                    SST_CHECK(u >= 0 && u < a.L);
+                    const float gw = __ldg(a.gwin + u);                        // g / N_f
+                    const int s = sb0[it][run] + 64 * Z * di;
+                    const int p = pa0[run] + DP * di - (s >= Rr ? Rp : 0);
+                    SST_CHECK(p == Gm::phys(s % Rr));
+                    const float2 yv = cscale(x[Z * i], gw);
+                    ring[p] += yv.x;
+                    yb[it][i] = yv.y;
+                }
             }
             __syncthreads();
             if (hasB) {
 #pragma unroll
-                for (int run = 0; run < 2; ++run) {
-                    int sl = sb0[run] + (int)H;
-                    if (sl >= Rr) sl -= Rr;
-                    sb0[run] = sl;
-                    pb0[run] = Gm::phys(sl);
-                }
+                for (int it = 0; it < TPT; ++it) {
+                    constexpr int NRUN = OPL > 1 ? 2 : 1;
+                    int s0[NRUN], p0[NRUN];
 #pragma unroll
-                for (int i = 0; i < OPL; ++i) {
-                    const int run = i >= HALF, di = i - (run ? HALF : 0);
-                    const int p = pb0[run] + DP * di - (sb0[run] + 64 * Z * di >= Rr ? Rp : 0);
-                    SST_CHECK(p == Gm::phys((sb0[run] + 64 * Z * di) % Rr));
-                    ring[p] += yb[i];
+                    for (int run = 0; run < NRUN; ++run) {
+                        s0[run] = sb0[it][run] + (int)H;
+                        if (s0[run] >= Rr) s0[run] -= Rr;
+                        p0[run] = Gm::phys(s0[run]);
+                    }
+#pragma unroll
+                    for (int i = 0; i < OPL; ++i) {
+                        const int run = (OPL > 1 && i >= ((OPL + 1) / 2)) ? 1 : 0, di = i - (run ? ((OPL + 1) / 2) : 0);
+                        const int s = s0[run] + 64 * Z * di;
+                        const int p = p0[run] + (64 * Z + Gm::SUPER) * di - (s >= Rr ? Rp : 0);
+                        SST_CHECK(p == Gm::phys(s % Rr));
+                        ring[p] += yb[it][i];
+                    }
                 }
             }
         }
@@ -329,19 +408,24 @@ static cudaError_t launch_nb_b(const InvArgs& a, int grid, cudaStream_t s) {
     auto kern = inv_nb_kernel<N2, Z, RM>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, a.lay.total);
     if (e != cudaSuccess) return e;
-    kern<<<grid, NbGeom<N2, Z>::TPB, a.lay.total, s>>>(a);
+    kern<<<grid, NbGeom<N2, Z, RM == kNbFull>::TPB, a.lay.total, s>>>(a);
     return cudaGetLastError();
 }
 
 template <int N2, int Z>
 static cudaError_t launch_nb_z(const InvArgs& a, int grid, cudaStream_t s) {
-    if (inv_nb_rows(N2, a.k1, a.bins, a.zoom) <= 5) return launch_nb_b<N2, Z, 5>(a, grid, s);   // C2, C3
-    return launch_nb_b<N2, Z, 8>(a, grid, s);
+    if constexpr (N2 == 8) {
+        if constexpr (Z >= 4) return launch_nb_b<N2, Z, kNbFull>(a, grid, s);   // C5
+        return cudaErrorInvalidValue;
+    } else {
+        if (inv_nb_rows(N2, a.k1, a.bins, a.zoom) <= 5) return launch_nb_b<N2, Z, 5>(a, grid, s);   // C2, C3
+        return launch_nb_b<N2, Z, 8>(a, grid, s);
+    }
 }
 
 template <int N2>
 static cudaError_t launch_nb(const InvArgs& a, int grid, cudaStream_t s) {
-    if constexpr (N2 == 16 || N2 == 32) {
+    if constexpr (N2 == 8 || N2 == 16 || N2 == 32) {
         switch (a.zoom) {
             case 1: return launch_nb_z<N2, 1>(a, grid, s);
             case 2: return launch_nb_z<N2, 2>(a, grid, s);
@@ -354,18 +438,23 @@ static cudaError_t launch_nb(const InvArgs& a, int grid, cudaStream_t s) {
 
 template <int N2, int Z>
 static int occ_nb_z(int smem, int device) {
-    int nb = 0, sms = 0;
-    auto kern = inv_nb_kernel<N2, Z, 5>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NbGeom<N2, Z>::TPB, smem);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    return (nb > 0 ? nb : 1) * sms;
+    constexpr int RM = N2 == 8 ? kNbFull : 5;
+    if constexpr (N2 == 8 && Z < 4) {
+        return 0;
+    } else {
+        int nb = 0, sms = 0;
+        auto kern = inv_nb_kernel<N2, Z, RM>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NbGeom<N2, Z, RM == kNbFull>::TPB, smem);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        return (nb > 0 ? nb : 1) * sms;
+    }
 }
 
 template <int N2>
 static int occ_nb(int hop, int L, int zoom, int k1, int bins, int device) {
     if (!inv_nb_applicable(64 * N2, L, 64 * N2 / 2, hop, zoom, k1, bins)) return 0;
-    if constexpr (N2 == 16 || N2 == 32) {
+    if constexpr (N2 == 8 || N2 == 16 || N2 == 32) {
         const int smem = inv_nb_layout(N2, L, hop, zoom, bins).total;
         if (smem > 227 * 1024) return 0;
         switch (zoom) {

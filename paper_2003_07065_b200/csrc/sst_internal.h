@@ -75,33 +75,38 @@ __host__ __device__ inline InvLayout inv_layout(int n2, int L, int H, int zoom) 
 
 // narrow-band inverse (inv_nb_kernel.cuh): the z N_f-point band IDFT as 64 x J (J = z N2) with the
 // sum over residues inside the second stage (warp shuffles) instead of a shared-memory round trip.
-// Applies to full windows (L = N_f, c = N_f / 2), N_f in {1024, 2048}, z in {1, 2, 4, 8}, hop a
-// multiple of 8 (chunks of the 64 rows then own disjoint OLA slot classes mod 8) and a band whose
-// band/mirror rows fit 8 of the 64 rows (RM <= 8: C2, C3).
-// T staging buffers of the narrow-band inverse: 2 (the copy of pair p + 1 is issued when pair p starts)
+// Applies to full windows (L = N_f, c = N_f / 2) with
+//   narrow band: N_f in {1024, 2048}, z in {1, 2, 4, 8}, band/mirror rows within 8 of the 64 (C2, C3);
+//   full band:   N_f = 512, z in {4, 8}, k1 = 0 and B = z N_f / 2 (C5).
+// T staging buffers of the narrow-band form: 2 (the copy of pair p + 1 is issued when pair p starts)
 // or 1 (issued after pair p's last stage-1 read; half the shared footprint)
 #ifndef SST_NB_TBUF
 #define SST_NB_TBUF 1
 #endif
 __host__ __device__ inline int inv_nb_rows(int n2, int k1, int bins, int zoom) { return (k1 + bins / zoom + n2 - 1) / n2; }
+__host__ __device__ inline bool inv_nb_full(int nfft, int zoom, int k1, int bins) {
+    return nfft == 512 && (zoom == 4 || zoom == 8) && k1 == 0 && bins == zoom * nfft / 2;
+}
 __host__ __device__ inline bool inv_nb_applicable(int nfft, int L, int c, int hop, int zoom, int k1, int bins) {
     const int n2 = nfft / 64;
+    if (L != nfft || c != nfft / 2 || hop < 1 || hop > L) return false;
+    if (inv_nb_full(nfft, zoom, k1, bins)) return true;
     if (n2 != 16 && n2 != 32) return false;
-    if (L != nfft || c != nfft / 2 || hop < 8 || hop % 8 != 0 || hop > L) return false;
     if (zoom != 1 && zoom != 2 && zoom != 4 && zoom != 8) return false;
     return inv_nb_rows(n2, k1, bins, zoom) <= 8;
 }
-// [chunk buffer: N2 rows x (J + z) float2][OLA ring: ring = round_up(L + 3 hop, 64 z) slots (sample
-// index mod ring), stored bank-skewed (inv_nb_kernel.cuh: up to ring / (2 z) + 32 more floats)]
-// [T staging: 2 buffers x 2 rows x round_up(B + 1, 2) float2 (entry B: a zero)][2 mbarriers]
-// (g_off = T staging offset)
+// [chunk buffer: RPC rows (narrow: N2, full: 32) x (J + z) float2][OLA ring: ring = round_up(L + 3 hop,
+// 64 z) slots (sample index mod ring), stored bank-skewed (inv_nb_kernel.cuh: up to ring / (2 z) + 32
+// more floats)][narrow: T staging, SST_NB_TBUF buffers x 2 rows x round_up(B + 1, 2) float2 (entry B: a
+// zero), 2 mbarriers]   (g_off = T staging offset)
 __host__ __device__ inline InvLayout inv_nb_layout(int n2, int L, int H, int zoom, int bins) {
     InvLayout v{};
+    const bool full = inv_nb_full(64 * n2, zoom, 0, bins);
     v.pairs = 1;
-    v.ring_off = round_up(n2 * (zoom * n2 + zoom) * 8, 16);
+    v.ring_off = round_up((full ? 32 : n2) * (zoom * n2 + zoom) * 8, 16);
     v.ring = round_up(L + 3 * H, 64 * zoom);
     v.g_off = round_up(v.ring_off + (v.ring + (zoom > 1 ? v.ring / (2 * zoom) : 0) + 64) * 4, 16);
-    v.total = v.g_off + SST_NB_TBUF * 2 * round_up(bins + 1, 2) * 8 + 16;
+    v.total = full ? v.g_off : v.g_off + SST_NB_TBUF * 2 * round_up(bins + 1, 2) * 8 + 16;
     return v;
 }
 

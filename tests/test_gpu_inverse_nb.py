@@ -1,9 +1,11 @@
-"""Narrow-band inverse path (inv_nb_kernel.cuh, SST_IPATH_NARROWBAND): isolated parity against the
+"""Narrow-band inverse path (inv_nb_kernel.cuh, SST_IPATH_NARROWBAND, incl. its full-band form for C5's
+shape): isolated parity against the
 oracle's sst_inverse (Eq. 25-26, with P:L222's zero-padded z N_f IDFT) on seeded synthetic
 band planes from gen.planes (no SST arithmetic), at relative L2 <= 1e-4 (north star), plus agreement
 with the residue-split kernel (SST_IPATH_RESIDUE, forced by SST_INV_NB=0 at plan creation) on the
 same plane.  Cases cover both N_f instantiations (1024, 2048), z in {1, 2, 4, 8}, bands from DC and
-with k1 > 0, band/mirror row counts RM <= 5 and 6..8, hops that are multiples of 8, an odd frame
+with k1 > 0, band/mirror row counts RM <= 5 and 6..8, the full band (N_f = 512, z = 4, 8), hops
+8-40 and 3, 5, 12, an odd frame
 count (last pair without frame B), frame sub-ranges through sst_inverse_accumulate, and C2 / C3 at
 full size in the bench's launch configuration (sampled output windows of the whole record).
 """
@@ -43,6 +45,10 @@ NB = [
     (50000, 25600.0, 1024, 128.0, 16, 1024, 400.0, 3200.0, 4),     # N_f = 1024, z = 4, RM = 8
     (30000, 25600.0, 1024, 128.0, 40, 1024, 0.0, 1200.0, 8),       # N_f = 1024, z = 8, hop 40
     (20000, 25600.0, 1024, 128.0, 8, 1024, 100.0, 1500.0, 1),      # N_f = 1024, z = 1
+    (50000, 51200.0, 2048, 256.0, 12, 2048, 0.0, 4000.0, 4),       # hop 12 (not a multiple of 8)
+    (30000, 25600.0, 1024, 128.0, 5, 1024, 0.0, 2000.0, 2),        # hop 5
+    (40000, 25600.0, 512, 64.0, 4, 512, 0.0, 12800.0, 8),          # C5 shape: full band (k1 = 0, B = z N/2)
+    (30001, 25600.0, 512, 64.0, 3, 512, 0.0, 12800.0, 4),          # full band, z = 4, hop 3, odd N
 ]
 
 
