@@ -75,8 +75,8 @@ constexpr int kNbFull = 32;
 
 template <int N2, int Z, int RM>
 __global__ void __launch_bounds__(NbGeom<N2, Z, RM == kNbFull>::TPB,
-                                  ((RM == kNbFull ? 12 : SST_NB_WARPS) * 32 / NbGeom<N2, Z, RM == kNbFull>::TPB < 16
-                                       ? (RM == kNbFull ? 12 : SST_NB_WARPS) * 32 / NbGeom<N2, Z, RM == kNbFull>::TPB : 16))
+                                  ((RM == kNbFull ? (SST_NB_FULL_TMA ? 8 : 12) : SST_NB_WARPS) * 32 / NbGeom<N2, Z, RM == kNbFull>::TPB < 16
+                                       ? (RM == kNbFull ? (SST_NB_FULL_TMA ? 8 : 12) : SST_NB_WARPS) * 32 / NbGeom<N2, Z, RM == kNbFull>::TPB : 16))
 inv_nb_kernel(const InvArgs a) {
     constexpr bool FULL = RM == kNbFull;
     using Gm = NbGeom<N2, Z, FULL>;
@@ -146,8 +146,9 @@ inv_nb_kernel(const InvArgs a) {
     // the buffer's mbarrier; cooperative loads where the rows are not 16-byte aligned / sized
     const int Bp = (B + 2) & ~1;                          // row stride; entries [B, Bp) stay zero
     float2* tst = reinterpret_cast<float2*>(smem_raw + a.lay.g_off);
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw + a.lay.g_off + SST_NB_TBUF * 2 * Bp * 8);
-    const bool bulk = !FULL && ((reinterpret_cast<uintptr_t>(a.T) & 15) == 0) && (a.ldT % 2 == 0) && (B % 2 == 0);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw + a.lay.g_off + (FULL ? 1 : SST_NB_TBUF) * 2 * Bp * 8);
+    const bool bulk = (!FULL || SST_NB_FULL_TMA) && ((reinterpret_cast<uintptr_t>(a.T) & 15) == 0) && (a.ldT % 2 == 0) &&
+                      (B % 2 == 0);
     auto issue = [&](int64_t f, int sel) {                // thread 0: rows f, f + 1 (< f_hi) -> buffer sel
         const int nrows = (f + 1 < f_hi) ? 2 : 1;
         fence_proxy_async();
@@ -163,6 +164,13 @@ inv_nb_kernel(const InvArgs a) {
         }
         __syncthreads();
         if (bulk && t == 0) issue(f_lo, 0);
+    } else if constexpr (SST_NB_FULL_TMA) {
+        if (t == 0) {
+            mbar_init(&mbar[0], 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+        if (bulk && t == 0) issue(f_lo, 0);
     }
     uint32_t phase = 0;                                   // bit s = parity of buffer s's next completion
     int base0 = 0;                                        // slot of the pair's first sample sA - c
@@ -173,6 +181,28 @@ inv_nb_kernel(const InvArgs a) {
         const float2* tB = tA + Bp;
         float2 vf[FULL ? 64 : 1];                         // full band: the column's 64 stage-1 outputs
         if constexpr (FULL) {
+          if (bulk) {
+            // T rows staged by TMA (issued after the previous pair's inputs were read)
+            mbar_wait(&mbar[0], phase & 1);
+            phase ^= 1u;
+            const float2* sB = hasB ? tA + Bp : tA;
+#pragma unroll
+            for (int jh = 0; jh < 32; ++jh) {
+                float2 ta = tA[J * jh + t], tb = sB[J * jh + t];
+                if (jh == 0 && t == 0) { ta.y = 0.0f; tb.y = 0.0f; }         // DC (j = 0): real part only (R14)
+                vf[jh] = __fadd2_rn(ta, make_float2(-tb.y, tb.x));           // H_A + i H_B
+            }
+#pragma unroll
+            for (int jh = 32; jh < 64; ++jh) {
+                const int l = (jh == 32 && t == 0) ? B - J : J * (64 - jh) - t;
+                float2 ta = tA[l], tb = sB[l];
+                if (jh == 32 && t == 0) { ta = make_float2(0.0f, 0.0f); tb = ta; }   // l = B: none
+                vf[jh] = __fadd2_rn(make_float2(ta.x, tb.x), make_float2(tb.y, -ta.y));   // conj H_A + i conj H_B
+            }
+            Fft<64, +1>::run(vf);
+#pragma unroll
+            for (int tl = 1; tl < 64; ++tl) vf[tl] = cmulc(vf[tl], __ldg(a.tw + tl * N2 + tq));   // e^{i 2 pi tq tau_lo / N}
+          } else {
             {
                 // L2 prefetch of the next pair's T rows (their DRAM latency overlaps this pair)
                 const int64_t fn = f0 + 2;
@@ -211,6 +241,7 @@ inv_nb_kernel(const InvArgs a) {
             Fft<64, +1>::run(vf);
 #pragma unroll
             for (int tl = 1; tl < 64; ++tl) vf[tl] = cmulc(vf[tl], __ldg(a.tw + tl * N2 + tq));   // e^{i 2 pi tq tau_lo / N}
+          }
         } else if (bulk) {
             if (SST_NB_TBUF == 2 && t == 0 && f0 + 2 < f_hi) issue(f0 + 2, sel ^ 1);
             mbar_wait(&mbar[sel], (phase >> sel) & 1);
@@ -294,6 +325,7 @@ inv_nb_kernel(const InvArgs a) {
             __syncthreads();
             if (ch == 0) flush(sA - c);                                       // earlier pairs are complete
             if (!FULL && SST_NB_TBUF == 1 && ch == CH - 1 && bulk && t == 0 && f0 + 2 < f_hi) issue(f0 + 2, 0);   // inputs read
+            if (FULL && ch == 0 && bulk && t == 0 && f0 + 2 < f_hi) issue(f0 + 2, 0);                          // inputs read
 
             // ---- stage 2, task it: row r2 = t / Z + (TPB / Z) it (tau_lo = KPC ch + r2 % KPC + 8 (r2 / KPC)),
             // residue b; frame A (real part) is overlap-added now, frame B (imaginary part, H samples

@@ -83,6 +83,11 @@ __host__ __device__ inline InvLayout inv_layout(int n2, int L, int H, int zoom) 
 #ifndef SST_NB_TBUF
 #define SST_NB_TBUF 1
 #endif
+// full band: 1 = the pair's T rows staged by TMA (one buffer, issued after the previous pair's inputs
+// are read; C5 inverse 22.5 ms per 2^24 samples); 0 = loaded straight into registers (24.2 ms)
+#ifndef SST_NB_FULL_TMA
+#define SST_NB_FULL_TMA 1
+#endif
 __host__ __device__ inline int inv_nb_rows(int n2, int k1, int bins, int zoom) { return (k1 + bins / zoom + n2 - 1) / n2; }
 __host__ __device__ inline bool inv_nb_full(int nfft, int zoom, int k1, int bins) {
     return nfft == 512 && (zoom == 4 || zoom == 8) && k1 == 0 && bins == zoom * nfft / 2;
@@ -106,7 +111,8 @@ __host__ __device__ inline InvLayout inv_nb_layout(int n2, int L, int H, int zoo
     v.ring_off = round_up((full ? 32 : n2) * (zoom * n2 + zoom) * 8, 16);
     v.ring = round_up(L + 3 * H, 64 * zoom);
     v.g_off = round_up(v.ring_off + (v.ring + (zoom > 1 ? v.ring / (2 * zoom) : 0) + 64) * 4, 16);
-    v.total = full ? v.g_off : v.g_off + SST_NB_TBUF * 2 * round_up(bins + 1, 2) * 8 + 16;
+    v.total = full ? (SST_NB_FULL_TMA ? v.g_off + 2 * round_up(bins + 1, 2) * 8 + 16 : v.g_off)
+                   : v.g_off + SST_NB_TBUF * 2 * round_up(bins + 1, 2) * 8 + 16;
     return v;
 }
 
