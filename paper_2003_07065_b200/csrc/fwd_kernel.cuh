@@ -444,7 +444,11 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
             const int lane = threadIdx.x & 31;
             const int wib = (WPG > 1) ? (tg >> 5) : 0;     // warp within the group
             const int ebank = (N2 < 32) ? ((32 - ((lane / N2) * N2) % 32) % 32) & ~3 : 0;
-            int* acc = reinterpret_cast<int*>(buf) + ebank + wib * 4 * CH;   // planar [hi_re|lo_re|hi_im|lo_im][CH]
+            // planar [hi_re|lo_re|hi_im|lo_im][CH], or (IL: the dense bands of the BIG path, whose readout
+            // of CH bins per pass dominates the squeeze) interleaved [CH][hi_re, lo_re, hi_im, lo_im]: one
+            // 16-byte shared load per bin in the readout instead of four
+            constexpr bool IL = BIG && WPG == 1;
+            int* acc = reinterpret_cast<int*>(buf) + ebank + wib * 4 * CH;
             __shared__ float wscale[TPB / 32];
             float vmax = 0.0f;
 #pragma unroll
@@ -459,10 +463,16 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                 const int lc = min(CH, a.bins - l0);
                 {
                     int4* z4 = reinterpret_cast<int4*>(reinterpret_cast<int*>(buf) + ebank);
-                    const int lc4 = (lc + 3) >> 2;
+                    if constexpr (IL) {
+                        // (clearing on read in the readout instead, zeroing only before the first pass,
+                        // measured slower: C5 26.98 -> 28.59 ms per 2^24 samples)
+                        for (int i = tg; i < lc; i += N2) z4[i] = make_int4(0, 0, 0, 0);
+                    } else {
+                        const int lc4 = (lc + 3) >> 2;
 #pragma unroll
-                    for (int q = 0; q < 4 * WPG; ++q)
-                        for (int i = tg; i < lc4; i += N2) z4[q * (CH / 4) + i] = make_int4(0, 0, 0, 0);
+                        for (int q = 0; q < 4 * WPG; ++q)
+                            for (int i = tg; i < lc4; i += N2) z4[q * (CH / 4) + i] = make_int4(0, 0, 0, 0);
+                    }
                 }
                 group_sync<N2>(group);
 #pragma unroll
@@ -479,10 +489,12 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                         asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xr) : "f"(vr));
                         asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xi) : "f"(vi));
                         SST_CHECK(lr >= 0 && lr < CH && (int)(acc - reinterpret_cast<int*>(buf)) + 3 * CH + lr < 2 * CAP);
-                        atomicAdd(acc + lr, (int)(xr >> 20));
-                        atomicAdd(acc + CH + lr, (int)(xr & 0xFFFFF));
-                        atomicAdd(acc + 2 * CH + lr, (int)(xi >> 20));
-                        atomicAdd(acc + 3 * CH + lr, (int)(xi & 0xFFFFF));
+                        constexpr int PS = IL ? 1 : CH;                   // limb stride
+                        int* ab = acc + (IL ? 4 * lr : lr);
+                        atomicAdd(ab, (int)(xr >> 20));
+                        atomicAdd(ab + PS, (int)(xr & 0xFFFFF));
+                        atomicAdd(ab + 2 * PS, (int)(xi >> 20));
+                        atomicAdd(ab + 3 * PS, (int)(xi & 0xFFFFF));
                     }
                 }
                 group_sync<N2>(group);
@@ -501,6 +513,9 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                                 si += limbs_to_float(ah[2 * CH + i], ah[3 * CH + i], is);
                             }
                             t = make_float2(sr, si);
+                        } else if constexpr (IL) {
+                            const int4 v = reinterpret_cast<const int4*>(a0)[i];
+                            t = make_float2(limbs_to_float(v.x, v.y, iscale), limbs_to_float(v.z, v.w, iscale));
                         } else {
                             t = make_float2(limbs_to_float(a0[i], a0[CH + i], iscale),
                                             limbs_to_float(a0[2 * CH + i], a0[3 * CH + i], iscale));
