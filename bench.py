@@ -702,7 +702,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=8)
+    ap.add_argument("--e2e-chunks", type=int, default=4)
     ap.add_argument("--e2e-no-graph", action="store_true", help="launch the e2e round trip chunk by chunk")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--legs", default="C4,C5", help="extra fixed-record legs (strong scaling), 'none' for none")

@@ -43,5 +43,5 @@ if bench:
     f, i = bench["fwd_ms"], bench["inv_ms"]
     print(f"# bench run of the same build (no ncu): fwd {f:.3f} ms, inv {i:.3f} ms per step (CUDA events) -> "
           f"fwd share {100 * f / (f + i):.1f}%")
-print("## e2e leg (pipeline.RoundTrip: 8 frame chunks per step (CUDA graph replay), forward / inverse_accumulate / finalize per chunk)")
+print("## e2e leg (pipeline.RoundTrip: --e2e-chunks frame chunks per step (CUDA graph replay), forward / inverse_accumulate / finalize per chunk)")
 print("\n".join(table(e2e)))
