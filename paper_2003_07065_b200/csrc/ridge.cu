@@ -80,6 +80,26 @@ __device__ __forceinline__ void scan_thread(const double* V, int l, int a0, int 
     }
 }
 
+// smallest maximiser of V[a] - lam (l - a)^2 over a in [a0, a1] by one warp (lanes split the
+// range, then a warp argmax that keeps the smallest index on ties) -> opt[l]
+__device__ __forceinline__ void warp_scan(const double* V, int l, int a0, int a1, double lam, int lane, int* opt) {
+    double best = -INFINITY;
+    int arg = a0;
+    for (int a = a0 + lane; a <= a1; a += 32) {
+        const double v = ridge_cand(V, l, a, lam);
+        if (v > best) { best = v; arg = a; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+        if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
+    }
+    if (lane == 0) opt[l] = arg;
+}
+
+constexpr int kRidgeLong = 64;     // a thread-per-point level's ranges of at least this length go to the warp
+
 __global__ void __launch_bounds__(kRidgeThreads, 1)
 ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int suppress, const double* floor_in,
                 int32_t* back, int32_t* paths) {
@@ -106,36 +126,44 @@ ridge_dp_kernel(double* E, int64_t rows, int cols, double lam, int count, int su
             int32_t* bk = back + m * cols;
             for (int d = 0; d < levels; ++d) {
                 const int step = S >> (d + 1);                 // points p = step (2i + 1), p <= cols
-                const int npts = (cols >= step) ? ((cols - step) / (2 * step) + 1) : 0;
+                const int npts = (cols >= step) ? (((cols - step) >> (levels - d)) + 1) : 0;   // 2 step = 2^(levels-d)
                 if (npts <= NW) {
                     // one warp per point: lanes split the candidate range, then a warp argmax
                     for (int i = warp; i < npts; i += NW) {
                         const int p = step * (2 * i + 1), l = p - 1;
                         const int a0 = (p - step >= 1) ? opt[p - step - 1] : 0;
                         const int a1 = (p + step <= cols) ? opt[p + step - 1] : cols - 1;
-                        double best = -INFINITY;
-                        int arg = a0;
-                        for (int a = a0 + lane; a <= a1; a += 32) {
-                            const double v = ridge_cand(V, l, a, lam);
-                            if (v > best) { best = v; arg = a; }
-                        }
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) {
-                            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                            const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
-                            if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
-                        }
-                        if (lane == 0) opt[l] = arg;
+                        warp_scan(V, l, a0, a1, lam, lane, opt);
                     }
                 } else {
-                    for (int i = tid; i < npts; i += kRidgeThreads) {
+                    // one thread per point; the points of a warp whose candidate range is long (the
+                    // optimum jumps across it: two peaks of V, or lambda = 0 where the edge points
+                    // span [0, argmax] and [argmax, B)) are then scanned by the whole warp, one after
+                    // another, so no lane scans more than kRidgeLong candidates serially and no
+                    // extra CTA barrier is needed
+                    for (int i0 = tid - lane; i0 < npts; i0 += kRidgeThreads) {
+                        const int i = i0 + lane;
+                        const bool in = i < npts;
                         const int p = step * (2 * i + 1), l = p - 1;
-                        const int a0 = (p - step >= 1) ? opt[p - step - 1] : 0;
-                        const int a1 = (p + step <= cols) ? opt[p + step - 1] : cols - 1;
-                        double best;
-                        int arg;
-                        scan_thread(V, l, a0, a1, lam, best, arg);
-                        opt[l] = arg;
+                        int a0 = 0, a1 = -1;
+                        if (in) {
+                            a0 = (p - step >= 1) ? opt[p - step - 1] : 0;
+                            a1 = (p + step <= cols) ? opt[p + step - 1] : cols - 1;
+                        }
+                        const bool lng = a1 - a0 >= kRidgeLong;
+                        if (in && !lng) {
+                            double best;
+                            int arg;
+                            scan_thread(V, l, a0, a1, lam, best, arg);
+                            opt[l] = arg;
+                        }
+                        unsigned m = __ballot_sync(0xffffffffu, lng);
+                        while (m) {
+                            const int src = __ffs(m) - 1;
+                            m &= m - 1;
+                            warp_scan(V, __shfl_sync(0xffffffffu, l, src), __shfl_sync(0xffffffffu, a0, src),
+                                      __shfl_sync(0xffffffffu, a1, src), lam, lane, opt);
+                        }
                     }
                 }
                 __syncthreads();

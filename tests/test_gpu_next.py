@@ -141,10 +141,10 @@ def _oracle_ridges(To, lam, count, suppress=3):
 
 @pytest.mark.parametrize("hop,zoom,lam,count", [(2, 1, 0.01, 2), (4, 2, 0.05, 2), (1, 1, 0.0, 1), (2, 1, 1e-4, 2)])
 def test_ridge_dp_exact_on_identical_emissions(P, hop, zoom, lam, count):
-    """Reading R22's DP on the GPU (one CTA, fp64; per frame the windowed scan when the range of V
-    allows it, else the exact divide and conquer -- lambda = 0 and 1e-4 take the latter, 0.01 / 0.05
-    the former) fed the ORACLE's emissions E: paths identical to the oracle's O(F B^2) recurrence
-    on every frame, suppression included (same fp64 arithmetic, same lowest-bin ties)."""
+    """Reading R22's DP on the GPU (one CTA, fp64; per frame the exact divide and conquer over the
+    monotone smallest maximiser) fed the ORACLE's emissions E: paths identical to the oracle's
+    O(F B^2) recurrence on every frame, suppression included (same fp64 arithmetic, same lowest-bin
+    ties)."""
     plan, x, T, To, g, c = _two_tone_plan(P, hop=hop, zoom=zoom)
     Eo = O.ridge_emission(To)
     floor = float(np.log(1e-12 * np.abs(To).max()))
@@ -153,6 +153,40 @@ def test_ridge_dp_exact_on_identical_emissions(P, hop, zoom, lam, count):
     paths = plan.ridge(E, fl, lam, count, 3).cpu().numpy()
     po = _oracle_ridges(To, lam, count)
     assert np.array_equal(paths, po)
+
+
+@pytest.mark.parametrize("lam,count", [(1e-6, 2), (3e-6, 2), (1e-4, 1), (0.0, 1)])
+def test_ridge_dp_exact_jumping_optimum(P, lam, count):
+    """The DP at C1's band width (B = 2048) on seeded synthetic emissions whose optimum jumps
+    between two distant ridges of alternating strength (1400 bins apart, jump penalty lambda d^2
+    ~ 2-200): the divide and conquer then meets points whose candidate range spans the jump --
+    paths still identical to the oracle's O(F B^2) recurrence on every frame, suppression included."""
+    c1 = get_config("C1")
+    plan = P.Plan(c1.N, c1.fs, c1.L, c1.sigma, c1.hop, c1.nfft, c1.f1, c1.f2, c1.zoom, gamma=1e-3)
+    B = plan.bins
+    assert B >= 2048
+    F = 48
+    rng = np.random.default_rng(20260421)
+    Eo = rng.normal(0.0, 0.5, size=(F, B))
+    la = 300 + np.cumsum(rng.integers(-2, 3, size=F))              # two wandering ridges
+    lb = 1700 + np.cumsum(rng.integers(-2, 3, size=F))
+    sa = np.where(rng.random(F) < 0.5, 6.0, 3.0)                    # alternating strengths
+    Eo[np.arange(F), la] += sa
+    Eo[np.arange(F), lb] += 9.0 - sa
+    Eo[:, 1000:1010] += rng.normal(0.0, 0.1, size=(F, 10)) + 2.0     # a weak plateau between them
+    floor = float(Eo.min() - 5.0)
+    E = torch.from_numpy(np.ascontiguousarray(Eo)).to(DEV)
+    fl = torch.tensor(floor, dtype=torch.float64, device=DEV)
+    paths = plan.ridge(E, fl, lam, count, 3).cpu().numpy()
+    out, Ec = [], Eo.copy()
+    for _ in range(count):
+        p = O.ridge_dp(Ec, lam)
+        out.append(p)
+        Ec = O.ridge_suppress(Ec, p, 3, floor)
+    po = np.array(out)
+    assert np.array_equal(paths, po)
+    if lam <= 1e-6:                                                  # the optimum does jump
+        assert np.any(np.abs(np.diff(po[0])) > 1000)
 
 
 @pytest.mark.parametrize("hop,zoom,lam,count", [(2, 1, 0.01, 2), (4, 2, 0.05, 2), (1, 1, 0.0, 1)])
