@@ -189,6 +189,33 @@ def test_ridge_dp_exact_jumping_optimum(P, lam, count):
         assert np.any(np.abs(np.diff(po[0])) > 1000)
 
 
+@pytest.mark.parametrize("f2,zoom,rows,lam,count,kind", [
+    (1.0, 1, 5, 0.0, 1, "int"), (2.0, 1, 1, 1.0, 2, "int"), (3.0, 1, 7, 1.0, 3, "int"),
+    (11.0, 3, 40, 1.0, 2, "int"), (11.0, 3, 40, 0.0, 2, "int"), (25.0, 4, 64, 0.25, 3, "int"),
+    (25.0, 4, 2, 1e3, 1, "normal"), (32.0, 4, 33, 1e-3, 2, "normal"), (32.0, 4, 65, 0.0, 1, "normal")])
+def test_ridge_dp_edges_and_ties(P, f2, zoom, rows, lam, count, kind):
+    """Edge cases of the DP against the oracle's recurrence on seeded synthetic emissions: band
+    widths B = 1, 2, 3, 33, 100, 128 (not powers of two: ragged divide-and-conquer levels), one and
+    two frames, suppression wider than the band, and integer-valued emissions with an integer
+    lambda, where candidates tie EXACTLY (the smallest-bin rule of R22 decides) -- paths equal."""
+    plan = P.Plan(4096, 128.0, 128, 16.0, 4, 128, 0.0, f2, zoom, gamma=1e-3)
+    B = plan.bins
+    assert B == int(round(zoom * f2))
+    rng = np.random.default_rng(1000 * B + rows)
+    Eo = (rng.integers(0, 3, size=(rows, B)).astype(np.float64) if kind == "int"
+          else rng.normal(0.0, 1.0, size=(rows, B)))
+    floor = float(Eo.min() - 5.0)
+    E = torch.from_numpy(np.ascontiguousarray(Eo)).to(DEV)
+    fl = torch.tensor(floor, dtype=torch.float64, device=DEV)
+    paths = plan.ridge(E, fl, lam, count, 3).cpu().numpy()
+    out, Ec = [], Eo.copy()
+    for _ in range(count):
+        p = O.ridge_dp(Ec, lam)
+        out.append(p)
+        Ec = O.ridge_suppress(Ec, p, 3, floor)
+    assert np.array_equal(paths, np.array(out))
+
+
 @pytest.mark.parametrize("hop,zoom,lam,count", [(2, 1, 0.01, 2), (4, 2, 0.05, 2), (1, 1, 0.0, 1)])
 def test_ridge_paths_end_to_end(P, hop, zoom, lam, count):
     """End to end on the GPU (GPU plane -> GPU emissions -> GPU DP) vs the oracle end to end: the
