@@ -437,17 +437,23 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
             // v_max 2^-39), so the band value is bitwise reproducible.
             // N2 = 64: each of the frame's two warps squeezes into its own half of the group buffer.
             constexpr int WPG = (N2 > 32) ? N2 / 32 : 1;   // warps per group
-            // band bins per pass (4 int32 each); groups sharing a warp offset their planes by up to
-            // 28 ints so that the warp's 32-bit accesses spread over the banks
-            constexpr int CH = ((N2 < 32 ? 2 * CAP - 32 : 2 * CAP) / 4 / WPG) & ~3;
+            // planar [hi_re|lo_re|hi_im|lo_im][CH], or (IL: the dense bands of the BIG path, whose
+            // zeroing and readout of CH bins per pass bound it on the L1/shared pipe) interleaved
+            // [CH][re, im] with ONE int32 limb per component: at most K = N/2 + 1 <= 2^KB - 1 sources
+            // land on a target, so with |X| <= 2^QB, QB = 31 - KB, the int32 sum cannot overflow and
+            // is still exact and order-free (quantum v_max 2^-QB instead of 2^-39: C5 2^-22, far
+            // below the north star's 1e-3 relative L2); half the bytes of four limbs per bin
+            constexpr bool IL = BIG && WPG == 1;
+            constexpr int KB = ceil_log2_c(N / 2 + 2);     // 2^KB - 1 >= N/2 + 1
+            constexpr int QB = IL ? 31 - KB : 39;
+            constexpr int LPB = IL ? 2 : 4;                 // int32 limbs per bin
+            // band bins per pass; groups sharing a warp offset their planes by up to 28 ints so that
+            // the warp's 32-bit accesses spread over the banks
+            constexpr int CH = ((N2 < 32 ? 2 * CAP - 32 : 2 * CAP) / LPB / WPG) & ~3;
             static_assert(CH % 4 == 0 && CH > 0, "int4 zeroing");
             const int lane = threadIdx.x & 31;
             const int wib = (WPG > 1) ? (tg >> 5) : 0;     // warp within the group
             const int ebank = (N2 < 32) ? ((32 - ((lane / N2) * N2) % 32) % 32) & ~3 : 0;
-            // planar [hi_re|lo_re|hi_im|lo_im][CH], or (IL: the dense bands of the BIG path, whose readout
-            // of CH bins per pass dominates the squeeze) interleaved [CH][hi_re, lo_re, hi_im, lo_im]: one
-            // 16-byte shared load per bin in the readout instead of four
-            constexpr bool IL = BIG && WPG == 1;
             int* acc = reinterpret_cast<int*>(buf) + ebank + wib * 4 * CH;
             __shared__ float wscale[TPB / 32];
             float vmax = 0.0f;
@@ -456,8 +462,8 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                 if (bl[i] >= 0) vmax = fmaxf(vmax, fmaxf(fabsf(bsr[i]), fabsf(bsi[i])));
             const unsigned vb = __reduce_max_sync(0xffffffffu, __float_as_uint(vmax));
             const int ex = max(-87, (int)((vb >> 23) & 0xff) - 126);   // v_max < 2^ex
-            const float scale = __uint_as_float((unsigned)(127 + 39 - ex) << 23);
-            const float iscale = __uint_as_float((unsigned)(127 - 39 + ex) << 23);
+            const float scale = __uint_as_float((unsigned)(127 + QB - ex) << 23);
+            const float iscale = __uint_as_float((unsigned)(127 - QB + ex) << 23);
             if (WPG > 1 && lane == 0) wscale[threadIdx.x >> 5] = iscale;
             for (int l0 = 0; l0 < a.bins; l0 += CH) {
                 const int lc = min(CH, a.bins - l0);
@@ -466,7 +472,7 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                     if constexpr (IL) {
                         // (clearing on read in the readout instead, zeroing only before the first pass,
                         // measured slower: C5 26.98 -> 28.59 ms per 2^24 samples)
-                        for (int i = tg; i < lc; i += N2) z4[i] = make_int4(0, 0, 0, 0);
+                        for (int i = tg; i < (lc + 1) >> 1; i += N2) z4[i] = make_int4(0, 0, 0, 0);
                     } else {
                         const int lc4 = (lc + 3) >> 2;
 #pragma unroll
@@ -485,16 +491,23 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                     const float vr = bsr[i] * scale, vi = bsi[i] * scale;
                     if (in) {                                         // a6: T_acc[l] += S (Eq. 27/28)
                         // volatile: keep the conversions inside this rarely-taken branch
-                        long long xr, xi;
-                        asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xr) : "f"(vr));
-                        asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xi) : "f"(vi));
-                        SST_CHECK(lr >= 0 && lr < CH && (int)(acc - reinterpret_cast<int*>(buf)) + 3 * CH + lr < 2 * CAP);
-                        constexpr int PS = IL ? 1 : CH;                   // limb stride
-                        int* ab = acc + (IL ? 4 * lr : lr);
-                        atomicAdd(ab, (int)(xr >> 20));
-                        atomicAdd(ab + PS, (int)(xr & 0xFFFFF));
-                        atomicAdd(ab + 2 * PS, (int)(xi >> 20));
-                        atomicAdd(ab + 3 * PS, (int)(xi & 0xFFFFF));
+                        if constexpr (IL) {
+                            int xr, xi;
+                            asm volatile("cvt.rni.s32.f32 %0, %1;" : "=r"(xr) : "f"(vr));
+                            asm volatile("cvt.rni.s32.f32 %0, %1;" : "=r"(xi) : "f"(vi));
+                            SST_CHECK(lr >= 0 && lr < CH && (int)(acc - reinterpret_cast<int*>(buf)) + 2 * lr + 1 < 2 * CAP);
+                            atomicAdd(acc + 2 * lr, xr);
+                            atomicAdd(acc + 2 * lr + 1, xi);
+                        } else {
+                            long long xr, xi;
+                            asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xr) : "f"(vr));
+                            asm volatile("cvt.rni.s64.f32 %0, %1;" : "=l"(xi) : "f"(vi));
+                            SST_CHECK(lr >= 0 && lr < CH && (int)(acc - reinterpret_cast<int*>(buf)) + 3 * CH + lr < 2 * CAP);
+                            atomicAdd(acc + lr, (int)(xr >> 20));
+                            atomicAdd(acc + CH + lr, (int)(xr & 0xFFFFF));
+                            atomicAdd(acc + 2 * CH + lr, (int)(xi >> 20));
+                            atomicAdd(acc + 3 * CH + lr, (int)(xi & 0xFFFFF));
+                        }
                     }
                 }
                 group_sync<N2>(group);
@@ -514,8 +527,10 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
                             }
                             t = make_float2(sr, si);
                         } else if constexpr (IL) {
-                            const int4 v = reinterpret_cast<const int4*>(a0)[i];
-                            t = make_float2(limbs_to_float(v.x, v.y, iscale), limbs_to_float(v.z, v.w, iscale));
+                            // (two bins per lane with 16-byte loads and stores measured slower: C5
+                            // forward 21.37 -> 22.12 ms per 2^24 samples)
+                            const int2 v = reinterpret_cast<const int2*>(a0)[i];
+                            t = make_float2((float)v.x * iscale, (float)v.y * iscale);
                         } else {
                             t = make_float2(limbs_to_float(a0[i], a0[CH + i], iscale),
                                             limbs_to_float(a0[2 * CH + i], a0[3 * CH + i], iscale));

@@ -38,6 +38,7 @@ __host__ __device__ constexpr int groups_of(int n2, bool fwd) { return tpb_of(n2
 // a warp so consecutive groups start N2 float2 apart in the banks (conflict-free 64-bit half-warps)
 __host__ __device__ constexpr int cap_of(int n2) { return 64 * (n2 + 1) + (n2 < 16 ? n2 : 0); }
 __host__ __device__ constexpr int round_up(int v, int m) { return (v + m - 1) / m * m; }
+__host__ __device__ constexpr int ceil_log2_c(int v) { return v <= 1 ? 0 : 1 + ceil_log2_c((v + 1) / 2); }
 
 // forward dynamic shared memory: [G exchange buffers][taps L float2][2 input tiles][2 mbarriers]
 constexpr int kFwdStaticSmem = 1024;   // the forward's static shared memory (reductions, counters), bound
