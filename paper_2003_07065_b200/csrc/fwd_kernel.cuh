@@ -453,7 +453,9 @@ __global__ void __launch_bounds__(Geom<N2, true>::TPB, Geom<N2, true>::TPB == 25
             static_assert(CH % 4 == 0 && CH > 0, "int4 zeroing");
             const int lane = threadIdx.x & 31;
             const int wib = (WPG > 1) ? (tg >> 5) : 0;     // warp within the group
-            const int ebank = (N2 < 32) ? ((32 - ((lane / N2) * N2) % 32) % 32) & ~3 : 0;
+            // (IL: 8-byte bins; group buffers start CAP float2 = 16 banks (mod 32) apart, so the groups of a
+            // half-warp already read disjoint banks in the readout -- an offset would make them collide)
+            const int ebank = (N2 < 32 && !IL) ? ((32 - ((lane / N2) * N2) % 32) % 32) & ~3 : 0;
             int* acc = reinterpret_cast<int*>(buf) + ebank + wib * 4 * CH;
             __shared__ float wscale[TPB / 32];
             float vmax = 0.0f;
