@@ -8,12 +8,14 @@ rows = list(csv.reader(io.StringIO(out)))
 h, units = rows[0], rows[1]
 path = sys.argv[4] if len(sys.argv) > 4 else os.path.join(ROOT, "profiles", "traffic.json")
 t = json.load(open(path)) if os.path.exists(path) else {}
+seen = set()
 for r in rows[2:]:
     d = dict(zip(h, r))
     name = d["Kernel Name"]
     kern = "forward" if "fwd_kernel" in name else "inverse" if ("inv_kernel" in name or "inv_nb_kernel" in name) else None
-    if kern is None:
+    if kern is None or kern in seen:   # first launch per kernel: later ones are list-mode R23 repair launches
         continue
+    seen.add(kern)
     def mb(k):
         v = float(d[k]); u = units[h.index(k)]
         return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
