@@ -70,9 +70,6 @@ __global__ void finalize_kernel(float* y, int64_t y_off, int64_t y_len, InvArgs 
 }
 
 // ------------------------------------------------------------------------------- R23 ---------
-#ifndef SST_REDECIDE_PAIR
-#define SST_REDECIDE_PAIR 0
-#endif
 constexpr int kRedecideSplit = 8;   // CTAs per queue region (latency hiding: the per-bin sums are long)
 // Deferred fp64 re-decisions (reading R23): one warp per queued bin (frame within the launch, k, fp32
 // target), the direct Eq. 8 sum over the frame's samples in global memory, the oracle's decision in
@@ -105,30 +102,7 @@ __global__ void __launch_bounds__(256) redecide_kernel(const FwdArgs a, int mode
         double2 w = __ldg(a.tw64 + (((unsigned)k * (unsigned)(u - a.c)) & msk));   // W^{k (u - c)}
         const double2 st = __ldg(a.tw64 + ((8u * (unsigned)k) & msk));             // W^{8 k}
         double sr = 0.0, si = 0.0, dr = 0.0, di = 0.0;
-        // full windows (L = N_f, all of C2-C5): taps j and j + N_f/2 share their twiddle up to
-        // W^{k N_f/2} = (-1)^k, so the pair is combined before the complex product (6 instead of
-        // 10 fp64 operations per tap on this FP64-pipe-bound kernel)
-        const bool pair = SST_REDECIDE_PAIR && a.L == a.nfft;
-        if (ok && pair) {
-            const int h = a.L >> 1;
-            const double sg = (k & 1) ? -1.0 : 1.0;
-#pragma unroll 4
-            for (int j = u; j < h; j += 8) {
-                const int64_t sj = s0 + j, sj2 = sj + h;
-                const double x1 = (sj >= v_lo && sj < v_hi) ? (double)__ldg(a.x + (sj - a.x_off)) : 0.0;
-                const double x2 = (sj2 >= v_lo && sj2 < v_hi) ? sg * (double)__ldg(a.x + (sj2 - a.x_off)) : 0.0;
-                const double2 g1 = __ldg(a.taps64 + j);
-                const double2 g2 = __ldg(a.taps64 + j + h);
-                const double p = fma(x2, g2.x, x1 * g1.x), q = fma(x2, g2.y, x1 * g1.y);
-                sr = fma(p, w.x, sr);
-                si = fma(p, w.y, si);
-                dr = fma(q, w.x, dr);
-                di = fma(q, w.y, di);
-                const double wr = fma(w.x, st.x, -w.y * st.y);
-                w.y = fma(w.x, st.y, w.y * st.x);
-                w.x = wr;
-            }
-        } else if (ok) {
+        if (ok) {
 #pragma unroll 4
             for (int j = u; j < a.L; j += 8) {
                 const int64_t sj = s0 + j;
