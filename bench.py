@@ -627,7 +627,9 @@ def run_ours(args, cfg_base):
     inv_tf = inv_fl * nfr_rank / (inv_ms * 1e-3) / 1e12 if inv_ms > 0 else 0.0
     fwd_gbs = fwd_b * nfr_rank / (fwd_ms * 1e-3) / 1e9
     inv_gbs = inv_b * nfr_rank / (inv_ms * 1e-3) / 1e9 if inv_ms > 0 else 0.0
-    dom = "forward" if fwd_ms >= inv_ms else "inverse"
+    # the two calls tie within ~0.5 % on C3 (8.85 vs 8.83 ms): a tie (< 2 %) reports the forward, the
+    # one further from its roofline, so that the headline fraction does not flip from run to run
+    dom = "forward" if fwd_ms >= 0.98 * inv_ms else "inverse"
     ach = fwd_tf if dom == "forward" else inv_tf
     traffic = {"bytes": None, "source": "not measured (N > 1 or --no-traffic)"}
     roofline = {"bound": "alu", "kernel": f"sst_{dom}", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
